@@ -1,0 +1,187 @@
+"""Schedule execution on host buffers (test infrastructure; see oracle/__init__.py).
+
+Executes a TACCL-EF program the way PAPER.md:741–752 describes it: every rank runs its
+threadblocks' steps in order, a step waits for its dependencies, a send's chunks reach the
+matched receive on the peer, a receive "with optional reduction" combines them with a local
+source (sum; readings G4/G5), and a copy moves chunks locally
+(PAPER.md:768–769). The engine walks one topological order of the happens-before DAG
+(default: deterministic Kahn; tests pass every linear extension of tiny programs).
+
+Two value domains share the engine:
+* symbolic — AG/A2A tokens are chunk ids, AR tokens are (chunk index, contribution count
+  per rank); scratch and output start as BOTTOM; reading BOTTOM is an `uninit` error; the
+  final state is checked against the postcondition (App. B);
+* numeric — NumPy arrays, `c_e` elements per chunk; scratch and output
+  start poisoned with 0xA5 bytes (reading G11); sums: int32 wraps mod 2^32 (G13), float32 is
+  one IEEE binary32 round-to-nearest-even add, bfloat16 is the correctly rounded bf16 sum of
+  two bf16 values computed as fp32 add + RNE to bf16 (G6; pinned in tests against exact
+  rational arithmetic).
+"""
+from __future__ import annotations
+
+from collections import deque
+
+import numpy as np
+
+from .collectives import DTYPES, chunk_elems, postcondition, precondition
+from .ef import Program, ScheduleError
+from .validate import build_graph, check_structure, topo_order
+
+BOTTOM = None
+
+
+def _steps(prog: Program, graph, order):
+    for v in order:
+        r, t, k = graph.nodes[v]
+        tb = prog.gpus[r].tbs[t]
+        yield v, r, tb, tb.steps[k]
+
+
+def _execute(prog: Program, graph, order, bufs, read, write, reduce):
+    """Shared engine. bufs[r][buf] is a rank's buffer; read/write move cnt chunks."""
+    queues = {key: deque() for key in graph.conns}
+    for v, r, tb, st in _steps(prog, graph, order):
+        where = (r, tb.id, st.s)
+        if st.type == "cpy":
+            write(bufs[r][st.dstbuf], st.dstoff, st.cnt, read(bufs[r][st.srcbuf], st.srcoff, st.cnt, where))
+        elif st.type == "s":
+            queues[(r, tb.send, tb.chan)].append(read(bufs[r][st.srcbuf], st.srcoff, st.cnt, where))
+        elif st.type == "r":
+            write(bufs[r][st.dstbuf], st.dstoff, st.cnt, queues[(tb.recv, r, tb.chan)].popleft())
+        elif st.type == "rrc":
+            got = queues[(tb.recv, r, tb.chan)].popleft()
+            mine = read(bufs[r][st.srcbuf], st.srcoff, st.cnt, where)
+            write(bufs[r][st.dstbuf], st.dstoff, st.cnt, reduce(mine, got, where))
+        # nop: nothing moves
+
+
+def _prepare(prog, graph, order):
+    if graph is None:
+        errs = check_structure(prog)
+        if errs:
+            raise ScheduleError("structure", errs[0])
+        graph = build_graph(prog)
+    if order is None:
+        order = topo_order(graph)
+    return graph, order
+
+
+# ------------------------------------------------------------------------------ symbolic
+
+def run_symbolic(prog: Program, graph=None, order=None, check=True):
+    """Execute on chunk tokens; return per-rank output token lists. With check=True raise
+    ScheduleError('uninit' | 'postcondition') like the validator."""
+    graph, order = _prepare(prog, graph, order)
+    n, p = prog.nranks, prog.chunks_per_rank
+    pre = precondition(prog.coll, n, p)
+    bufs = []
+    for g in prog.gpus:
+        b = {"i": [BOTTOM] * g.i_chunks, "o": [BOTTOM] * g.o_chunks, "s": [BOTTOM] * g.s_chunks}
+        for k, tok in pre[g.id].items():
+            b["i"][k] = tok
+        bufs.append(b)
+
+    def read(buf, off, cnt, where):
+        vals = buf[off:off + cnt]
+        for q, x in enumerate(vals):
+            if x is BOTTOM:
+                raise ScheduleError("uninit", "rank %d tb%d:s%d reads chunk %d before any write"
+                                    % (where + (off + q,)))
+        return list(vals)
+
+    def write(buf, off, cnt, vals):
+        buf[off:off + cnt] = vals
+
+    def reduce(mine, got, where):
+        if prog.coll != "allreduce":
+            raise ScheduleError("structure", "rank %d tb%d:s%d reduces in a non-reducing "
+                                             "collective" % where)
+        out = []
+        for a, b in zip(mine, got):
+            if a[0] != b[0]:
+                raise ScheduleError("postcondition", "rank %d tb%d:s%d reduces chunk %d with "
+                                                     "chunk %d" % (where + (a[0], b[0])))
+            out.append((a[0], tuple(x + y for x, y in zip(a[1], b[1]))))
+        return out
+
+    _execute(prog, graph, order, bufs, read, write, reduce)
+    outs = [b["o"] for b in bufs]
+    if check:
+        post = postcondition(prog.coll, n, p)
+        for r in range(n):
+            for k, want in sorted(post[r].items()):
+                got = outs[r][k]
+                if got != want:
+                    raise ScheduleError("postcondition", _post_msg(prog.coll, r, k, want, got))
+    return outs
+
+
+def _post_msg(coll, r, k, want, got):
+    if coll != "allreduce":
+        return f"(chunk {want}, rank {r}) missing: o[{k}] holds {got!r}"
+    if got is BOTTOM:
+        return f"(chunk {k}, rank {r}) missing: o[{k}] never written"
+    missing = [s for s, c in enumerate(got[1]) if c == 0]
+    extra = [s for s, c in enumerate(got[1]) if c > 1]
+    return (f"(chunk {k}, rank {r}) reduction wrong: chunk {got[0]}, missing contributions "
+            f"from ranks {missing}, repeated from ranks {extra}")
+
+
+# ------------------------------------------------------------------------------ numeric
+
+def bf16_round(f32: np.ndarray) -> np.ndarray:
+    """float32 -> bfloat16 bits, round to nearest even; NaN stays a quiet NaN."""
+    bits = np.ascontiguousarray(f32, dtype=np.float32).view(np.uint32)
+    rounded = ((bits.astype(np.uint64) + 0x7FFF + ((bits >> 16) & 1)) >> 16).astype(np.uint16)
+    nan = np.isnan(f32)
+    if nan.any():
+        rounded[nan] = ((bits[nan] >> 16) | 0x0040).astype(np.uint16)
+    return rounded
+
+
+def bf16_to_f32(bits: np.ndarray) -> np.ndarray:
+    return (bits.astype(np.uint32) << 16).view(np.float32)
+
+
+def add(a: np.ndarray, b: np.ndarray, dtype: str) -> np.ndarray:
+    """One reduction step dst = src + received in the schedule's dtype."""
+    if dtype == "int32":
+        return (a.view(np.uint32) + b.view(np.uint32)).view(np.int32)
+    if dtype == "float32":
+        with np.errstate(over="ignore", invalid="ignore"):
+            return (a + b).astype(np.float32)
+    if dtype == "bfloat16":
+        with np.errstate(over="ignore", invalid="ignore"):
+            return bf16_round(bf16_to_f32(a) + bf16_to_f32(b))
+    raise ValueError(dtype)
+
+
+def run(prog: Program, inputs, dtype: str, graph=None, order=None):
+    """Numeric execution. inputs: one 1-D array per rank (dtype storage per DTYPES, bf16 as
+    uint16 bits). Returns the per-rank output arrays."""
+    graph, order = _prepare(prog, graph, order)
+    n, p = prog.nranks, prog.chunks_per_rank
+    np_dt, _ = DTYPES[dtype]
+    e_in = inputs[0].size
+    count = e_in // n if prog.coll == "alltoall" else e_in
+    ce = chunk_elems(prog.coll, n, p, count)
+    bufs = []
+    for g in prog.gpus:
+        x = np.ascontiguousarray(inputs[g.id], dtype=np_dt)
+        if x.size != g.i_chunks * ce:
+            raise ValueError(f"rank {g.id}: input has {x.size} elements, want {g.i_chunks * ce}")
+        o = np.full(g.o_chunks * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
+        s = np.full(g.s_chunks * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
+        bufs.append({"i": x, "o": o, "s": s})
+
+    def read(buf, off, cnt, where):
+        return buf[off * ce:(off + cnt) * ce].copy()
+
+    def write(buf, off, cnt, vals):
+        buf[off * ce:(off + cnt) * ce] = vals
+
+    def reduce(mine, got, where):
+        return add(mine, got, dtype)
+
+    _execute(prog, graph, order, bufs, read, write, reduce)
+    return [b["o"] for b in bufs]

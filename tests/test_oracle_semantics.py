@@ -1,0 +1,116 @@
+"""Oracle pins that hold for any schedule: determinism over every linearisation (brute force
+on tiny programs), symbolic/numeric agreement, and the instance invariant.
+Programs come from tests/golden and from the product's generator (its text is an input here;
+the oracle checks it against the collective's definition)."""
+import functools
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.validate import build_graph, topo_order
+from conftest import golden
+
+
+def linear_extensions(graph, limit):
+    """All topological orders (DFS), or None if there are more than `limit`."""
+    n = len(graph.nodes)
+    pred_mask = [0] * n
+    for u, vs in enumerate(graph.succ):
+        for v in vs:
+            pred_mask[v] |= 1 << u
+
+    @functools.lru_cache(maxsize=None)
+    def count(done):
+        if done == (1 << n) - 1:
+            return 1
+        return sum(count(done | (1 << v)) for v in range(n)
+                   if not (done >> v) & 1 and (pred_mask[v] & ~done) == 0)
+
+    total = count(0)
+    if total > limit:
+        return None, total
+    out = []
+
+    def rec(done, order):
+        if len(order) == n:
+            out.append(list(order))
+            return
+        for v in range(n):
+            if not (done >> v) & 1 and (pred_mask[v] & ~done) == 0:
+                order.append(v)
+                rec(done | (1 << v), order)
+                order.pop()
+    rec(0, [])
+    return out, total
+
+
+def _inputs(prog, count, dtype, seed):
+    rng = np.random.default_rng(seed)
+    n = prog.nranks
+    e_in = n * count if prog.coll == "alltoall" else count
+    if dtype == "int32":
+        return [rng.integers(-2**31, 2**31, e_in, dtype=np.int64).astype(np.int32) for _ in range(n)]
+    return [rng.integers(0, 1 << 16, e_in).astype(np.uint16) for _ in range(n)]
+
+
+def _check_all_orders(prog, count, dtype, limit=100000):
+    graph = build_graph(prog)
+    orders, total = linear_extensions(graph, limit)
+    assert orders is not None, f"{total} linear extensions"
+    ins = _inputs(prog, count, dtype, 11)
+    ref = oracle.run(prog, ins, dtype, graph=graph, order=topo_order(graph))
+    sym_ref = oracle.run_symbolic(prog, graph=graph, order=topo_order(graph))
+    for order in orders:
+        outs = oracle.run(prog, ins, dtype, graph=graph, order=order)
+        assert all(np.array_equal(a, b) for a, b in zip(outs, ref))
+        assert oracle.run_symbolic(prog, graph=graph, order=order) == sym_ref
+    return total
+
+
+def test_all_linearisations_c1():
+    total = _check_all_orders(oracle.parse(golden("c1_ag_ring_n2_p2.xml")), 8, "int32")
+    assert total > 1
+
+
+def test_all_linearisations_gar():
+    total = _check_all_orders(oracle.parse(golden("ar_rsag_n2_p1.xml")), 6, "int32")
+    assert total > 1
+
+
+def test_allgather_output_matches_definition_on_golden():
+    prog = oracle.parse(golden("c1_ag_ring_n2_p2.xml"))
+    ins = _inputs(prog, 10, "bfloat16", 12)
+    outs = oracle.run(prog, ins, "bfloat16")
+    want = oracle.expected_outputs("allgather", ins, "bfloat16")
+    assert all(np.array_equal(a, b) for a, b in zip(outs, want))
+
+
+def test_symbolic_numeric_agree_on_chunk_id_encoding():
+    # numeric run with every element = chunk id * 1000 + offset decodes to the symbolic tokens
+    prog = oracle.parse(golden("c1_ag_ring_n2_p2.xml"))
+    ce = 7
+    ins = [np.array([(r * 2 + k) * 1000 + e for k in range(2) for e in range(ce)], np.int32)
+           for r in range(2)]
+    outs = oracle.run(prog, ins, "int32")
+    sym = oracle.run_symbolic(prog)
+    for o, s in zip(outs, sym):
+        for k, tok in enumerate(s):
+            assert (o[k * ce:(k + 1) * ce] // 1000 == tok).all()
+
+
+def test_instance_expansion_invariant_on_golden():
+    for f, dtype, count in (("c1_ag_ring_n2_p2.xml", "int32", 24), ("ar_rsag_n2_p1.xml", "int32", 24)):
+        prog = oracle.parse(golden(f))
+        for m in (2, 3, 4):
+            prog.instances = m
+            exp = oracle.expand_instances(prog)
+            assert exp.instances == 1 and exp.chunks_per_rank == prog.chunks_per_rank * m
+            assert sum(len(t.steps) > 0 for t in exp.gpus[0].tbs) == m * sum(
+                len(t.steps) > 0 for t in prog.gpus[0].tbs)
+            assert oracle.validate(exp).ok
+            ins = _inputs(prog, count, dtype, 13)
+            a = oracle.run(prog, ins, dtype)
+            b = oracle.run(exp, ins, dtype)
+            assert all(np.array_equal(x, y) for x, y in zip(a, b))
