@@ -1,0 +1,154 @@
+/*
+ * taccl.h — C ABI of the B200 executor for TACCL-EF chunk schedules (arXiv 2111.04867).
+ *
+ * The library runs synthesized collective algorithms (Allgather, Alltoall, Allreduce):
+ * every GPU executes per-threadblock programs of send / recv / recvReduceCopy / copy steps
+ * over chunk indices with cross-step dependencies, the paper's runtime model
+ * (§6.1), in ONE kernel launch per collective call. Bytes
+ * move by direct loads/stores into peer HBM over NVLink/NVSwitch (CUDA IPC mappings); no
+ * NCCL call is on the path. Schedule syntax: docs/SCHEDULE.md (EF v1).
+ *
+ * Threading: one communicator per process (global state). Calls are not thread-safe. As in
+ * NCCL, every rank must issue the same sequence of collective calls on one stream.
+ *
+ * Errors: every call returns taccl_result_t. On failure taccl_last_error() returns a
+ * thread-local message naming the failing check (e.g. "postcondition: (chunk 5, rank 3)
+ * missing"). Device-side failures (a spin wait that exceeded TACCL_TIMEOUT_S seconds) are
+ * recorded in the communicator's error word and surface from taccl_check() as
+ * TACCL_ERR_TIMEOUT; the communicator must then be destroyed.
+ */
+#ifndef TACCL_H
+#define TACCL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TACCL_SUCCESS = 0,
+  TACCL_ERR_INVALID_ARG = 1,      /* bad pointer/size/count, count not divisible into chunks */
+  TACCL_ERR_INVALID_SCHEDULE = 2, /* schedule failed a check (last_error names it)          */
+  TACCL_ERR_NO_ALGO = 3,          /* no loaded algorithm matches (coll, nranks, bytes)        */
+  TACCL_ERR_CUDA = 4,             /* a CUDA runtime call failed (last_error has the string)   */
+  TACCL_ERR_UNSUPPORTED = 5,      /* e.g. in-place call, too many ranks/threadblocks          */
+  TACCL_ERR_TIMEOUT = 6,          /* device watchdog fired (see taccl_check)                  */
+  TACCL_ERR_NOT_INITIALIZED = 7,  /* no communicator, or peers not set                        */
+  TACCL_ERR_NOT_REGISTERED = 8    /* buffer not registered with taccl_register_buffer         */
+} taccl_result_t;
+
+typedef enum { TACCL_ALLGATHER = 0, TACCL_ALLTOALL = 1, TACCL_ALLREDUCE = 2 } taccl_coll_t;
+
+/* Element types. AG/A2A move raw bytes (dtype only sets the element size); AR sums:
+ * INT32 wraps mod 2^32, FLOAT32 is IEEE binary32 round-to-nearest-even, BFLOAT16
+ * accumulates in fp32 and rounds to nearest even once per reduction (chains of rrc into one
+ * destination are fused). */
+typedef enum { TACCL_INT32 = 0, TACCL_FLOAT32 = 1, TACCL_BFLOAT16 = 2 } taccl_dtype_t;
+
+typedef struct taccl_algo* taccl_algo_t;
+
+/* Hard limits of this build (taccl_load_algo rejects larger programs with UNSUPPORTED). */
+#define TACCL_MAX_RANKS 8    /* one NVSwitch domain of 8 B200s                        */
+#define TACCL_MAX_CHAN 16    /* channels per (peer, direction)                         */
+#define TACCL_MAX_SPLIT 128  /* instances x lanes per threadblock                      */
+#define TACCL_MAX_TB 64      /* threadblocks per rank in one schedule                  */
+#define TACCL_HANDLE_BYTES 128 /* size of one exported handle blob                     */
+
+/* ---- diagnostics ----------------------------------------------------------------------- */
+
+/* Message for the last failing call on this thread ("" if none). Never NULL. */
+const char* taccl_last_error(void);
+
+/* Non-blocking check of the device error word; TACCL_ERR_TIMEOUT if a watchdog fired. */
+taccl_result_t taccl_check(void);
+
+/* ---- schedule checks (host only; usable without a GPU) -------------------------------- */
+
+/* Parse and check EF v1 text (docs/SCHEDULE.md) in the documented order: syntax,
+ * structure, match, cycle, race (direct_store != 0: the executor's single-assignment rule;
+ * 0: queue semantics), uninit, postcondition (collective pre/postcondition over chunks,
+ * App. B). `text` need not be NUL-terminated; it is not retained.
+ * Returns SUCCESS or INVALID_SCHEDULE; last_error is "<class>: <message>". */
+taccl_result_t taccl_validate(const char* text, size_t len, int direct_store);
+
+/* ---- communicator (one per process) ---------------------------------------------------- */
+
+/* One rank per process on `cuda_device`. Allocates the rank's arena in device memory:
+ * flags plus `scratch_bytes` of scratch/staging (0 = default 256 MiB, env
+ * TACCL_SCRATCH_BYTES overrides). Peers are unusable until taccl_comm_set_peers. */
+taccl_result_t taccl_comm_init(int rank, int nranks, int cuda_device, size_t scratch_bytes);
+
+/* All `nranks` ranks emulated in this process on one device (tests and single-GPU runs of
+ * multi-rank schedules): one launch runs every rank's threadblocks, peers are the other
+ * ranks' arenas in the same HBM. Use taccl_run_emulated. */
+taccl_result_t taccl_comm_init_emulated(int nranks, int cuda_device, size_t scratch_bytes);
+
+/* Writes this rank's arena IPC handle blob (TACCL_HANDLE_BYTES) to `out`; *len = size. */
+taccl_result_t taccl_comm_export_handle(void* out, size_t* len);
+
+/* `all_handles` = nranks blobs of `len_each` bytes in rank order (from an all-gather of
+ * taccl_comm_export_handle). Opens the peers' arenas. */
+taccl_result_t taccl_comm_set_peers(const void* all_handles, size_t len_each);
+
+/* Frees algorithms, buffers registrations, peer mappings and the arena. */
+taccl_result_t taccl_comm_destroy(void);
+
+/* ---- user buffer registration (zero-copy direct stores) -------------------------------- */
+
+/* Collective, like NCCL window registration: every rank registers its own buffer of the
+ * same role in the same order. Step 1: export a blob for [ptr, ptr+bytes) (any pointer
+ * inside a cudaMalloc'd allocation). Step 2: pass all ranks' blobs (rank order) to
+ * taccl_register_buffer. Afterwards a taccl_run whose recvbuf lies inside [ptr, ptr+bytes)
+ * stores into the peers' registered buffers at the same offset. */
+taccl_result_t taccl_buffer_export(const void* ptr, size_t bytes, void* out, size_t* len);
+taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* all_blobs,
+                                     size_t len_each);
+
+/* ---- north-star calls ------------------------------------------------------------------ */
+
+/* Parse, check (direct-store mode) and upload a schedule. The algorithm is registered
+ * under (coll, nranks, [minBytes, maxBytes)) for selection by taccl_run; `*out` may be
+ * NULL. The text is copied. Requires an initialized communicator with matching nranks. */
+taccl_result_t taccl_load_algo(const char* schedule_text, size_t len, taccl_algo_t* out);
+
+/* Run the collective with the loaded algorithm selected by (coll, nranks, S) where S =
+ * output bytes (AG), per-rank send bytes (A2A), buffer bytes (AR). NCCL count convention:
+ * AG count = elements per rank (recvbuf holds nranks*count), A2A count = elements per
+ * peer (both buffers hold nranks*count), AR count = total elements. sendbuf/recvbuf are
+ * device pointers; recvbuf must be registered (taccl_register_buffer) unless emulated.
+ * Out-of-place only (in-place -> UNSUPPORTED). Enqueues ONE kernel on `stream`
+ * (a cudaStream_t; NULL = legacy default stream); returns without synchronizing. The
+ * call is CUDA-graph capturable (epochs live on the device). */
+taccl_result_t taccl_run(taccl_coll_t coll, const void* sendbuf, void* recvbuf, size_t count,
+                         taccl_dtype_t dtype, void* stream);
+
+/* Emulated communicator: sendbufs[r]/recvbufs[r] are rank r's device buffers. */
+taccl_result_t taccl_run_emulated(taccl_coll_t coll, const void* const* sendbufs,
+                                  void* const* recvbufs, size_t count, taccl_dtype_t dtype,
+                                  void* stream);
+
+/* Same as taccl_run with HOST buffers: copies sendbuf H2D, runs, copies recvbuf D2H on
+ * `stream` through library-owned device buffers, and synchronizes the stream. For
+ * end-to-end measurements; pinned host memory gives full PCIe bandwidth. */
+taccl_result_t taccl_run_host(taccl_coll_t coll, const void* host_sendbuf, void* host_recvbuf,
+                              size_t count, taccl_dtype_t dtype, void* stream);
+
+/* Unregister and free an algorithm (invalid while a run using it is in flight). */
+taccl_result_t taccl_free(taccl_algo_t algo);
+
+/* ---- introspection (tests, bench) ----------------------------------------------------- */
+
+/* Launch geometry taccl_run would use: CTAs of the single launch and split factor
+ * (instances x lanes). */
+taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dtype,
+                               int* ctas, int* split, int* threads);
+
+/* Number of executor kernel launches issued by this process so far. */
+uint64_t taccl_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TACCL_H */

@@ -1,0 +1,384 @@
+// sm_100a executor for TACCL-EF programs: one launch runs every threadblock program of the
+// local rank(s) ("execute the entire algorithm in a single kernel launch").
+//
+// Grid: for each local rank, ntb x split CTAs; CTA (t, j) runs threadblock t's steps on
+// piece j of every chunk it touches (split = instances x lanes; instance semantics
+// subchunk j of every chunk follows the parent's path). Steps run in
+// program order and wait on their dependencies.
+//
+// Data path (no NCCL): a send stores the piece straight into the matched receive's
+// destination in the peer's HBM (peer pointers come from CUDA IPC mappings, NVLink 5 /
+// NVSwitch) — the user's output buffer or scratch for `r`, a library staging slot for
+// `rrc` — with 16-byte vector loads/stores; then one thread publishes a per-(connection,
+// piece) sequence flag with a system-scope release. A receive acquires that flag. An `rrc`
+// then reduces src + staged bytes locally (fused reduce-on-receive; chains of rrc into one
+// destination are fused into one multi-input pass, K_RRC_FUSED).
+// Buffer reuse across calls: each receiving CTA first writes "entered epoch e" into its
+// sender's arena; a sender's first store of the call waits for it.
+// Epochs live in device memory (incremented by the rank's last CTA), so launches are
+// CUDA-graph capturable. Every spin wait has a %globaltimer watchdog.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "taccl_internal.h"
+
+namespace taccl {
+namespace {
+
+using u64 = unsigned long long;
+
+__device__ __forceinline__ u64 ld_acquire_sys(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 ld_acquire_gpu(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(u64* p, u64 v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 globaltimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int4 ld_cg(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_v4(int4* p, int4 v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Wait until *p >= target. sys: the writer is another GPU (or may be). Returns false on timeout.
+template <bool SYS>
+__device__ bool wait_ge(const u64* p, u64 target, u64 timeout_ns) {
+  if ((SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= target) return true;
+  const u64 t0 = globaltimer();
+  for (;;) {
+    for (int i = 0; i < 256; ++i)
+      if ((SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= target) return true;
+    if (globaltimer() - t0 > timeout_ns) return false;
+  }
+}
+
+// ---------------------------------------------------------------- CTA-wide data movement
+constexpr int kUnroll = 8;
+
+__device__ void cta_copy(char* __restrict__ dst, const char* __restrict__ src, int64_t n) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const int64_t nv = n >> 4;
+    const int4* s = reinterpret_cast<const int4*>(src);
+    int4* d = reinterpret_cast<int4*>(dst);
+    int64_t i = tid;
+    for (; i + (int64_t)(kUnroll - 1) * nt < nv; i += (int64_t)kUnroll * nt) {
+      int4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) v[u] = ld_cg(s + i + (int64_t)u * nt);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) st_v4(d + i + (int64_t)u * nt, v[u]);
+    }
+    for (; i < nv; i += nt) st_v4(d + i, ld_cg(s + i));
+    for (int64_t b = (nv << 4) + tid; b < n; b += nt) dst[b] = src[b];
+  } else if ((((uintptr_t)dst | (uintptr_t)src) & 3) == 0) {
+    const int64_t nw = n >> 2;
+    const int* s = reinterpret_cast<const int*>(src);
+    int* d = reinterpret_cast<int*>(dst);
+    for (int64_t i = tid; i < nw; i += nt) d[i] = __ldcg(s + i);
+    for (int64_t b = (nw << 2) + tid; b < n; b += nt) dst[b] = src[b];
+  } else {
+    for (int64_t b = tid; b < n; b += nt) dst[b] = src[b];
+  }
+}
+
+// dst = src0 + stage[0] + ... + stage[ns-1], element type by DT. int32 wraps (unsigned adds,
+// G13); float32 adds in chain order with IEEE RNE (no FTZ: built without fast-math); bf16
+// accumulates in fp32 and rounds to nearest even once. V = elements per 16-byte vector.
+template <int DT>
+struct Elt;
+template <>
+struct Elt<TACCL_INT32> {
+  using acc = unsigned int;
+  static constexpr int bytes = 4, V = 4;
+  __device__ static void unpack(const int4& w, acc* o) {
+    o[0] = w.x; o[1] = w.y; o[2] = w.z; o[3] = w.w;
+  }
+  __device__ static int4 pack(const acc* a) { return make_int4(a[0], a[1], a[2], a[3]); }
+  __device__ static acc load(const char* p) { return __ldcg(reinterpret_cast<const unsigned int*>(p)); }
+  __device__ static void store(char* p, acc v) { *reinterpret_cast<unsigned int*>(p) = v; }
+  __device__ static acc add(acc a, acc b) { return a + b; }
+};
+template <>
+struct Elt<TACCL_FLOAT32> {
+  using acc = float;
+  static constexpr int bytes = 4, V = 4;
+  __device__ static void unpack(const int4& w, acc* o) {
+    o[0] = __int_as_float(w.x); o[1] = __int_as_float(w.y);
+    o[2] = __int_as_float(w.z); o[3] = __int_as_float(w.w);
+  }
+  __device__ static int4 pack(const acc* a) {
+    return make_int4(__float_as_int(a[0]), __float_as_int(a[1]), __float_as_int(a[2]), __float_as_int(a[3]));
+  }
+  __device__ static acc load(const char* p) { return __ldcg(reinterpret_cast<const float*>(p)); }
+  __device__ static void store(char* p, acc v) { *reinterpret_cast<float*>(p) = v; }
+  __device__ static acc add(acc a, acc b) { return __fadd_rn(a, b); }
+};
+template <>
+struct Elt<TACCL_BFLOAT16> {
+  using acc = float;
+  static constexpr int bytes = 2, V = 8;
+  __device__ static void unpack(const int4& w, acc* o) {
+    const unsigned int u[4] = {(unsigned)w.x, (unsigned)w.y, (unsigned)w.z, (unsigned)w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      o[2 * i] = __uint_as_float(u[i] << 16);
+      o[2 * i + 1] = __uint_as_float(u[i] & 0xffff0000u);
+    }
+  }
+  __device__ static unsigned int rn(float f) {
+    return (unsigned int)__bfloat16_as_ushort(__float2bfloat16_rn(f));
+  }
+  __device__ static int4 pack(const acc* a) {
+    return make_int4(rn(a[0]) | rn(a[1]) << 16, rn(a[2]) | rn(a[3]) << 16,
+                     rn(a[4]) | rn(a[5]) << 16, rn(a[6]) | rn(a[7]) << 16);
+  }
+  __device__ static acc load(const char* p) {
+    return __uint_as_float((unsigned int)__ldcg(reinterpret_cast<const unsigned short*>(p)) << 16);
+  }
+  __device__ static void store(char* p, acc v) { *reinterpret_cast<unsigned short*>(p) = (unsigned short)rn(v); }
+  __device__ static acc add(acc a, acc b) { return __fadd_rn(a, b); }
+};
+
+template <int DT>
+__device__ void cta_reduce(char* dst, const char* src0, const char* const* stages, int ns,
+                           int64_t soff, int64_t nelem) {
+  using E = Elt<DT>;
+  constexpr int V = E::V;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  uintptr_t align = (uintptr_t)dst | (uintptr_t)src0;
+  for (int s = 0; s < ns; ++s) align |= (uintptr_t)(stages[s] + soff);
+  const int64_t nv = (align & 15) ? 0 : nelem / V;
+  for (int64_t v = tid; v < nv; v += nt) {
+    const int64_t off = v * 16;
+    typename E::acc acc[V], in[V];
+    E::unpack(ld_cg(reinterpret_cast<const int4*>(src0 + off)), acc);
+    for (int s = 0; s < ns; ++s) {
+      E::unpack(ld_cg(reinterpret_cast<const int4*>(stages[s] + soff + off)), in);
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] = E::add(acc[e], in[e]);
+    }
+    st_v4(reinterpret_cast<int4*>(dst + off), E::pack(acc));
+  }
+  for (int64_t e = nv * V + tid; e < nelem; e += nt) {
+    const int64_t off = e * E::bytes;
+    typename E::acc acc = E::load(src0 + off);
+    for (int s = 0; s < ns; ++s) acc = E::add(acc, E::load(stages[s] + soff + off));
+    E::store(dst + off, acc);
+  }
+}
+
+__device__ void reduce_dispatch(int dtype, char* dst, const char* src0, const char* const* stages,
+                                int ns, int64_t soff, int64_t nelem) {
+  if (dtype == TACCL_INT32) cta_reduce<TACCL_INT32>(dst, src0, stages, ns, soff, nelem);
+  else if (dtype == TACCL_FLOAT32) cta_reduce<TACCL_FLOAT32>(dst, src0, stages, ns, soff, nelem);
+  else cta_reduce<TACCL_BFLOAT16>(dst, src0, stages, ns, soff, nelem);
+}
+
+// ---------------------------------------------------------------- the interpreter
+struct Ctx {
+  const KArgs* a;
+  const KRank* r;
+  int t, j;
+  u64 epoch;
+};
+
+__device__ __forceinline__ char* local_base(const Ctx& c, int buf) {
+  switch (buf) {
+    case KB_I: return const_cast<char*>(c.r->in);
+    case KB_O: return c.r->out;
+    case KB_S: return c.r->arena + c.a->scratch_off;
+    default: return c.r->arena + c.a->staging_off;
+  }
+}
+__device__ __forceinline__ char* remote_base(const Ctx& c, int peer, int buf) {
+  switch (buf) {
+    case KB_O: return c.r->peer_out[peer];
+    case KB_S: return c.r->peer_arena[peer] + c.a->scratch_off;
+    default: return c.r->peer_arena[peer] + c.a->staging_off;
+  }
+}
+
+// Element range [lo, hi) of piece j inside one chunk (same rule on every rank).
+__device__ __forceinline__ void piece(const KArgs& a, int j, int64_t* lo, int64_t* hi) {
+  const int64_t ng = a.chunk_elems / a.granule;
+  *lo = (int64_t)j * ng / a.split * a.granule;
+  *hi = (int64_t)(j + 1) * ng / a.split * a.granule;
+}
+
+__device__ void record_error(const Ctx& c, int what, int step) {
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(c.r->arena + kOffCtrl);
+  if (atomicCAS(&ctrl->error, 0u, 1u) == 0u) {
+    ctrl->err_rank = c.r->rank;
+    ctrl->err_tb = c.t;
+    ctrl->err_step = step;
+    ctrl->err_what = what;
+    __threadfence_system();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_constant__ KArgs A) {
+  __shared__ int s_abort;
+  __shared__ u64 s_epoch;
+  __shared__ const char* s_stage[kMaxRanks + 1];
+  const int tid = threadIdx.x;
+  int lr = 0;
+  while (lr + 1 < A.nlocal && (int)blockIdx.x >= A.r[lr + 1].cta_begin) ++lr;
+  const KRank& R = A.r[lr];
+  const int local = blockIdx.x - R.cta_begin;
+  Ctx c{&A, &R, local / A.split, local % A.split, 0};
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
+  if (tid == 0) {
+    s_epoch = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
+    s_abort = 0;
+  }
+  __syncthreads();
+  c.epoch = s_epoch;
+  const u64 E = c.epoch << 24;
+  const KTB tb = R.tbs[c.t];
+  u64* my_data = reinterpret_cast<u64*>(R.arena + kOffData);
+  u64* my_ready = reinterpret_cast<u64*>(R.arena + kOffReady);
+  u64* my_done = reinterpret_cast<u64*>(R.arena + kOffDone);
+  // entry handshake: tell our sender we are in this call (its stores may now land)
+  if (tb.recv >= 0 && tid == 0) {
+    u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
+    st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, c.j), c.epoch);
+  }
+  bool sender_ready = false;
+  int64_t lo, hi;
+  piece(A, c.j, &lo, &hi);
+  const int64_t ce = A.chunk_elems;
+  const int elt = A.elt;
+
+  for (int k = 0; k < tb.nsteps; ++k) {
+    const KStep st = R.steps[tb.step_begin + k];
+    if (tid == 0) {
+      bool ok = true;
+      for (int d = 0; d < st.dep_count && ok; ++d) {
+        const int dt = R.deps[2 * (st.dep_begin + d)], dk = R.deps[2 * (st.dep_begin + d) + 1];
+        ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + c.j, E | (u64)(dk + 1), A.timeout_ns);
+      }
+      if (ok && st.op == K_SEND && !sender_ready) {
+        ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, c.j), c.epoch, A.timeout_ns);
+        sender_ready = true;
+      }
+      if (ok && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRC_FUSED))
+        ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, c.j), E | (u64)(st.seq + 1), A.timeout_ns);
+      if (ok && st.op == K_RRC_FUSED) {
+        for (int f = 0; f < st.fuse_count && ok; ++f) {
+          const int* fz = R.fused + 3 * (st.fuse_begin + f);
+          const KTB o = R.tbs[fz[0]];
+          ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, c.j), E | (u64)(fz[1] + 1), A.timeout_ns);
+        }
+      }
+      if (!ok) {
+        record_error(c, st.op, k);
+        s_abort = 1;
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;
+
+    // pieces: one contiguous range when split == 1, else piece j of each of the cnt chunks
+    const int npieces = A.split == 1 ? 1 : st.cnt;
+    const int64_t pbytes = A.split == 1 ? (int64_t)st.cnt * ce * elt : (hi - lo) * elt;
+    const int64_t p0 = A.split == 1 ? 0 : lo * elt;
+    const int64_t cbytes = ce * elt;
+    switch (st.op) {
+      case K_SEND: {
+        const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
+        char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes + p0;
+        for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
+        break;
+      }
+      case K_CPY: {
+        const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
+        char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
+        for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
+        break;
+      }
+      case K_RRC:
+      case K_RRC_FUSED: {
+        if (tid == 0) {
+          int ns = 0;
+          if (st.op == K_RRC_FUSED)
+            for (int f = 0; f < st.fuse_count; ++f)
+              s_stage[ns++] = local_base(c, KB_STAGE) + (int64_t)R.fused[3 * (st.fuse_begin + f) + 2] * cbytes + p0;
+          s_stage[ns] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes + p0;
+        }
+        __syncthreads();
+        const int ns = (st.op == K_RRC_FUSED ? st.fuse_count : 0) + 1;
+        const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
+        char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
+        for (int q = 0; q < npieces; ++q)
+          reduce_dispatch(A.dtype, dst + q * cbytes, src + q * cbytes, s_stage, ns, q * cbytes, pbytes / elt);
+        break;
+      }
+      default:  // K_RECV, K_NOP, K_RECV_ONLY: no data work on this side
+        break;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (st.op == K_SEND) {
+        __threadfence_system();
+        u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
+        st_relaxed_sys(data + flag_slot(R.rank, tb.chan, c.j), E | (u64)(st.seq + 1));
+      }
+      if (st.need_done) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + c.j, E | (u64)(k + 1));
+    }
+  }
+  // completion: the rank's last CTA advances the rank's epoch for the next call
+  if (tid == 0) {
+    const unsigned total = (unsigned)R.ntb * (unsigned)A.split;
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctrl->finished) : "memory");
+    if (prev == total - 1) {
+      ctrl->finished = 0;
+      *reinterpret_cast<volatile u64*>(&ctrl->epoch) = c.epoch + 1;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_executor(const KArgs& a, int grid, void* stream, std::string* err) {
+  taccl_exec_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("kernel launch: ") + cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
+int executor_max_ctas(int device, std::string* err) {
+  int per_sm = 0, sms = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, taccl_exec_kernel, kThreads, 0);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    *err = std::string("occupancy query: ") + cudaGetErrorString(e);
+    return -1;
+  }
+  return per_sm * sms;
+}
+
+}  // namespace taccl

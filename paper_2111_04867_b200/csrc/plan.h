@@ -1,0 +1,22 @@
+// Per-rank device plan built from a checked program (plan.cpp).
+#pragma once
+#include <vector>
+
+#include "taccl_internal.h"
+
+namespace taccl {
+
+struct RankPlan {
+  std::vector<KTB> tbs;
+  std::vector<KStep> steps;
+  std::vector<int32_t> deps;   // pairs (tb, step)
+  std::vector<int32_t> fused;  // triples (tb, seq, soff)
+  int stage_chunks = 0;        // rrc staging this rank needs (chunk units)
+  int scratch_chunks = 0;      // EF scratch buffer (chunk units)
+  int fused_chains = 0;
+};
+
+// `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables).
+std::vector<RankPlan> build_plans(const Program& P, bool fuse);
+
+}  // namespace taccl

@@ -1,0 +1,615 @@
+// C ABI (include/taccl.h): communicator, IPC peer mappings, buffer registration, algorithm
+// registry and the single-launch collective call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+#include "taccl_internal.h"
+
+using namespace taccl;
+
+namespace {
+
+thread_local std::string g_err;
+
+taccl_result_t fail(taccl_result_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess) return fail(TACCL_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr uint32_t kMagicArena = 0x7acc1a7e;
+constexpr uint32_t kMagicBuf = 0x7acc1b0f;
+
+struct HandleBlob {  // TACCL_HANDLE_BYTES
+  uint32_t magic;
+  int32_t rank;
+  uint64_t offset;   // pointer - allocation base
+  uint64_t bytes;
+  cudaIpcMemHandle_t h;  // 64 bytes
+  char pad[TACCL_HANDLE_BYTES - 24 - sizeof(cudaIpcMemHandle_t)];
+};
+static_assert(sizeof(HandleBlob) == TACCL_HANDLE_BYTES, "blob size");
+
+struct DevPlan {  // one rank's plan in device memory
+  void* mem = nullptr;
+  const KTB* tbs = nullptr;
+  const KStep* steps = nullptr;
+  const int32_t* deps = nullptr;
+  const int32_t* fused = nullptr;
+  int ntb = 0;
+};
+
+struct Algo {
+  std::string name;
+  Coll coll;
+  int nranks, p, instances;
+  uint64_t min_bytes, max_bytes;
+  int max_scratch_chunks = 0, max_stage_chunks = 0, max_steps_cnt = 1;
+  std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
+  std::vector<int> ntb;         // per rank
+  int fused_chains = 0;
+};
+
+struct Reg {
+  uintptr_t lo, hi;
+  char* peer_base[kMaxRanks];  // peer's registered pointer (own rank: local pointer)
+};
+
+struct Comm {
+  bool up = false, emulated = false, peers_set = false;
+  int rank = 0, nranks = 0, device = 0;
+  size_t arena_bytes = 0;
+  std::vector<char*> arenas;           // local arenas (1, or nranks if emulated)
+  char* peer_arena[kMaxRanks] = {};    // every rank's arena as seen by this process
+  std::vector<Algo*> algos;
+  std::vector<Reg> regs;
+  std::map<std::string, char*> ipc_open;  // handle bytes -> mapped base
+  int max_ctas = 0;
+  uint64_t launches = 0;
+  uint64_t timeout_ns = 0;
+  // host-run staging (taccl_run_host): library-owned pinned bounce is the user's job
+};
+
+Comm g;
+
+int elt_size(taccl_dtype_t d) { return d == TACCL_BFLOAT16 ? 2 : 4; }
+
+size_t env_size(const char* name, size_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return (size_t)strtoull(v, nullptr, 10);
+}
+
+taccl_result_t alloc_arena(char** out, size_t scratch) {
+  char* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, kOffScratch + scratch));
+  CUDA_TRY(cudaMemset(p, 0, kOffScratch));
+  Ctrl c{};
+  c.epoch = 1;
+  CUDA_TRY(cudaMemcpy(p + kOffCtrl, &c, sizeof(c), cudaMemcpyHostToDevice));
+  *out = p;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t comm_common_init(int nranks, int device, size_t scratch) {
+  if (g.up) return fail(TACCL_ERR_INVALID_ARG, "communicator already initialized");
+  if (nranks < 1 || nranks > kMaxRanks)
+    return fail(TACCL_ERR_UNSUPPORTED, "nranks must be in [1, " + std::to_string(kMaxRanks) + "]");
+  CUDA_TRY(cudaSetDevice(device));
+  g.nranks = nranks;
+  g.device = device;
+  g.arena_bytes = kOffScratch + (scratch ? scratch : env_size("TACCL_SCRATCH_BYTES", 256ull << 20));
+  g.timeout_ns = (uint64_t)(env_size("TACCL_TIMEOUT_S", 20) * 1000000000ull);
+  std::string err;
+  g.max_ctas = executor_max_ctas(device, &err);
+  if (g.max_ctas <= 0) return fail(TACCL_ERR_CUDA, err);
+  return TACCL_SUCCESS;
+}
+
+// allocation base of a device pointer via the driver entry point (no libcuda link dependency)
+taccl_result_t alloc_base(const void* ptr, char** base, size_t* size) {
+  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) return fail(TACCL_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    fn = (GetRange)f;
+  }
+  unsigned long long b = 0;
+  size_t s = 0;
+  if (fn(&b, &s, (unsigned long long)(uintptr_t)ptr) != 0)
+    return fail(TACCL_ERR_INVALID_ARG, "pointer is not device memory from cudaMalloc");
+  *base = (char*)(uintptr_t)b;
+  *size = s;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t open_handle(const cudaIpcMemHandle_t& h, char** out) {
+  std::string key((const char*)&h, sizeof(h));
+  auto it = g.ipc_open.find(key);
+  if (it != g.ipc_open.end()) {
+    *out = it->second;
+    return TACCL_SUCCESS;
+  }
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  g.ipc_open[key] = (char*)p;
+  *out = (char*)p;
+  return TACCL_SUCCESS;
+}
+
+// message bytes S used for algorithm selection (SURVEY.md §8(b) convention 4, reading G8)
+uint64_t select_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
+  if (coll == TACCL_ALLREDUCE) return (uint64_t)count * elt;
+  return (uint64_t)n * count * elt;
+}
+
+Algo* select_algo(taccl_coll_t coll, uint64_t S) {
+  for (auto it = g.algos.rbegin(); it != g.algos.rend(); ++it) {  // latest load wins
+    Algo* a = *it;
+    if ((int)a->coll == (int)coll && a->nranks == g.nranks && S >= a->min_bytes &&
+        (a->max_bytes == UINT64_MAX || S < a->max_bytes))
+      return a;
+  }
+  return nullptr;
+}
+
+struct Geometry {
+  int64_t ce = 0, chunk_bytes = 0, granule = 1;
+  int split = 1, grid = 0;
+  int64_t scratch_off = 0, staging_off = 0, need = 0;
+};
+
+taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt, int nlocal_ranks,
+                        int64_t base_off, Geometry* G) {
+  int n_in, n_out;
+  buffer_chunks(a->coll, a->nranks, a->p, &n_in, &n_out);
+  const int64_t e_in = coll == TACCL_ALLTOALL ? (int64_t)a->nranks * count : (int64_t)count;
+  if (e_in % n_in)
+    return fail(TACCL_ERR_INVALID_ARG, "count " + std::to_string(count) + " does not split into " +
+                                           std::to_string(n_in) + " equal chunks (reading G2)");
+  G->ce = e_in / n_in;
+  G->chunk_bytes = G->ce * elt;
+  G->granule = (G->chunk_bytes % 16 == 0) ? 16 / elt : 1;
+  // lanes: extra CTAs per threadblock on top of the schedule's instances (same split rule)
+  int total_tb = 0;
+  for (int r = 0; r < a->nranks; ++r)
+    if (a->plans[r].mem) total_tb += a->ntb[r];
+  int lanes = 1;
+  const size_t forced = env_size("TACCL_LANES", 0);
+  const int64_t min_piece = (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
+  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", 296));
+  if (forced) {
+    lanes = (int)forced;
+  } else {
+    const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes / a->instances;
+    while (lanes * 2 * a->instances <= kMaxSplit && total_tb * a->instances * lanes * 2 <= target &&
+           step_bytes / (lanes * 2) >= min_piece)
+      lanes *= 2;
+  }
+  G->split = a->instances * lanes;
+  if (G->split > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances x lanes exceeds TACCL_MAX_SPLIT");
+  G->grid = total_tb * G->split;
+  if (G->grid > g.max_ctas)
+    return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
+                                           std::to_string(g.max_ctas));
+  G->scratch_off = kOffScratch + base_off;
+  G->staging_off = G->scratch_off + (((int64_t)a->max_scratch_chunks * G->chunk_bytes + 255) & ~(int64_t)255);
+  G->need = G->staging_off + (int64_t)a->max_stage_chunks * G->chunk_bytes;
+  if ((size_t)G->need > g.arena_bytes)
+    return fail(TACCL_ERR_INVALID_ARG, "arena too small: need " + std::to_string(G->need) + " bytes, have " +
+                                           std::to_string(g.arena_bytes) + " (raise scratch_bytes / TACCL_SCRATCH_BYTES)");
+  (void)nlocal_ranks;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int elt,
+                      const std::vector<int>& ranks, const void* const* sends, void* const* recvs,
+                      char* const (*peer_out)[kMaxRanks], void* stream) {
+  KArgs A;
+  memset(&A, 0, sizeof(A));
+  A.nlocal = (int)ranks.size();
+  A.split = G.split;
+  A.elt = elt;
+  A.dtype = dtype;
+  A.chunk_elems = G.ce;
+  A.granule = G.granule;
+  A.scratch_off = G.scratch_off;
+  A.staging_off = G.staging_off;
+  A.timeout_ns = g.timeout_ns;
+  int cta = 0;
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    const int r = ranks[i];
+    KRank& R = A.r[i];
+    const DevPlan& dp = a->plans[r];
+    R.tbs = dp.tbs;
+    R.steps = dp.steps;
+    R.deps = dp.deps;
+    R.fused = dp.fused;
+    R.in = (const char*)sends[i];
+    R.out = (char*)recvs[i];
+    R.arena = g.peer_arena[r];
+    for (int q = 0; q < g.nranks; ++q) {
+      R.peer_out[q] = peer_out[i][q];
+      R.peer_arena[q] = g.peer_arena[q];
+    }
+    R.rank = r;
+    R.ntb = dp.ntb;
+    R.cta_begin = cta;
+    cta += dp.ntb * G.split;
+  }
+  std::string err;
+  if (launch_executor(A, cta, stream, &err)) return fail(TACCL_ERR_CUDA, err);
+  ++g.launches;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t check_common(taccl_coll_t coll, size_t count, taccl_dtype_t dtype) {
+  if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
+  if (!g.emulated && !g.peers_set && g.nranks > 1) return fail(TACCL_ERR_NOT_INITIALIZED, "peers not set");
+  if (coll < TACCL_ALLGATHER || coll > TACCL_ALLREDUCE) return fail(TACCL_ERR_INVALID_ARG, "bad collective");
+  if (dtype < TACCL_INT32 || dtype > TACCL_BFLOAT16) return fail(TACCL_ERR_INVALID_ARG, "bad dtype");
+  (void)count;
+  return TACCL_SUCCESS;
+}
+
+size_t in_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
+  return coll == TACCL_ALLTOALL ? (size_t)n * count * elt : count * elt;
+}
+size_t out_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
+  return coll == TACCL_ALLREDUCE ? count * elt : (size_t)n * count * elt;
+}
+
+taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, size_t count,
+                       taccl_dtype_t dtype, void* stream, int64_t base_off, bool arena_out) {
+  taccl_result_t rc = check_common(coll, count, dtype);
+  if (rc) return rc;
+  if (g.emulated) return fail(TACCL_ERR_INVALID_ARG, "emulated communicator: use taccl_run_emulated");
+  if (count == 0) return TACCL_SUCCESS;
+  const int elt = elt_size(dtype), n = g.nranks;
+  if (!sendbuf || !recvbuf) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
+  const size_t ib = in_bytes(coll, count, elt, n), ob = out_bytes(coll, count, elt, n);
+  if ((const char*)sendbuf < (const char*)recvbuf + ob && (const char*)recvbuf < (const char*)sendbuf + ib)
+    return fail(TACCL_ERR_UNSUPPORTED, "in-place / overlapping buffers are not supported (reading G10)");
+  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n));
+  if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
+  Geometry G;
+  if ((rc = geometry(a, coll, count, elt, 1, base_off, &G))) return rc;
+  char* peer_out[1][kMaxRanks] = {};
+  if (arena_out) {
+    for (int q = 0; q < n; ++q) peer_out[0][q] = g.peer_arena[q] + ((char*)recvbuf - g.peer_arena[g.rank]);
+  } else if (n > 1) {
+    const Reg* hit = nullptr;
+    for (const Reg& rg : g.regs)
+      if ((uintptr_t)recvbuf >= rg.lo && (uintptr_t)recvbuf + ob <= rg.hi) hit = &rg;
+    if (!hit) return fail(TACCL_ERR_NOT_REGISTERED, "recvbuf is not inside a registered buffer (taccl_register_buffer)");
+    const uintptr_t off = (uintptr_t)recvbuf - hit->lo;
+    for (int q = 0; q < n; ++q) peer_out[0][q] = hit->peer_base[q] + off;
+  } else {
+    peer_out[0][0] = (char*)recvbuf;
+  }
+  std::vector<int> ranks{g.rank};
+  const void* s[1] = {sendbuf};
+  void* r[1] = {recvbuf};
+  return launch(a, G, dtype, elt, ranks, s, r, peer_out, stream);
+}
+
+taccl_result_t upload(const RankPlan& rp, DevPlan* dp) {
+  const size_t b1 = rp.tbs.size() * sizeof(KTB), b2 = rp.steps.size() * sizeof(KStep);
+  const size_t b3 = rp.deps.size() * 4, b4 = rp.fused.size() * 4;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t total = al(b1) + al(b2) + al(b3) + al(b4) + 256;
+  char* m = nullptr;
+  CUDA_TRY(cudaMalloc(&m, total));
+  std::vector<char> host(total, 0);
+  size_t o = 0;
+  auto put = [&](const void* src, size_t bytes) {
+    if (bytes) memcpy(host.data() + o, src, bytes);
+    size_t at = o;
+    o += al(bytes);
+    return m + at;
+  };
+  dp->tbs = (const KTB*)put(rp.tbs.data(), b1);
+  dp->steps = (const KStep*)put(rp.steps.data(), b2);
+  dp->deps = (const int32_t*)put(rp.deps.data(), b3);
+  dp->fused = (const int32_t*)put(rp.fused.data(), b4);
+  CUDA_TRY(cudaMemcpy(m, host.data(), total, cudaMemcpyHostToDevice));
+  dp->mem = m;
+  dp->ntb = (int)rp.tbs.size();
+  return TACCL_SUCCESS;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* taccl_last_error(void) { return g_err.c_str(); }
+
+taccl_result_t taccl_check(void) {
+  if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
+  for (size_t i = 0; i < g.arenas.size(); ++i) {
+    Ctrl c;
+    CUDA_TRY(cudaMemcpy(&c, g.arenas[i] + kOffCtrl, sizeof(c), cudaMemcpyDeviceToHost));
+    if (c.error)
+      return fail(TACCL_ERR_TIMEOUT, "device watchdog: rank " + std::to_string(c.err_rank) + " tb " +
+                                         std::to_string(c.err_tb) + " step " + std::to_string(c.err_step) +
+                                         " (op " + std::to_string(c.err_what) + ") waited longer than TACCL_TIMEOUT_S");
+  }
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_validate(const char* text, size_t len, int direct_store) {
+  if (!text) return fail(TACCL_ERR_INVALID_ARG, "null text");
+  try {
+    Program P = parse_ef(text, len);
+    check_program(P, direct_store != 0);
+  } catch (const SchedError& e) {
+    return fail(TACCL_ERR_INVALID_SCHEDULE, e.kind + ": " + e.msg);
+  }
+  g_err.clear();
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_comm_init(int rank, int nranks, int cuda_device, size_t scratch_bytes) {
+  if (rank < 0 || rank >= nranks) return fail(TACCL_ERR_INVALID_ARG, "rank out of range");
+  taccl_result_t rc = comm_common_init(nranks, cuda_device, scratch_bytes);
+  if (rc) return rc;
+  char* a = nullptr;
+  if ((rc = alloc_arena(&a, g.arena_bytes - kOffScratch))) return rc;
+  g.arenas = {a};
+  g.rank = rank;
+  g.peer_arena[rank] = a;
+  g.emulated = false;
+  g.peers_set = (nranks == 1);
+  g.up = true;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_comm_init_emulated(int nranks, int cuda_device, size_t scratch_bytes) {
+  taccl_result_t rc = comm_common_init(nranks, cuda_device, scratch_bytes);
+  if (rc) return rc;
+  g.arenas.clear();
+  for (int r = 0; r < nranks; ++r) {
+    char* a = nullptr;
+    if ((rc = alloc_arena(&a, g.arena_bytes - kOffScratch))) return rc;
+    g.arenas.push_back(a);
+    g.peer_arena[r] = a;
+  }
+  g.rank = 0;
+  g.emulated = true;
+  g.peers_set = true;
+  g.up = true;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_comm_export_handle(void* out, size_t* len) {
+  if (!g.up || g.emulated) return fail(TACCL_ERR_NOT_INITIALIZED, "no multi-process communicator");
+  if (!out || !len) return fail(TACCL_ERR_INVALID_ARG, "null argument");
+  HandleBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kMagicArena;
+  b.rank = g.rank;
+  b.bytes = g.arena_bytes;
+  CUDA_TRY(cudaIpcGetMemHandle(&b.h, g.arenas[0]));
+  memcpy(out, &b, sizeof(b));
+  *len = sizeof(b);
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_comm_set_peers(const void* all, size_t len_each) {
+  if (!g.up || g.emulated) return fail(TACCL_ERR_NOT_INITIALIZED, "no multi-process communicator");
+  if (!all || len_each != sizeof(HandleBlob)) return fail(TACCL_ERR_INVALID_ARG, "bad handle blobs");
+  for (int q = 0; q < g.nranks; ++q) {
+    HandleBlob b;
+    memcpy(&b, (const char*)all + q * len_each, sizeof(b));
+    if (b.magic != kMagicArena || b.rank != q) return fail(TACCL_ERR_INVALID_ARG, "handle blob " + std::to_string(q) + " is not rank " + std::to_string(q) + "'s arena");
+    if (b.bytes != g.arena_bytes) return fail(TACCL_ERR_INVALID_ARG, "ranks disagree on arena size");
+    if (q == g.rank) continue;
+    char* p = nullptr;
+    taccl_result_t rc = open_handle(b.h, &p);
+    if (rc) return rc;
+    g.peer_arena[q] = p;
+  }
+  g.peers_set = true;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_comm_destroy(void) {
+  if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
+  cudaDeviceSynchronize();
+  for (Algo* a : g.algos) {
+    for (auto& p : a->plans)
+      if (p.mem) cudaFree(p.mem);
+    delete a;
+  }
+  for (auto& kv : g.ipc_open) cudaIpcCloseMemHandle(kv.second);
+  for (char* a : g.arenas) cudaFree(a);
+  g = Comm();
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_buffer_export(const void* ptr, size_t bytes, void* out, size_t* len) {
+  if (!g.up || g.emulated) return fail(TACCL_ERR_NOT_INITIALIZED, "no multi-process communicator");
+  if (!ptr || !out || !len) return fail(TACCL_ERR_INVALID_ARG, "null argument");
+  char* base = nullptr;
+  size_t size = 0;
+  taccl_result_t rc = alloc_base(ptr, &base, &size);
+  if (rc) return rc;
+  if ((const char*)ptr + bytes > base + size) return fail(TACCL_ERR_INVALID_ARG, "range exceeds its allocation");
+  HandleBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kMagicBuf;
+  b.rank = g.rank;
+  b.offset = (uint64_t)((const char*)ptr - base);
+  b.bytes = bytes;
+  CUDA_TRY(cudaIpcGetMemHandle(&b.h, base));
+  memcpy(out, &b, sizeof(b));
+  *len = sizeof(b);
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* all, size_t len_each) {
+  if (!g.up || g.emulated) return fail(TACCL_ERR_NOT_INITIALIZED, "no multi-process communicator");
+  if (!ptr || !all || len_each != sizeof(HandleBlob)) return fail(TACCL_ERR_INVALID_ARG, "bad arguments");
+  Reg rg;
+  rg.lo = (uintptr_t)ptr;
+  rg.hi = rg.lo + bytes;
+  for (int q = 0; q < g.nranks; ++q) {
+    HandleBlob b;
+    memcpy(&b, (const char*)all + q * len_each, sizeof(b));
+    if (b.magic != kMagicBuf || b.rank != q) return fail(TACCL_ERR_INVALID_ARG, "buffer blob " + std::to_string(q) + " invalid");
+    if (b.bytes != bytes) return fail(TACCL_ERR_INVALID_ARG, "ranks registered buffers of different sizes");
+    if (q == g.rank) {
+      rg.peer_base[q] = (char*)ptr;
+      continue;
+    }
+    char* base = nullptr;
+    taccl_result_t rc = open_handle(b.h, &base);
+    if (rc) return rc;
+    rg.peer_base[q] = base + b.offset;
+  }
+  g.regs.push_back(rg);
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) {
+  if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
+  if (!text) return fail(TACCL_ERR_INVALID_ARG, "null text");
+  std::unique_ptr<Algo> a(new Algo);
+  std::vector<RankPlan> plans;
+  try {
+    Program P = parse_ef(text, len);
+    check_program(P, true);
+    if (P.nranks != g.nranks)
+      return fail(TACCL_ERR_INVALID_ARG, "schedule has nranks=" + std::to_string(P.nranks) + ", communicator " + std::to_string(g.nranks));
+    for (const Gpu& gp : P.gpus) {
+      if ((int)gp.tbs.size() > kMaxTB) return fail(TACCL_ERR_UNSUPPORTED, "more than TACCL_MAX_TB threadblocks on a rank");
+      for (const TB& tb : gp.tbs) {
+        if (tb.chan >= kMaxChan) return fail(TACCL_ERR_UNSUPPORTED, "chan >= TACCL_MAX_CHAN");
+        for (const Step& st : tb.steps) a->max_steps_cnt = std::max(a->max_steps_cnt, st.cnt);
+      }
+    }
+    if (P.instances > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances > TACCL_MAX_SPLIT");
+    plans = build_plans(P, env_size("TACCL_NO_FUSE", 0) == 0);
+    a->name = P.name;
+    a->coll = P.coll;
+    a->nranks = P.nranks;
+    a->p = P.p;
+    a->instances = P.instances;
+    a->min_bytes = P.min_bytes;
+    a->max_bytes = P.max_bytes;
+  } catch (const SchedError& e) {
+    return fail(TACCL_ERR_INVALID_SCHEDULE, e.kind + ": " + e.msg);
+  }
+  a->plans.assign(a->nranks, DevPlan());
+  a->ntb.assign(a->nranks, 0);
+  for (int r = 0; r < a->nranks; ++r) {
+    a->ntb[r] = (int)plans[r].tbs.size();
+    a->max_scratch_chunks = std::max(a->max_scratch_chunks, plans[r].scratch_chunks);
+    a->max_stage_chunks = std::max(a->max_stage_chunks, plans[r].stage_chunks);
+    a->fused_chains += plans[r].fused_chains;
+    if (g.emulated || r == g.rank) {
+      taccl_result_t rc = upload(plans[r], &a->plans[r]);
+      if (rc) return rc;
+    }
+  }
+  Algo* raw = a.release();
+  g.algos.push_back(raw);
+  if (out) *out = (taccl_algo_t)raw;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_free(taccl_algo_t algo) {
+  auto it = std::find(g.algos.begin(), g.algos.end(), (Algo*)algo);
+  if (it == g.algos.end()) return fail(TACCL_ERR_INVALID_ARG, "unknown algorithm");
+  for (auto& p : (*it)->plans)
+    if (p.mem) cudaFree(p.mem);
+  delete *it;
+  g.algos.erase(it);
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_run(taccl_coll_t coll, const void* sendbuf, void* recvbuf, size_t count,
+                         taccl_dtype_t dtype, void* stream) {
+  return run_one(coll, sendbuf, recvbuf, count, dtype, stream, 0, false);
+}
+
+taccl_result_t taccl_run_emulated(taccl_coll_t coll, const void* const* sendbufs, void* const* recvbufs,
+                                  size_t count, taccl_dtype_t dtype, void* stream) {
+  taccl_result_t rc = check_common(coll, count, dtype);
+  if (rc) return rc;
+  if (!g.emulated) return fail(TACCL_ERR_INVALID_ARG, "not an emulated communicator");
+  if (!sendbufs || !recvbufs) return fail(TACCL_ERR_INVALID_ARG, "null buffer array");
+  if (count == 0) return TACCL_SUCCESS;
+  const int elt = elt_size(dtype), n = g.nranks;
+  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n));
+  if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
+  Geometry G;
+  if ((rc = geometry(a, coll, count, elt, n, 0, &G))) return rc;
+  std::vector<int> ranks(n);
+  char* peer_out[kMaxRanks][kMaxRanks] = {};
+  for (int r = 0; r < n; ++r) {
+    ranks[r] = r;
+    if (!sendbufs[r] || !recvbufs[r]) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
+    for (int q = 0; q < n; ++q) peer_out[r][q] = (char*)recvbufs[q];
+  }
+  return launch(a, G, dtype, elt, ranks, sendbufs, recvbufs, peer_out, stream);
+}
+
+taccl_result_t taccl_run_host(taccl_coll_t coll, const void* host_send, void* host_recv, size_t count,
+                              taccl_dtype_t dtype, void* stream) {
+  taccl_result_t rc = check_common(coll, count, dtype);
+  if (rc) return rc;
+  if (g.emulated) return fail(TACCL_ERR_INVALID_ARG, "emulated communicator: not supported for host runs");
+  if (!host_send || !host_recv) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
+  const int elt = elt_size(dtype), n = g.nranks;
+  const size_t ib = in_bytes(coll, count, elt, n), ob = out_bytes(coll, count, elt, n);
+  // library-owned device buffers: the front of this rank's (symmetric) arena scratch region
+  const int64_t in_off = 0, out_off = ((int64_t)ib + 4095) & ~(int64_t)4095;
+  const int64_t base = (out_off + (int64_t)ob + 4095) & ~(int64_t)4095;
+  if ((size_t)(kOffScratch + base) > g.arena_bytes) return fail(TACCL_ERR_INVALID_ARG, "arena too small for host run");
+  char* dev_in = g.arenas[0] + kOffScratch + in_off;
+  char* dev_out = g.arenas[0] + kOffScratch + out_off;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(dev_in, host_send, ib, cudaMemcpyHostToDevice, s));
+  if ((rc = run_one(coll, dev_in, dev_out, count, dtype, stream, base, true))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(host_recv, dev_out, ob, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dtype, int* ctas, int* split,
+                               int* threads) {
+  taccl_result_t rc = check_common(coll, count, dtype);
+  if (rc) return rc;
+  const int elt = elt_size(dtype);
+  Algo* a = select_algo(coll, select_bytes(coll, count, elt, g.nranks));
+  if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
+  Geometry G;
+  if ((rc = geometry(a, coll, count, elt, 1, 0, &G))) return rc;
+  if (ctas) *ctas = G.grid;
+  if (split) *split = G.split;
+  if (threads) *threads = kThreads;
+  return TACCL_SUCCESS;
+}
+
+uint64_t taccl_launch_count(void) { return g.launches; }
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+// Internal types shared by the loader/validator (host C++) and the executor (CUDA).
+// The on-device plan layout and the arena layout are defined here once.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/taccl.h"
+
+namespace taccl {
+
+// ---------------------------------------------------------------- parsed program (host)
+enum StepType : int8_t { ST_S = 0, ST_R = 1, ST_RRC = 2, ST_CPY = 3, ST_NOP = 4 };
+enum BufId : int8_t { B_NONE = -1, B_I = 0, B_O = 1, B_S = 2 };
+enum Coll : int8_t { C_AG = 0, C_A2A = 1, C_AR = 2 };
+
+struct Step {
+  int s = 0;
+  StepType type = ST_NOP;
+  BufId srcbuf = B_NONE;
+  int srcoff = 0;
+  BufId dstbuf = B_NONE;
+  int dstoff = 0;
+  int cnt = 0;
+  std::vector<std::pair<int, int>> deps;  // (tb, step) on the same rank
+};
+
+struct TB {
+  int id = 0, send = -1, recv = -1, chan = 0;
+  std::vector<Step> steps;
+};
+
+struct Gpu {
+  int id = 0, i_chunks = 0, o_chunks = 0, s_chunks = 0;
+  std::vector<TB> tbs;
+  int nchunks(BufId b) const { return b == B_I ? i_chunks : b == B_O ? o_chunks : s_chunks; }
+};
+
+struct Program {
+  std::string name;
+  Coll coll = C_AG;
+  int nranks = 0, p = 1, instances = 1;
+  uint64_t min_bytes = 0, max_bytes = 0;  // max_bytes == UINT64_MAX means inf
+  std::vector<Gpu> gpus;
+};
+
+// A check failure. kind is one of docs/SCHEDULE.md's classes.
+struct SchedError {
+  std::string kind, msg;
+};
+
+Program parse_ef(const char* text, size_t len);         // throws SchedError("syntax")
+void check_program(const Program& prog, bool direct);   // throws SchedError
+void buffer_chunks(Coll c, int n, int p, int* n_in, int* n_out);
+
+// Happens-before over a checked program (program order + deps + send->recv matching).
+class HB {
+ public:
+  explicit HB(const Program& P);  // throws SchedError on match / cycle errors
+  ~HB();
+  HB(const HB&) = delete;
+  HB& operator=(const HB&) = delete;
+  bool before(int r, int t, int k, int r2, int t2, int k2) const;  // strict reachability
+ private:
+  struct Impl;
+  Impl* impl_;
+};
+
+// ---------------------------------------------------------------- device plan
+// Step codes executed by the kernel.
+enum KOp : int8_t {
+  K_SEND = 0,      // copy local src -> peer (o / s / staging), then publish data flag
+  K_RECV = 1,      // wait data flag (bytes already stored by the peer)
+  K_RRC = 2,       // wait data flag, dst = src + staging
+  K_CPY = 3,       // local copy
+  K_NOP = 4,       // deps only
+  K_RRC_FUSED = 5, // wait all chain flags, dst = src + sum(staging_i) in fp32 (bf16) / dtype
+  K_RECV_ONLY = 6  // rrc absorbed into a later fused step: no data work, no flag wait
+};
+enum KBuf : int8_t { KB_I = 0, KB_O = 1, KB_S = 2, KB_STAGE = 3 };
+
+struct KStep {
+  int8_t op;
+  int8_t srcbuf, dstbuf;  // KBuf
+  int8_t rbuf;            // K_SEND: destination buffer on the peer (KB_O / KB_S / KB_STAGE)
+  int32_t srcoff, dstoff, cnt;  // chunk units
+  int32_t roff;           // K_SEND: destination offset on the peer (chunk units)
+  int32_t seq;            // message index on the tb's connection (K_SEND/K_RECV/K_RRC)
+  int32_t soff;           // K_RRC: this rank's staging offset (chunk units)
+  int32_t dep_begin, dep_count;  // into KRankPlan.deps (pairs tb, step)
+  int32_t fuse_begin, fuse_count;  // K_RRC_FUSED: into KRankPlan.fused (tb, seq, soff) triples
+  int32_t need_done;      // some step depends on this one
+};
+
+struct KTB {
+  int32_t send, recv, chan;
+  int32_t step_begin, nsteps;
+};
+
+// ---------------------------------------------------------------- arena layout (bytes)
+// Identical on every rank so peers can compute addresses in each other's arenas.
+constexpr int kMaxRanks = TACCL_MAX_RANKS;
+constexpr int kMaxChan = TACCL_MAX_CHAN;
+constexpr int kMaxSplit = TACCL_MAX_SPLIT;
+constexpr int kMaxTB = TACCL_MAX_TB;
+constexpr size_t kFlagSlots = (size_t)kMaxRanks * kMaxChan * kMaxSplit;
+constexpr size_t kOffData = 0;                                   // u64[kFlagSlots], written by senders
+constexpr size_t kOffReady = kOffData + kFlagSlots * 8;          // u64[kFlagSlots], written by receivers
+constexpr size_t kOffDone = kOffReady + kFlagSlots * 8;          // u64[kMaxTB*kMaxSplit], local
+constexpr size_t kOffCtrl = kOffDone + (size_t)kMaxTB * kMaxSplit * 8;
+constexpr size_t kCtrlBytes = 256;   // epoch (u64), finished (u32), error (u32), err detail
+constexpr size_t kOffScratch = (kOffCtrl + kCtrlBytes + 4095) & ~(size_t)4095;
+
+#ifdef __CUDACC__
+#define TACCL_HD __host__ __device__
+#else
+#define TACCL_HD
+#endif
+
+TACCL_HD inline size_t flag_slot(int peer, int chan, int j) {
+  return ((size_t)peer * kMaxChan + chan) * kMaxSplit + j;
+}
+
+struct Ctrl {
+  unsigned long long epoch;
+  unsigned int finished;
+  unsigned int error;       // 0 ok, 1 timeout
+  int err_rank, err_tb, err_step, err_what;
+};
+
+}  // namespace taccl
+
+namespace taccl {
+
+// ---------------------------------------------------------------- kernel arguments
+// Per local rank (one in multi-process mode, all ranks when emulated). Passed by value.
+struct KRank {
+  const KTB* tbs;
+  const KStep* steps;
+  const int32_t* deps;     // pairs (tb, step)
+  const int32_t* fused;    // triples (tb, seq, soff) per absorbed rrc of a fused chain
+  const char* in;
+  char* out;
+  char* arena;
+  char* peer_out[kMaxRanks];    // peer's output buffer (this call's recvbuf on the peer)
+  char* peer_arena[kMaxRanks];  // peer's arena (flags, scratch, staging)
+  int32_t rank, ntb, cta_begin, pad;
+};
+
+struct KArgs {
+  KRank r[kMaxRanks];
+  int32_t nlocal;          // local ranks in this launch
+  int32_t split;           // CTAs per threadblock (instances x lanes)
+  int32_t elt;             // element bytes
+  int32_t dtype;           // taccl_dtype_t
+  int64_t chunk_elems;     // c_e
+  int64_t granule;         // piece boundaries are multiples of this many elements
+  int64_t scratch_off;     // byte offset of the EF scratch buffer inside every arena
+  int64_t staging_off;     // byte offset of the rrc staging area inside every arena
+  uint64_t timeout_ns;
+};
+
+constexpr int kThreads = 512;
+
+// executor.cu
+int launch_executor(const KArgs& a, int grid, void* stream, std::string* err);
+int executor_max_ctas(int device, std::string* err);  // co-resident CTA capacity
+
+}  // namespace taccl

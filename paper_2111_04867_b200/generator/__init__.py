@@ -1,0 +1,21 @@
+"""Offline CPU schedule generator: template and greedy algorithms lowered
+to EF v1 text (docs/SCHEDULE.md). Not on the timed path."""
+from .algorithm import Algorithm, Transfer  # noqa: F401
+from .lowering import LoweringError, lower  # noqa: F401
+from . import templates  # noqa: F401
+
+
+def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), **kw):
+    """EF v1 text for (collective, algorithm) — the one-call entry the CLI and tests use."""
+    if algo == "hier":
+        if nranks % 2:
+            raise ValueError("hier needs 2 x k ranks")
+        fn = {"allgather": templates.hier_allgather, "alltoall": templates.hier_alltoall}[coll]
+        alg = fn(nranks // 2, chunks, **kw)
+    elif algo == "greedy":
+        from .greedy import synthesize
+        alg = synthesize(coll, nranks, chunks, **kw)
+    else:
+        alg = templates.TEMPLATES[(coll, algo)](nranks, chunks)
+    name = f"{alg.name}_m{instances}"
+    return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name)
