@@ -245,7 +245,11 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
   while (lr + 1 < A.nlocal && (int)blockIdx.x >= A.r[lr + 1].cta_begin) ++lr;
   const KRank& R = A.r[lr];
   const int local = blockIdx.x - R.cta_begin;
-  Ctx c{&A, &R, local / A.split, local % A.split, 0};
+  // CTA (t, c0) runs pieces j = c0, c0 + C, ... of threadblock t, each piece's whole program
+  // before the next (every CTA visits pieces in increasing order, so a wait on piece j only
+  // ever depends on piece-j work of CTAs that have finished all their pieces < j).
+  Ctx c{&A, &R, local / A.ctas_per_tb, 0, 0};
+  const int c0 = local % A.ctas_per_tb;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
@@ -258,97 +262,100 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
   u64* my_data = reinterpret_cast<u64*>(R.arena + kOffData);
   u64* my_ready = reinterpret_cast<u64*>(R.arena + kOffReady);
   u64* my_done = reinterpret_cast<u64*>(R.arena + kOffDone);
-  // entry handshake: tell our sender we are in this call (its stores may now land)
-  if (tb.recv >= 0 && tid == 0) {
-    u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
-    st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, c.j), c.epoch);
-  }
-  bool sender_ready = false;
-  int64_t lo, hi;
-  piece(A, c.j, &lo, &hi);
   const int64_t ce = A.chunk_elems;
   const int elt = A.elt;
+  const int64_t cbytes = ce * elt;
 
-  for (int k = 0; k < tb.nsteps; ++k) {
-    const KStep st = R.steps[tb.step_begin + k];
-    if (tid == 0) {
-      bool ok = true;
-      for (int d = 0; d < st.dep_count && ok; ++d) {
-        const int dt = R.deps[2 * (st.dep_begin + d)], dk = R.deps[2 * (st.dep_begin + d) + 1];
-        ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + c.j, E | (u64)(dk + 1), A.timeout_ns);
-      }
-      if (ok && st.op == K_SEND && !sender_ready) {
-        ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, c.j), c.epoch, A.timeout_ns);
-        sender_ready = true;
-      }
-      if (ok && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRC_FUSED))
-        ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, c.j), E | (u64)(st.seq + 1), A.timeout_ns);
-      if (ok && st.op == K_RRC_FUSED) {
-        for (int f = 0; f < st.fuse_count && ok; ++f) {
-          const int* fz = R.fused + 3 * (st.fuse_begin + f);
-          const KTB o = R.tbs[fz[0]];
-          ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, c.j), E | (u64)(fz[1] + 1), A.timeout_ns);
-        }
-      }
-      if (!ok) {
-        record_error(c, st.op, k);
-        s_abort = 1;
-      }
+  for (int j = c0; j < A.split; j += A.ctas_per_tb) {
+    c.j = j;
+    // entry handshake: tell our sender we are in this call (its stores may now land)
+    if (tb.recv >= 0 && tid == 0) {
+      u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
+      st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
     }
-    __syncthreads();
-    if (s_abort) return;
-
-    // pieces: one contiguous range when split == 1, else piece j of each of the cnt chunks
-    const int npieces = A.split == 1 ? 1 : st.cnt;
-    const int64_t pbytes = A.split == 1 ? (int64_t)st.cnt * ce * elt : (hi - lo) * elt;
+    bool sender_ready = false;
+    int64_t lo, hi;
+    piece(A, j, &lo, &hi);
+    // one contiguous range when split == 1, else piece j of each of the step's cnt chunks
     const int64_t p0 = A.split == 1 ? 0 : lo * elt;
-    const int64_t cbytes = ce * elt;
-    switch (st.op) {
-      case K_SEND: {
-        const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
-        char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes + p0;
-        for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
-        break;
-      }
-      case K_CPY: {
-        const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
-        char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
-        for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
-        break;
-      }
-      case K_RRC:
-      case K_RRC_FUSED: {
-        if (tid == 0) {
+
+    for (int k = 0; k < tb.nsteps; ++k) {
+      const KStep st = R.steps[tb.step_begin + k];
+      if (tid == 0) {
+        bool ok = true;
+        for (int d = 0; d < st.dep_count && ok; ++d) {
+          const int dt = R.deps[2 * (st.dep_begin + d)], dk = R.deps[2 * (st.dep_begin + d) + 1];
+          ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
+        }
+        if (ok && st.op == K_SEND && !sender_ready) {
+          ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
+          sender_ready = true;
+        }
+        if (ok && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRC_FUSED))
+          ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
+        if (ok && st.op == K_RRC_FUSED) {
+          for (int f = 0; f < st.fuse_count && ok; ++f) {
+            const int* fz = R.fused + 3 * (st.fuse_begin + f);
+            const KTB o = R.tbs[fz[0]];
+            ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
+          }
+        }
+        if (ok && (st.op == K_RRC || st.op == K_RRC_FUSED)) {
           int ns = 0;
           if (st.op == K_RRC_FUSED)
             for (int f = 0; f < st.fuse_count; ++f)
               s_stage[ns++] = local_base(c, KB_STAGE) + (int64_t)R.fused[3 * (st.fuse_begin + f) + 2] * cbytes + p0;
           s_stage[ns] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes + p0;
         }
-        __syncthreads();
-        const int ns = (st.op == K_RRC_FUSED ? st.fuse_count : 0) + 1;
-        const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
-        char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
-        for (int q = 0; q < npieces; ++q)
-          reduce_dispatch(A.dtype, dst + q * cbytes, src + q * cbytes, s_stage, ns, q * cbytes, pbytes / elt);
-        break;
+        if (!ok) {
+          record_error(c, st.op, k);
+          s_abort = 1;
+        }
       }
-      default:  // K_RECV, K_NOP, K_RECV_ONLY: no data work on this side
-        break;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      if (st.op == K_SEND) {
-        __threadfence_system();
-        u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
-        st_relaxed_sys(data + flag_slot(R.rank, tb.chan, c.j), E | (u64)(st.seq + 1));
+      __syncthreads();
+      if (s_abort) return;
+
+      const int npieces = A.split == 1 ? 1 : st.cnt;
+      const int64_t pbytes = A.split == 1 ? (int64_t)st.cnt * cbytes : (hi - lo) * elt;
+      switch (st.op) {
+        case K_SEND: {
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
+          char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes + p0;
+          for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
+          break;
+        }
+        case K_CPY: {
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
+          char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
+          for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
+          break;
+        }
+        case K_RRC:
+        case K_RRC_FUSED: {
+          const int ns = (st.op == K_RRC_FUSED ? st.fuse_count : 0) + 1;
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
+          char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
+          for (int q = 0; q < npieces; ++q)
+            reduce_dispatch(A.dtype, dst + q * cbytes, src + q * cbytes, s_stage, ns, q * cbytes, pbytes / elt);
+          break;
+        }
+        default:  // K_RECV, K_NOP, K_RECV_ONLY: no data work on this side
+          break;
       }
-      if (st.need_done) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + c.j, E | (u64)(k + 1));
+      __syncthreads();
+      if (tid == 0) {
+        if (st.op == K_SEND) {
+          __threadfence_system();
+          u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
+          st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)(st.seq + 1));
+        }
+        if (st.need_done) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
+      }
     }
   }
   // completion: the rank's last CTA advances the rank's epoch for the next call
   if (tid == 0) {
-    const unsigned total = (unsigned)R.ntb * (unsigned)A.split;
+    const unsigned total = (unsigned)R.ntb * (unsigned)A.ctas_per_tb;
     unsigned prev;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctrl->finished) : "memory");
     if (prev == total - 1) {

@@ -85,6 +85,7 @@ struct Comm {
 };
 
 Comm g;
+uint64_t g_launches = 0;  // process lifetime (survives taccl_comm_destroy)
 
 int elt_size(taccl_dtype_t d) { return d == TACCL_BFLOAT16 ? 2 : 4; }
 
@@ -172,7 +173,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S) {
 
 struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, granule = 1;
-  int split = 1, grid = 0;
+  int split = 1, ctas_per_tb = 1, grid = 0;
   int64_t scratch_off = 0, staging_off = 0, need = 0;
 };
 
@@ -205,7 +206,10 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   }
   G->split = a->instances * lanes;
   if (G->split > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances x lanes exceeds TACCL_MAX_SPLIT");
-  G->grid = total_tb * G->split;
+  // every CTA of the launch must be co-resident (they wait on each other): pieces beyond the
+  // device's capacity are run one after another by the same CTA
+  G->ctas_per_tb = std::max(1, std::min(G->split, g.max_ctas / std::max(1, total_tb)));
+  G->grid = total_tb * G->ctas_per_tb;
   if (G->grid > g.max_ctas)
     return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
                                            std::to_string(g.max_ctas));
@@ -226,6 +230,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   memset(&A, 0, sizeof(A));
   A.nlocal = (int)ranks.size();
   A.split = G.split;
+  A.ctas_per_tb = G.ctas_per_tb;
   A.elt = elt;
   A.dtype = dtype;
   A.chunk_elems = G.ce;
@@ -252,11 +257,12 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     R.rank = r;
     R.ntb = dp.ntb;
     R.cta_begin = cta;
-    cta += dp.ntb * G.split;
+    cta += dp.ntb * G.ctas_per_tb;
   }
   std::string err;
   if (launch_executor(A, cta, stream, &err)) return fail(TACCL_ERR_CUDA, err);
   ++g.launches;
+  ++g_launches;
   return TACCL_SUCCESS;
 }
 
@@ -610,6 +616,6 @@ taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dt
   return TACCL_SUCCESS;
 }
 
-uint64_t taccl_launch_count(void) { return g.launches; }
+uint64_t taccl_launch_count(void) { return g_launches; }
 
 }  // extern "C"

@@ -152,7 +152,8 @@ struct KRank {
 struct KArgs {
   KRank r[kMaxRanks];
   int32_t nlocal;          // local ranks in this launch
-  int32_t split;           // CTAs per threadblock (instances x lanes)
+  int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
+  int32_t ctas_per_tb;     // CTAs per threadblock (<= split); CTA c runs pieces c, c+C, ...
   int32_t elt;             // element bytes
   int32_t dtype;           // taccl_dtype_t
   int64_t chunk_elems;     // c_e
