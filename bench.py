@@ -1,0 +1,287 @@
+#!/usr/bin/env python
+"""Benchmark of the TACCL-schedule executor (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl taccl|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1, one rank per GPU)
+
+A step is one collective call = one launch of the whole hot path (SURVEY.md §8(a) a0–a8).
+  N = 1: Allgather with one rank = the local copy path, 1 GiB bf16 output (north star
+         "1 GPU (local copy path vs HBM roofline)"); value = read+write bytes / time.
+  N > 1: Allgather, direct (all-pairs, uc-max) schedule, 1 GiB bf16 output, one process per
+         GPU, peers' HBM mapped with CUDA IPC; value = aggregate bus bandwidth over all ranks
+         (N x nccl-tests busbw, busbw = S/t x (N-1)/N); busbw per GPU and its fraction of
+         900 GB/s NVLink are reported beside it.
+Inputs are resident in HBM before the timed region and larger than L2 (126 MB), so no
+flush is needed. Timing: W warm-up calls, barrier + synchronize, K calls between CUDA
+events on the launching stream, synchronize, max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NVLINK_NOMINAL = 900.0     # GB/s per direction per GPU (NVLink 5)
+NVLINK_MEASURED_REF = 770.0  # peer copy per direction, /opt/skills/guides/B200_PROFILING.md
+HBM_FALLBACK = 6650.0      # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="taccl", choices=["taccl", "reference"])
+    ap.add_argument("--size", type=int, default=GIB, help="S: Allgather output bytes")
+    ap.add_argument("--algo", default="direct")
+    ap.add_argument("--chunks", type=int, default=1)
+    ap.add_argument("--instances", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_gpu{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def busbw_factor(coll, n):
+    return 2.0 * (n - 1) / n if coll == "allreduce" else (n - 1) / n
+
+
+def cpu_oracle_baseline(size_bytes, n, algo, seconds=10.0):
+    """The oracle (test infrastructure) as it stands, on a bounded sample of the workload."""
+    import numpy as np
+
+    import oracle
+    from paper_2111_04867_b200.generator import generate
+    from paper_2111_04867_b200.inputs import random_bits
+    sample = min(size_bytes, 256 << 20)
+    count = sample // 2 // n
+    prog = oracle.parse(generate("allgather", algo, n, 1, 1))
+    ins = [random_bits(count, "bfloat16", 2, r) for r in range(n)]
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        outs = oracle.run(prog, ins, "bfloat16")
+        times.append(time.perf_counter() - t0)
+    assert np.array_equal(outs[0][:count], ins[0])
+    t = statistics.median(times)
+    per_rank_bytes = (2 * sample) if n == 1 else sample * busbw_factor("allgather", n)
+    value = per_rank_bytes * n / t / 1e9
+    return {"value": round(value, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"Allgather n={n} {algo} schedule, {sample >> 20} MiB output bf16 (of {size_bytes >> 20} MiB), "
+                      f"median of {len(times)} runs of oracle.run (NumPy, single thread)",
+            "host_cores_available": len(os.sched_getaffinity(0))}
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n = world if world > 1 else a.gpus
+    if n != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE {world}")
+    coll = "allgather"
+    S = a.size
+    workload = (f"allgather n=1 local copy path, {S >> 20} MiB bf16" if n == 1 else
+                f"allgather {a.algo} schedule n={n} p={a.chunks} m={a.instances}, {S >> 20} MiB output bf16")
+    metric = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+
+    if a.impl == "reference":
+        # reference arm = the oracle (no runnable reference exists: /root/reference is a paper)
+        if rank != 0:
+            return
+        steps = a.steps or 3
+        cpu = cpu_oracle_baseline(S, n, a.algo, seconds=max(2.0, 2.0 * (steps + a.warmup)))
+        line = {"impl": "reference", "metric": metric, "value": cpu["value"], "unit": "GB/s", "n_gpus": n,
+                "steps": steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": workload + " (oracle, bounded sample)", "l2": "inputs > L2"},
+                "cpu_baseline": cpu, "e2e": {"value": cpu["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                             "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_04867_b200 import taccl
+    from paper_2111_04867_b200.generator import generate
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    count = S // 2 // n  # bf16 elements per rank
+    scratch = (2 * S + (64 << 20)) if not a.no_e2e else (64 << 20)
+    comm = taccl.Comm(rank=rank, nranks=n, device=local_rank, scratch_bytes=scratch)
+    comm.load(generate(coll, a.algo if n > 1 else "direct", n, a.chunks, a.instances))
+    g = torch.Generator(device="cuda").manual_seed(211104867 + rank)
+    inp = torch.randint(-32768, 32767, (count,), dtype=torch.int16, device="cuda", generator=g).view(torch.bfloat16)
+    out = torch.empty(n * count, dtype=torch.bfloat16, device="cuda")
+    comm.register(out)
+    stream = torch.cuda.current_stream()
+    steps = a.steps or (1000 if n == 1 else 400)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, a.warmup)):
+        comm.all_gather(out, inp)
+    barrier()
+    comm.check()
+    # correctness of what we time (sampled): own chunk and one peer chunk
+    ref = torch.randint(-32768, 32767, (count,), dtype=torch.int16, device="cuda",
+                        generator=torch.Generator(device="cuda").manual_seed(211104867 + (rank + 1) % n)).view(torch.bfloat16)
+    assert torch.equal(out[rank * count:(rank + 1) * count], inp)
+    assert torch.equal(out[((rank + 1) % n) * count:((rank + 1) % n + 1) * count], ref)
+
+    launches0 = taccl.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(steps):
+            comm.all_gather(out, inp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = taccl.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    comm.check()
+    t_step = ms / 1e3 / steps
+    if n == 1:
+        per_rank_bytes = 2.0 * S
+        value = per_rank_bytes / t_step / 1e9
+        peak, src = hbm_peak()
+        roof = {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(value / peak, 4), "peak_source": src}
+        busbw = None
+    else:
+        busbw = S / t_step * busbw_factor(coll, n) / 1e9
+        value = n * busbw
+        egress = S * (n - 1) / n  # algorithmic NVLink bytes per launch per GPU
+        ach = egress / t_step / 1e9
+        roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_NOMINAL, "unit": "GB/s",
+                "frac": round(ach / NVLINK_NOMINAL, 4),
+                "peak_source": f"nominal NVLink 5 per direction (north star); guide-measured peer copy {NVLINK_MEASURED_REF}"}
+    roof["traffic"] = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        roof["traffic"] = json.load(open(tr_path)).get(f"n{n}_{S}")
+    roof["kernel"] = "taccl_exec_kernel"
+
+    # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not a.no_e2e:
+        h_in = inp.cpu().pin_memory()
+        h_out = torch.empty(n * count, dtype=torch.bfloat16).pin_memory()
+        comm.run_host("allgather", h_out, h_in)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            comm.run_host("allgather", h_out, h_in)
+        barrier()
+        te = (time.perf_counter() - t0) / a.e2e_steps
+        if world > 1:
+            t = torch.tensor([te], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        assert torch.equal(h_out[rank * count:(rank + 1) * count], h_in)
+        ev = (2.0 * S if n == 1 else n * S * busbw_factor(coll, n)) / te / 1e9
+        e2e = {"value": round(ev, 2), "unit": "GB/s", "h2d_bytes_per_step": count * 2,
+               "d2h_bytes_per_step": n * count * 2, "ms_per_step": round(te * 1e3, 3),
+               "timing": "host wall clock around taccl_run_host (H2D + kernel + D2H + stream sync), max over ranks"}
+
+    if rank == 0:
+        line = {"metric": metric, "value": round(value, 2), "unit": "GB/s", "n_gpus": n, "steps": steps,
+                "warmup": a.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": workload, "size_bytes": S, "algo": a.algo if n > 1 else "copy",
+                           "chunks_per_rank": a.chunks, "instances": a.instances,
+                           "plan": comm.plan_info("allgather", count, taccl.BFLOAT16),
+                           "l2": "inputs and outputs > 126 MB L2 (no flush needed)",
+                           "value_definition": ("read+write bytes / t (local copy path)" if n == 1 else
+                                                "aggregate busbw = N * S/t * (N-1)/N")},
+                "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
+        if busbw is not None:
+            line["busbw_per_gpu"] = round(busbw, 2)
+            line["busbw_frac_of_900"] = round(busbw / NVLINK_NOMINAL, 4)
+        if n == 1 and not a.no_cpu:
+            line["cpu_baseline"] = cpu_oracle_baseline(S, n, "direct")
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+    comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
