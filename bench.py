@@ -182,7 +182,7 @@ def main():
     out = torch.empty(n * count, dtype=torch.bfloat16, device="cuda")
     comm.register(out)
     stream = torch.cuda.current_stream()
-    steps = a.steps or (1000 if n == 1 else 400)
+    steps = a.steps or (6000 if n == 1 else 2500)  # timed region >= ~2 s for the clock samples
 
     def barrier():
         if world > 1:
@@ -196,8 +196,9 @@ def main():
     # correctness of what we time (sampled): own chunk and one peer chunk
     ref = torch.randint(-32768, 32767, (count,), dtype=torch.int16, device="cuda",
                         generator=torch.Generator(device="cuda").manual_seed(211104867 + (rank + 1) % n)).view(torch.bfloat16)
-    assert torch.equal(out[rank * count:(rank + 1) * count], inp)
-    assert torch.equal(out[((rank + 1) % n) * count:((rank + 1) % n + 1) * count], ref)
+    ob = out.view(torch.int16)  # compare raw bits (random patterns include NaNs)
+    assert torch.equal(ob[rank * count:(rank + 1) * count], inp.view(torch.int16))
+    assert torch.equal(ob[((rank + 1) % n) * count:((rank + 1) % n + 1) * count], ref.view(torch.int16))
 
     launches0 = taccl.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -253,7 +254,7 @@ def main():
             t = torch.tensor([te], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        assert torch.equal(h_out[rank * count:(rank + 1) * count], h_in)
+        assert torch.equal(h_out.view(torch.int16)[rank * count:(rank + 1) * count], h_in.view(torch.int16))
         ev = (2.0 * S if n == 1 else n * S * busbw_factor(coll, n)) / te / 1e9
         e2e = {"value": round(ev, 2), "unit": "GB/s", "h2d_bytes_per_step": count * 2,
                "d2h_bytes_per_step": n * count * 2, "ms_per_step": round(te * 1e3, 3),

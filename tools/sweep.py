@@ -1,0 +1,157 @@
+#!/usr/bin/env python
+"""1 KB - 1 GB sweep of our executor vs NCCL (via torch.distributed) on the same box.
+
+  torchrun --nproc-per-node N tools/sweep.py [--colls allgather,alltoall,allreduce]
+           [--min 10 --max 30] [--out gpurun_out/sweep_nN.jsonl]
+
+Per size: barrier, 5 warm-up calls, I = max(20, ~50 ms worth) calls between CUDA events on
+the launching stream; t = elapsed / I; max over ranks (SURVEY.md §8(d) timing protocol).
+S convention (reading G8): AG output bytes, A2A per-rank send bytes, AR buffer bytes.
+busbw = S/t x (n-1)/n (AG, A2A) or 2(n-1)/n (AR); at n = 1 we report 2S/t (copy path).
+Every our-side result is checked (bit-exact for AG/A2A, int-valued AR) once per size.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2111_04867_b200 import taccl  # noqa: E402
+from paper_2111_04867_b200.generator import generate  # noqa: E402
+
+ALGOS = {"allgather": ["direct", "ring"], "alltoall": ["direct"], "allreduce": ["direct", "ring"]}
+
+
+def factor(coll, n):
+    if n == 1:
+        return 2.0
+    return 2.0 * (n - 1) / n if coll == "allreduce" else (n - 1) / n
+
+
+def timeit(fn, stream, world, target_ms=50.0):
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(5):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    est = max(e0.elapsed_time(e1) / 5, 1e-3)
+    iters = int(max(20, min(2000, target_ms / est)))
+    if world > 1:
+        t = torch.tensor([iters], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        iters = int(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(iters):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--colls", default="allgather,alltoall,allreduce")
+    ap.add_argument("--min", type=int, default=10)
+    ap.add_argument("--max", type=int, default=30)
+    ap.add_argument("--dtype", default="bfloat16")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--no-nccl", action="store_true")
+    a = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S_max = 1 << a.max
+    comm = taccl.Comm(rank=rank, nranks=n, device=local, scratch_bytes=S_max + (64 << 20))
+    dt = torch.bfloat16 if a.dtype == "bfloat16" else torch.float32
+    es = 2 if dt == torch.bfloat16 else 4
+    # buffers sized for the largest message; registered once (zero-copy)
+    big_in = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
+    big_out = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
+    comm.register(big_out)
+    stream = torch.cuda.current_stream()
+    out_f = open(a.out or os.path.join(ROOT, "gpurun_out", f"sweep_n{n}.jsonl"), "a") if rank == 0 else None
+    for coll in a.colls.split(","):
+        algos = ALGOS[coll] if n > 1 else ["direct"]
+        handles = {al: comm.load(generate(coll, al, n, 1, 1)) for al in algos}
+        for k in range(a.min, a.max + 1):
+            S = 1 << k
+            if coll == "allgather":
+                count = S // es // n
+                inp, out = big_in[:count], big_out[:n * count]
+            elif coll == "alltoall":
+                count = S // es // n
+                inp, out = big_in[:n * count], big_out[:n * count]
+            else:
+                count = S // es
+                inp, out = big_in[:count], big_out[:count]
+            if count == 0 or (coll != "allgather" and count % n):
+                continue
+            inp.copy_(torch.randint(-8, 8, inp.shape, device="cuda").to(dt))
+            rec = {"coll": coll, "n": n, "S": S, "dtype": a.dtype}
+            for al in algos:
+                # select this algorithm: load order decides (latest wins) -> reload on top
+                comm.free(handles[al])
+                handles[al] = comm.load(generate(coll, al, n, 1, 1))
+                ms, it = timeit(lambda: comm.run(coll, out, inp), stream, world)
+                rec[f"taccl_{al}_us"] = round(ms * 1e3, 3)
+                rec[f"taccl_{al}_busbw"] = round(S / (ms / 1e3) * factor(coll, n) / 1e9, 2)
+                # check once (bits for AG/A2A, int-valued sum for AR)
+                if coll == "allgather" and n > 1:
+                    ok = torch.equal(out[rank * count:(rank + 1) * count].view(torch.int16 if es == 2 else torch.int32),
+                                     inp.view(torch.int16 if es == 2 else torch.int32))
+                    rec[f"taccl_{al}_ok"] = bool(ok)
+            comm.check()
+            if n > 1 and not a.no_nccl:
+                if coll == "allgather":
+                    f = lambda: dist.all_gather_into_tensor(out, inp)  # noqa: E731
+                elif coll == "alltoall":
+                    f = lambda: dist.all_to_all_single(out, inp)  # noqa: E731
+                else:
+                    f = lambda: dist.all_reduce(out, op=dist.ReduceOp.SUM)  # noqa: E731
+                ms, it = timeit(f, stream, world)
+                rec["nccl_us"] = round(ms * 1e3, 3)
+                rec["nccl_busbw"] = round(S / (ms / 1e3) * factor(coll, n) / 1e9, 2)
+            elif n == 1:
+                ms, it = timeit(lambda: out.copy_(inp), stream, world)
+                rec["torch_copy_us"] = round(ms * 1e3, 3)
+                rec["torch_copy_gbs"] = round(S / (ms / 1e3) * 2 / 1e9, 2)
+            best = min((rec[f"taccl_{al}_us"], al) for al in algos)
+            rec["taccl_best"] = best[1]
+            rec["taccl_best_us"] = best[0]
+            rec["taccl_best_busbw"] = rec[f"taccl_{best[1]}_busbw"]
+            if "nccl_us" in rec:
+                rec["speedup_vs_nccl"] = round(rec["nccl_us"] / best[0], 3)
+            if rank == 0:
+                print(json.dumps(rec), flush=True)
+                out_f.write(json.dumps(rec) + "\n")
+        for h in handles.values():
+            comm.free(h)
+    comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
