@@ -52,7 +52,7 @@ typedef struct taccl_algo* taccl_algo_t;
 /* Hard limits of this build (taccl_load_algo rejects larger programs with UNSUPPORTED). */
 #define TACCL_MAX_RANKS 8    /* one NVSwitch domain of 8 B200s                        */
 #define TACCL_MAX_CHAN 16    /* channels per (peer, direction)                         */
-#define TACCL_MAX_SPLIT 128  /* instances x lanes per threadblock                      */
+#define TACCL_MAX_SPLIT 512  /* pieces per chunk (instances x lanes)                   */
 #define TACCL_MAX_TB 64      /* threadblocks per rank in one schedule                  */
 #define TACCL_HANDLE_BYTES 128 /* size of one exported handle blob                     */
 

@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
       __syncthreads();
       if (tid == 0) {
         if (st.op == K_SEND) {
-          __threadfence_system();
+          // all threads' peer stores are ordered before this by bar.sync (causality order);
+          // the system-scope acq_rel fence makes them visible before the flag (cumulativity)
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)(st.seq + 1));
         }

@@ -195,14 +195,15 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   int lanes = 1;
   const size_t forced = env_size("TACCL_LANES", 0);
   const int64_t min_piece = (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
-  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", 296));
+  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", g.max_ctas));
   if (forced) {
     lanes = (int)forced;
   } else {
+    // as many pieces as keep every piece >= min_piece, up to `target` CTAs in total
     const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes / a->instances;
-    while (lanes * 2 * a->instances <= kMaxSplit && total_tb * a->instances * lanes * 2 <= target &&
-           step_bytes / (lanes * 2) >= min_piece)
-      lanes *= 2;
+    const int64_t by_bytes = std::max<int64_t>(1, step_bytes / min_piece);
+    const int by_ctas = std::max(1, target / std::max(1, total_tb * a->instances));
+    lanes = (int)std::max<int64_t>(1, std::min<int64_t>({by_bytes, (int64_t)by_ctas, (int64_t)(kMaxSplit / a->instances)}));
   }
   G->split = a->instances * lanes;
   if (G->split > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances x lanes exceeds TACCL_MAX_SPLIT");
