@@ -218,11 +218,22 @@ __device__ __forceinline__ char* remote_base(const Ctx& c, int peer, int buf) {
   }
 }
 
-// Element range [lo, hi) of piece j inside one chunk (same rule on every rank).
-__device__ __forceinline__ void piece(const KArgs& a, int j, int64_t* lo, int64_t* hi) {
-  const int64_t ng = a.chunk_elems / a.granule;
-  *lo = (int64_t)j * ng / a.split * a.granule;
-  *hi = (int64_t)(j + 1) * ng / a.split * a.granule;
+// Byte ranges of piece j inside a step of `cnt` chunks (same rule on every rank): with one
+// piece the step is one contiguous range; otherwise every chunk is cut into stripes of
+// A.stripe bytes and piece j owns stripes j, j + split, ... of each chunk, so at any moment
+// all CTAs of a threadblock stream through one window of memory.
+template <typename F>
+__device__ __forceinline__ void for_piece(const KArgs& a, int j, int cnt, int64_t cbytes, F&& f) {
+  if (a.split == 1) {
+    f((int64_t)0, (int64_t)cnt * cbytes);
+    return;
+  }
+  const int64_t nb = (cbytes + a.stripe - 1) / a.stripe;
+  for (int q = 0; q < cnt; ++q)
+    for (int64_t b = j; b < nb; b += a.split) {
+      const int64_t off = b * a.stripe;
+      f((int64_t)q * cbytes + off, min(a.stripe, cbytes - off));
+    }
 }
 
 __device__ void record_error(const Ctx& c, int what, int step) {
@@ -262,9 +273,8 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
   u64* my_data = reinterpret_cast<u64*>(R.arena + kOffData);
   u64* my_ready = reinterpret_cast<u64*>(R.arena + kOffReady);
   u64* my_done = reinterpret_cast<u64*>(R.arena + kOffDone);
-  const int64_t ce = A.chunk_elems;
   const int elt = A.elt;
-  const int64_t cbytes = ce * elt;
+  const int64_t cbytes = A.chunk_elems * elt;
 
   for (int j = c0; j < A.split; j += A.ctas_per_tb) {
     c.j = j;
@@ -274,10 +284,6 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
       st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
     }
     bool sender_ready = false;
-    int64_t lo, hi;
-    piece(A, j, &lo, &hi);
-    // one contiguous range when split == 1, else piece j of each of the step's cnt chunks
-    const int64_t p0 = A.split == 1 ? 0 : lo * elt;
 
     for (int k = 0; k < tb.nsteps; ++k) {
       const KStep st = R.steps[tb.step_begin + k];
@@ -304,8 +310,8 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
           int ns = 0;
           if (st.op == K_RRC_FUSED)
             for (int f = 0; f < st.fuse_count; ++f)
-              s_stage[ns++] = local_base(c, KB_STAGE) + (int64_t)R.fused[3 * (st.fuse_begin + f) + 2] * cbytes + p0;
-          s_stage[ns] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes + p0;
+              s_stage[ns++] = local_base(c, KB_STAGE) + (int64_t)R.fused[3 * (st.fuse_begin + f) + 2] * cbytes;
+          s_stage[ns] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
         }
         if (!ok) {
           record_error(c, st.op, k);
@@ -315,28 +321,27 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
       __syncthreads();
       if (s_abort) return;
 
-      const int npieces = A.split == 1 ? 1 : st.cnt;
-      const int64_t pbytes = A.split == 1 ? (int64_t)st.cnt * cbytes : (hi - lo) * elt;
       switch (st.op) {
         case K_SEND: {
-          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
-          char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes + p0;
-          for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+          char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
+          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(dst + off, src + off, len); });
           break;
         }
         case K_CPY: {
-          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
-          char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
-          for (int q = 0; q < npieces; ++q) cta_copy(dst + q * cbytes, src + q * cbytes, pbytes);
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+          char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(dst + off, src + off, len); });
           break;
         }
         case K_RRC:
         case K_RRC_FUSED: {
           const int ns = (st.op == K_RRC_FUSED ? st.fuse_count : 0) + 1;
-          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes + p0;
-          char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes + p0;
-          for (int q = 0; q < npieces; ++q)
-            reduce_dispatch(A.dtype, dst + q * cbytes, src + q * cbytes, s_stage, ns, q * cbytes, pbytes / elt);
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+          char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+            reduce_dispatch(A.dtype, dst + off, src + off, s_stage, ns, off, len / elt);
+          });
           break;
         }
         default:  // K_RECV, K_NOP, K_RECV_ONLY: no data work on this side

@@ -172,7 +172,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S) {
 }
 
 struct Geometry {
-  int64_t ce = 0, chunk_bytes = 0, granule = 1;
+  int64_t ce = 0, chunk_bytes = 0, stripe = 0;
   int split = 1, ctas_per_tb = 1, grid = 0;
   int64_t scratch_off = 0, staging_off = 0, need = 0;
 };
@@ -187,7 +187,6 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
                                            std::to_string(n_in) + " equal chunks (reading G2)");
   G->ce = e_in / n_in;
   G->chunk_bytes = G->ce * elt;
-  G->granule = (G->chunk_bytes % 16 == 0) ? 16 / elt : 1;
   // lanes: extra CTAs per threadblock on top of the schedule's instances (same split rule)
   int total_tb = 0;
   for (int r = 0; r < a->nranks; ++r)
@@ -206,6 +205,14 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
     lanes = (int)std::max<int64_t>(1, std::min<int64_t>({by_bytes, (int64_t)by_ctas, (int64_t)(kMaxSplit / a->instances)}));
   }
   G->split = a->instances * lanes;
+  // stripes: a power of two (<= TACCL_STRIPE, default 64 KiB) that also divides the chunk
+  // when possible, so every stripe starts cache-line / page aligned
+  int64_t gb = elt;
+  while (gb < 4096 && G->chunk_bytes % (gb * 2) == 0) gb *= 2;
+  const int64_t smax = (int64_t)env_size("TACCL_STRIPE", 64 << 10);
+  int64_t st = gb;
+  while (st * 2 <= smax && st * 2 * G->split <= G->chunk_bytes) st *= 2;
+  G->stripe = st;
   if (G->split > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances x lanes exceeds TACCL_MAX_SPLIT");
   // every CTA of the launch must be co-resident (they wait on each other): pieces beyond the
   // device's capacity are run one after another by the same CTA
@@ -235,7 +242,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.elt = elt;
   A.dtype = dtype;
   A.chunk_elems = G.ce;
-  A.granule = G.granule;
+  A.stripe = G.stripe;
   A.scratch_off = G.scratch_off;
   A.staging_off = G.staging_off;
   A.timeout_ns = g.timeout_ns;

@@ -157,7 +157,7 @@ struct KArgs {
   int32_t elt;             // element bytes
   int32_t dtype;           // taccl_dtype_t
   int64_t chunk_elems;     // c_e
-  int64_t granule;         // piece boundaries are multiples of this many elements
+  int64_t stripe;          // bytes per stripe of a chunk (pieces own every split-th stripe)
   int64_t scratch_off;     // byte offset of the EF scratch buffer inside every arena
   int64_t staging_off;     // byte offset of the rrc staging area inside every arena
   uint64_t timeout_ns;
