@@ -194,7 +194,8 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   int lanes = 1;
   const size_t forced = env_size("TACCL_LANES", 0);
   const int64_t min_piece = (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
-  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", g.max_ctas));
+  // 128 CTAs x 512 threads measured best for both the HBM copy and NVLink pushes (profiles/r01_scan.txt)
+  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", 128));
   if (forced) {
     lanes = (int)forced;
   } else {
