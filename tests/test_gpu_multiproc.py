@@ -69,8 +69,8 @@ CASES = [
     ("allgather", "direct", 1, 1, "bfloat16", 1 << 16, None),
     ("allgather", "ring", 2, 2, "int32", 2 * 50001, None),
     ("alltoall", "direct", 2, 4, "bfloat16", 2 * 7777, None),
-    ("allreduce", "direct", 1, 1, "int32", 2 * 300001, "bits"),
-    ("allreduce", "ring", 2, 1, "bfloat16", 4 * 4099, "intval"),
+    ("allreduce", "direct", 1, 1, "int32", 4 * 300001, "bits"),
+    ("allreduce", "ring", 2, 1, "bfloat16", 8 * 4099, "intval"),
     ("allreduce", "direct", 1, 2, "float32", 2 * (1 << 18), "intval"),
     ("allgather", "direct", 1, 1, "bfloat16", 3, None),
 ]
