@@ -247,7 +247,7 @@ __device__ void record_error(const Ctx& c, int what, int step) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_constant__ KArgs A) {
   __shared__ int s_abort;
   __shared__ u64 s_epoch;
   __shared__ const char* s_stage[kMaxRanks + 1];
@@ -297,22 +297,17 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
           ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
           sender_ready = true;
         }
-        if (ok && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRC_FUSED))
+        if (ok && (st.op == K_RECV || st.op == K_RRC))
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
-        if (ok && st.op == K_RRC_FUSED) {
+        if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
             const int* fz = R.fused + 3 * (st.fuse_begin + f);
             const KTB o = R.tbs[fz[0]];
             ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
+            s_stage[f] = local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
           }
         }
-        if (ok && (st.op == K_RRC || st.op == K_RRC_FUSED)) {
-          int ns = 0;
-          if (st.op == K_RRC_FUSED)
-            for (int f = 0; f < st.fuse_count; ++f)
-              s_stage[ns++] = local_base(c, KB_STAGE) + (int64_t)R.fused[3 * (st.fuse_begin + f) + 2] * cbytes;
-          s_stage[ns] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
-        }
+        if (ok && st.op == K_RRC) s_stage[0] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
         if (!ok) {
           record_error(c, st.op, k);
           s_abort = 1;
@@ -334,21 +329,40 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
           for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(dst + off, src + off, len); });
           break;
         }
-        case K_RRC:
-        case K_RRC_FUSED: {
-          const int ns = (st.op == K_RRC_FUSED ? st.fuse_count : 0) + 1;
+        case K_RRC: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) {
-            reduce_dispatch(A.dtype, dst + off, src + off, s_stage, ns, off, len / elt);
+            reduce_dispatch(A.dtype, dst + off, src + off, s_stage, 1, off, len / elt);
           });
           break;
         }
-        default:  // K_RECV, K_NOP, K_RECV_ONLY: no data work on this side
+        case K_RRC_FUSED: {  // this member's portion of each range (16-byte aligned cuts)
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+          char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+          const int64_t unit = (cbytes % 16 == 0) ? 16 : elt;
+          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+            const int64_t nu = len / unit;
+            const int64_t a = off + nu * st.part / st.nparts * unit;
+            const int64_t b = (st.part + 1 == st.nparts) ? off + len : off + nu * (st.part + 1) / st.nparts * unit;
+            if (b > a) reduce_dispatch(A.dtype, dst + a, src + a, s_stage, st.fuse_count, a, (b - a) / elt);
+          });
+          break;
+        }
+        default:  // K_RECV, K_NOP: no data work on this side
           break;
       }
       __syncthreads();
       if (tid == 0) {
+        bool ok = true;  // post-dependencies: the other members of a fused chain
+        for (int d = 0; d < st.post_count && ok; ++d) {
+          const int dt = R.deps[2 * (st.post_begin + d)], dk = R.deps[2 * (st.post_begin + d) + 1];
+          ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
+        }
+        if (!ok) {
+          record_error(c, st.op, k);
+          s_abort = 1;
+        }
         if (st.op == K_SEND) {
           // all threads' peer stores are ordered before this by bar.sync (causality order);
           // the system-scope acq_rel fence makes them visible before the flag (cumulativity)
@@ -356,7 +370,11 @@ __global__ void __launch_bounds__(kThreads, 2) taccl_exec_kernel(const __grid_co
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)(st.seq + 1));
         }
-        if (st.need_done) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
+        if (st.need_done && ok) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
+      }
+      if (st.post_count) {
+        __syncthreads();
+        if (s_abort) return;
       }
     }
   }

@@ -27,6 +27,102 @@ bool overlap(BufId b1, int o1, int c1, BufId b2, int o2, int c2) {
 
 }  // namespace
 
+// rrc chain fusion (R3 in DESIGN.md). A chain X_1..X_K becomes K cooperating K_RRC_FUSED
+// steps: each member waits for all K staged inputs, reduces its 1/K portion of every piece
+// (dst = src(X_1) + stage_1 + ... + stage_K, chain order), and X_K publishes completion
+// only after every member's portion (post-dependencies). The chain edges between members
+// are dropped; every member inherits X_1's incoming edges (its tb predecessor and deps; the
+// matched send is covered by waiting on X_1's data flag), so whatever happened before X_1
+// happens before every member, and whatever followed X_K still follows all of them.
+void fuse_chains(const Gpu& g, const HB& hb, const std::map<std::pair<int, int>, int>& flat, RankPlan& rp,
+                 std::vector<std::vector<std::pair<int, int>>>& deps,
+                 std::vector<std::vector<std::pair<int, int>>>& post) {
+  auto step_of = [&](int t, int k) -> const Step& { return g.tbs[t].steps[k]; };
+  auto direct_pred = [&](int t, int k, int t2, int k2) {  // (t,k) directly precedes (t2,k2)?
+    if (t == t2 && k + 1 == k2) return true;
+    for (auto [dt, dk] : step_of(t2, k2).deps)
+      if (dt == t && dk == k) return true;
+    return false;
+  };
+  std::vector<std::pair<int, int>> rrcs;
+  for (const TB& tb : g.tbs)
+    for (const Step& st : tb.steps)
+      if (st.type == ST_RRC) rrcs.emplace_back(tb.id, st.s);
+  std::map<std::pair<int, int>, std::pair<int, int>> next, prev;
+  for (auto x : rrcs) {
+    const Step& a = step_of(x.first, x.second);
+    std::vector<std::pair<int, int>> cand;
+    for (auto y : rrcs) {
+      if (y == x) continue;
+      const Step& b = step_of(y.first, y.second);
+      if (b.srcbuf == a.dstbuf && b.srcoff == a.dstoff && b.dstbuf == a.dstbuf && b.dstoff == a.dstoff &&
+          b.cnt == a.cnt && direct_pred(x.first, x.second, y.first, y.second))
+        cand.push_back(y);
+    }
+    if (cand.size() == 1 && !prev.count(cand[0])) {
+      next[x] = cand[0];
+      prev[cand[0]] = x;
+    }
+  }
+  for (auto head : rrcs) {
+    if (prev.count(head) || !next.count(head)) continue;
+    std::vector<std::pair<int, int>> chain{head};
+    while (next.count(chain.back()) && (int)chain.size() < kMaxRanks) chain.push_back(next[chain.back()]);
+    const Step& first = step_of(head.first, head.second);
+    const auto last = chain.back();
+    const Step& lastst = step_of(last.first, last.second);
+    // legality: other accesses to the destination (any) or to first's source (writes)
+    bool ok = true;
+    for (const TB& tb : g.tbs) {
+      for (const Step& st : tb.steps) {
+        if (std::find(chain.begin(), chain.end(), std::make_pair(tb.id, st.s)) != chain.end()) continue;
+        bool touches = overlap(st.srcbuf, st.srcoff, st.cnt, lastst.dstbuf, lastst.dstoff, lastst.cnt) ||
+                       overlap(st.dstbuf, st.dstoff, st.cnt, lastst.dstbuf, lastst.dstoff, lastst.cnt) ||
+                       overlap(st.dstbuf, st.dstoff, st.cnt, first.srcbuf, first.srcoff, first.cnt);
+        if (!touches) continue;
+        // For an `r` (bytes land while its peer's send runs) "after the chain" is enough:
+        // the direct-store check already ordered the chain's last step before that send.
+        const int r = g.id;
+        const bool before_first = hb.before(r, tb.id, st.s, r, head.first, head.second);
+        const bool after_last = hb.before(r, last.first, last.second, r, tb.id, st.s);
+        if (!before_first && !after_last) ok = false;
+      }
+    }
+    if (!ok) continue;
+    // rewrite the members
+    const int K = (int)chain.size();
+    std::vector<std::pair<int, int>> head_in = first.deps;
+    if (head.second > 0) head_in.emplace_back(head.first, head.second - 1);
+    const int fb = (int32_t)rp.fused.size() / 3;
+    for (int i = 0; i < K; ++i) {
+      const KStep& x = rp.steps[flat.at(chain[i])];
+      rp.fused.push_back(chain[i].first);
+      rp.fused.push_back(x.seq);
+      rp.fused.push_back(x.soff);
+    }
+    for (int i = 0; i < K; ++i) {
+      const int fi = flat.at(chain[i]);
+      KStep& x = rp.steps[fi];
+      x.op = K_RRC_FUSED;
+      x.srcbuf = kbuf(first.srcbuf);
+      x.srcoff = first.srcoff;
+      x.fuse_begin = fb;
+      x.fuse_count = K;
+      x.part = i;
+      x.nparts = K;
+      if (i > 0) {
+        auto& d = deps[fi];
+        d.erase(std::remove(d.begin(), d.end(), chain[i - 1]), d.end());
+        for (auto e : head_in)
+          if (e.first != chain[i].first && std::find(d.begin(), d.end(), e) == d.end()) d.push_back(e);
+      }
+    }
+    auto& pl = post[flat.at(last)];
+    for (int i = 0; i + 1 < K; ++i)
+      if (chain[i].first != last.first) pl.push_back(chain[i]);
+  }
+}
+
 std::vector<RankPlan> build_plans(const Program& P, bool fuse) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
@@ -58,6 +154,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse) {
     rp.stage_chunks = stage_total[g.id];
     rp.scratch_chunks = g.s_chunks;
     std::map<std::pair<int, int>, int> flat;  // (tb, step) -> index in rp.steps
+    std::vector<std::vector<std::pair<int, int>>> deps, post;  // per flat step
     for (const TB& tb : g.tbs) {
       KTB kt{tb.send, tb.recv, tb.chan, (int32_t)rp.steps.size(), (int32_t)tb.steps.size()};
       rp.tbs.push_back(kt);
@@ -68,12 +165,8 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse) {
         ks.srcoff = st.srcoff;
         ks.dstoff = st.dstoff;
         ks.cnt = st.cnt;
-        ks.dep_begin = (int32_t)rp.deps.size() / 2;
-        ks.dep_count = (int32_t)st.deps.size();
-        for (auto [dt, dk] : st.deps) {
-          rp.deps.push_back(dt);
-          rp.deps.push_back(dk);
-        }
+        deps.push_back(st.deps);
+        post.emplace_back();
         switch (st.type) {
           case ST_S: {
             ks.op = K_SEND;
@@ -108,78 +201,26 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse) {
         rp.steps.push_back(ks);
       }
     }
-    // need_done: referenced by some dependency
+    if (fuse) fuse_chains(g, hb, flat, rp, deps, post);
+    // flatten dependency lists; need_done: referenced by some (post-)dependency
+    for (size_t i = 0; i < rp.steps.size(); ++i) {
+      KStep& ks = rp.steps[i];
+      ks.dep_begin = (int32_t)rp.deps.size() / 2;
+      ks.dep_count = (int32_t)deps[i].size();
+      for (auto [dt, dk] : deps[i]) {
+        rp.deps.push_back(dt);
+        rp.deps.push_back(dk);
+      }
+      ks.post_begin = (int32_t)rp.deps.size() / 2;
+      ks.post_count = (int32_t)post[i].size();
+      for (auto [dt, dk] : post[i]) {
+        rp.deps.push_back(dt);
+        rp.deps.push_back(dk);
+      }
+    }
     for (size_t d = 0; d + 1 < rp.deps.size(); d += 2) rp.steps[flat.at({rp.deps[d], rp.deps[d + 1]})].need_done = 1;
-
-    if (!fuse) continue;
-    // ---- rrc chain fusion
-    auto step_of = [&](int t, int k) -> const Step& { return g.tbs[t].steps[k]; };
-    auto direct_pred = [&](int t, int k, int t2, int k2) {  // (t,k) directly precedes (t2,k2)?
-      if (t == t2 && k + 1 == k2) return true;
-      for (auto [dt, dk] : step_of(t2, k2).deps)
-        if (dt == t && dk == k) return true;
-      return false;
-    };
-    std::vector<std::pair<int, int>> rrcs;
-    for (const TB& tb : g.tbs)
-      for (const Step& st : tb.steps)
-        if (st.type == ST_RRC) rrcs.emplace_back(tb.id, st.s);
-    std::map<std::pair<int, int>, std::pair<int, int>> next, prev;
-    for (auto x : rrcs) {
-      const Step& a = step_of(x.first, x.second);
-      std::vector<std::pair<int, int>> cand;
-      for (auto y : rrcs) {
-        if (y == x) continue;
-        const Step& b = step_of(y.first, y.second);
-        if (b.srcbuf == a.dstbuf && b.srcoff == a.dstoff && b.dstbuf == a.dstbuf && b.dstoff == a.dstoff &&
-            b.cnt == a.cnt && direct_pred(x.first, x.second, y.first, y.second))
-          cand.push_back(y);
-      }
-      if (cand.size() == 1 && !prev.count(cand[0])) {
-        next[x] = cand[0];
-        prev[cand[0]] = x;
-      }
-    }
-    for (auto head : rrcs) {
-      if (prev.count(head) || !next.count(head)) continue;
-      std::vector<std::pair<int, int>> chain{head};
-      while (next.count(chain.back()) && (int)chain.size() < kMaxRanks) chain.push_back(next[chain.back()]);
-      const Step& first = step_of(head.first, head.second);
-      const auto last = chain.back();
-      const Step& lastst = step_of(last.first, last.second);
-      // legality: other accesses to the destination (any) or to first's source (writes)
-      bool ok = true;
-      for (const TB& tb : g.tbs) {
-        for (const Step& st : tb.steps) {
-          if (std::find(chain.begin(), chain.end(), std::make_pair(tb.id, st.s)) != chain.end()) continue;
-          bool touches = overlap(st.srcbuf, st.srcoff, st.cnt, lastst.dstbuf, lastst.dstoff, lastst.cnt) ||
-                         overlap(st.dstbuf, st.dstoff, st.cnt, lastst.dstbuf, lastst.dstoff, lastst.cnt) ||
-                         overlap(st.dstbuf, st.dstoff, st.cnt, first.srcbuf, first.srcoff, first.cnt);
-          if (!touches) continue;
-          // For an `r` (bytes land while its peer's send runs) "after the chain" is enough:
-          // the direct-store check already ordered the chain's last step before that send.
-          const int r = g.id;
-          const bool before_first = hb.before(r, tb.id, st.s, r, head.first, head.second);
-          const bool after_last = hb.before(r, last.first, last.second, r, tb.id, st.s);
-          if (!before_first && !after_last) ok = false;
-        }
-      }
-      if (!ok) continue;
-      KStep& fused = rp.steps[flat.at(last)];
-      fused.op = K_RRC_FUSED;
-      fused.srcbuf = kbuf(first.srcbuf);
-      fused.srcoff = first.srcoff;
-      fused.fuse_begin = (int32_t)rp.fused.size() / 3;
-      fused.fuse_count = (int32_t)chain.size() - 1;
-      for (size_t i = 0; i + 1 < chain.size(); ++i) {
-        KStep& x = rp.steps[flat.at(chain[i])];
-        rp.fused.push_back(chain[i].first);
-        rp.fused.push_back(x.seq);
-        rp.fused.push_back(x.soff);
-        x.op = K_RECV_ONLY;
-      }
-      ++rp.fused_chains;
-    }
+    rp.fused_chains = (int)std::count_if(rp.steps.begin(), rp.steps.end(),
+                                         [](const KStep& k) { return k.op == K_RRC_FUSED && k.part == 0; });
   }
   return plans;
 }

@@ -76,8 +76,8 @@ enum KOp : int8_t {
   K_RRC = 2,       // wait data flag, dst = src + staging
   K_CPY = 3,       // local copy
   K_NOP = 4,       // deps only
-  K_RRC_FUSED = 5, // wait all chain flags, dst = src + sum(staging_i) in fp32 (bf16) / dtype
-  K_RECV_ONLY = 6  // rrc absorbed into a later fused step: no data work, no flag wait
+  K_RRC_FUSED = 5  // chain member: wait all chain flags, reduce its portion of
+                   // dst = src + sum(staging_i) (fp32 accumulation for bf16)
 };
 enum KBuf : int8_t { KB_I = 0, KB_O = 1, KB_S = 2, KB_STAGE = 3 };
 
@@ -90,7 +90,9 @@ struct KStep {
   int32_t seq;            // message index on the tb's connection (K_SEND/K_RECV/K_RRC)
   int32_t soff;           // K_RRC: this rank's staging offset (chunk units)
   int32_t dep_begin, dep_count;  // into KRankPlan.deps (pairs tb, step)
-  int32_t fuse_begin, fuse_count;  // K_RRC_FUSED: into KRankPlan.fused (tb, seq, soff) triples
+  int32_t fuse_begin, fuse_count;  // K_RRC_FUSED: chain members' (tb, seq, soff), chain order
+  int32_t part, nparts;   // K_RRC_FUSED: this member reduces portion `part` of `nparts`
+  int32_t post_begin, post_count;  // deps waited AFTER the work, before publishing done
   int32_t need_done;      // some step depends on this one
 };
 
