@@ -29,10 +29,13 @@ class Algorithm:
     chunks_per_rank: int   # p ("chunk partitioning")
     transfers: list = field(default_factory=list)
 
-    def add(self, chunks, src, dst, t, lat=1.0, reduce=False):
+    def add(self, chunks, src, dst, t, lat=1.0, reduce=False, arrive=None):
+        """`arrive` (default t + lat) must equal the send_time of any later forward of the
+        same chunk exactly: lowering orders a rank's events by these times."""
         if isinstance(chunks, int):
             chunks = (chunks,)
-        self.transfers.append(Transfer(tuple(chunks), src, dst, float(t), float(t) + lat, reduce))
+        a = float(t) + lat if arrive is None else float(arrive)
+        self.transfers.append(Transfer(tuple(chunks), src, dst, float(t), a, reduce))
 
 
 # ---- chunk-id helpers (SPEC.md:142) --------------------------------------------------

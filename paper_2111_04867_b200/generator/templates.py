@@ -103,8 +103,7 @@ def invert_allgather(ag: Algorithm, name=None) -> Algorithm:
     T = max(t.arrive_time for t in ag.transfers)
     rs = Algorithm(name or ag.name.replace("ag_", "rs_"), "allreduce", ag.nranks, ag.chunks_per_rank)
     for t in sorted(ag.transfers, key=lambda t: (-t.arrive_time, t.src, t.dst)):
-        rs.add(t.chunks, t.dst, t.src, T - t.arrive_time, lat=t.arrive_time - t.send_time,
-               reduce=True)
+        rs.add(t.chunks, t.dst, t.src, T - t.arrive_time, reduce=True, arrive=T - t.send_time)
     return rs
 
 
@@ -116,7 +115,7 @@ def allreduce(rs: Algorithm, ag: Algorithm, name) -> Algorithm:
     ar = Algorithm(name, "allreduce", rs.nranks, rs.chunks_per_rank)
     ar.transfers = list(rs.transfers)
     for t in ag.transfers:
-        ar.add(t.chunks, t.src, t.dst, t.send_time + T, lat=t.arrive_time - t.send_time)
+        ar.add(t.chunks, t.src, t.dst, t.send_time + T, arrive=t.arrive_time + T)
     return ar
 
 

@@ -1,0 +1,187 @@
+"""CPU tests of the offline schedule generator (templates, greedy stand-in, lowering).
+Every generated program is checked by the oracle against the collective's definition;
+structural facts are pinned to the paper's statements and SPEC.md's examples."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2111_04867_b200.generator import generate, templates
+from paper_2111_04867_b200.generator.greedy import synthesize, schedule_time
+from paper_2111_04867_b200.generator.topology import (
+    IB_ALPHA_US, IB_BETA_US_PER_MB, Link, Sketch, apply_sketch, multinode, nvswitch, parse_sketch,
+    relay_for_chunk, rotate)
+
+MATRIX = [(c, a, n, p, kw)
+          for c in ("allgather", "alltoall", "allreduce")
+          for a, kw in (("ring", {}), ("direct", {}), ("greedy", {"policy": "uc-max"}),
+                        ("greedy", {"policy": "uc-min"}))
+          for n in (2, 3, 4, 8) for p in (1, 2)
+          if (c, a) != ("alltoall", "ring")]
+MATRIX += [(c, "hier", n, p, {}) for c in ("allgather", "alltoall") for n in (4, 8) for p in (1, 2)]
+MATRIX += [(c, "greedy", 8, p, {"topology": "2x4"}) for c in ("allgather", "alltoall", "allreduce") for p in (1, 2)]
+
+
+@pytest.mark.parametrize("coll,algo,n,p,kw", MATRIX, ids=[f"{m[0]}-{m[1]}-n{m[2]}-p{m[3]}-{m[4]}" for m in MATRIX])
+def test_generated_schedule_is_correct(coll, algo, n, p, kw):
+    text = generate(coll, algo, n, p, 1, **kw)
+    v = oracle.validate(text)
+    assert v.ok, f"{v.kind}: {v.msg}"
+    # numeric spot check against the collective's definition
+    prog = oracle.parse(text)
+    rng = np.random.default_rng(n * 100 + p)
+    count = (n * p if coll != "allgather" else p) * 3
+    e_in = n * count if coll == "alltoall" else count
+    ins = [rng.integers(-1000, 1000, e_in).astype(np.int32) for _ in range(n)]
+    outs = oracle.run(prog, ins, "int32")
+    want = oracle.expected_outputs(coll, ins, "int32")
+    assert all(np.array_equal(a, b) for a, b in zip(outs, want))
+
+
+def test_generation_is_deterministic():
+    for args in (("allreduce", "greedy", 8, 2, 1), ("alltoall", "hier", 8, 2, 4)):
+        assert generate(*args) == generate(*args)
+
+
+def test_ring_has_n_minus_1_transfer_steps_per_chunk():
+    # "this algorithm requires n-1 link transfer steps per data chunk"
+    for n in (2, 4, 8):
+        alg = templates.ring_allgather(n, 2)
+        per_chunk = {}
+        for t in alg.transfers:
+            for c in t.chunks:
+                per_chunk[c] = per_chunk.get(c, 0) + 1
+        assert set(per_chunk.values()) == {n - 1}
+
+
+def test_uc_min_on_a_3_rank_switch_is_a_ring_uc_max_uses_all_links():
+    # SPEC.md acceptance 8 / PAPER.md:445-452: uc-min -> 3 utilised links forming a cycle,
+    # uc-max -> 6
+    mn = synthesize("allgather", 3, 1, policy="uc-min")
+    mx = synthesize("allgather", 3, 1, policy="uc-max")
+    lmin = {(t.src, t.dst) for t in mn.transfers}
+    lmax = {(t.src, t.dst) for t in mx.transfers}
+    assert len(lmin) == 3 and len(lmax) == 6
+    succ = dict(lmin)
+    x, seen = 0, []
+    for _ in range(3):
+        seen.append(x)
+        x = succ[x]
+    assert x == 0 and sorted(seen) == [0, 1, 2]
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_ring_identity_time(n):
+    # SPEC.md acceptance 2: a uniform ring Allgather takes (n-1)(alpha + beta*s)
+    size = 1 << 20
+    alg = synthesize("allgather", n, 1, policy="uc-min", size=size)
+    lat = Link(0.7, (1 << 20) / 900e9 * 1e6, "nvlink").cost(size / (1 << 20))
+    assert schedule_time(alg.transfers) == pytest.approx((n - 1) * lat, rel=1e-12)
+
+
+@pytest.mark.parametrize("size", [1 << 10, 1 << 20, 1 << 28])
+def test_greedy_never_slower_than_ring_baseline(size):
+    # SPEC.md acceptance 9 (under the same cost model, on a switch)
+    ring = synthesize("allgather", 8, 1, policy="uc-min", size=size)
+    best = min(schedule_time(synthesize("allgather", 8, 1, policy=pol, size=size).transfers)
+               for pol in ("uc-max", "uc-min"))
+    assert best <= schedule_time(ring.transfers) + 1e-9
+
+
+def test_contiguity_saving_matches_the_paper():
+    # PAPER.md:549-551 / SPEC.md acceptance 1: two 32 KB chunks over IB together are ~17% faster
+    ib = Link(IB_ALPHA_US, IB_BETA_US_PER_MB, "ib")
+    apart, together = 2 * ib.cost(32 / 1024), ib.cost(32 / 1024, 2)
+    assert apart == pytest.approx(10.025) and together == pytest.approx(8.325)
+    assert (apart - together) / apart == pytest.approx(0.1696, abs=5e-4)
+
+
+def test_greedy_merges_chunks_on_ib_links():
+    alg = synthesize("alltoall", 8, 2, topology="2x4", size=1 << 16)
+    ib = [t for t in alg.transfers if t.src // 4 != t.dst // 4]
+    assert ib and max(len(t.chunks) for t in ib) > 1
+    assert all(t.src % 4 == t.dst % 4 for t in ib)  # dgx2-sk-2: GPU i <-> GPU i only
+
+
+def test_relay_map_examples():
+    # (r1, r2) = (2, 1): rp=4 -> 5, rp=5 -> 5, rp=0 -> 1
+    sk = Sketch(chunk_to_relay=(2, 1))
+    assert [relay_for_chunk(sk, rp) for rp in (4, 5, 0)] == [5, 5, 1]
+
+
+def test_rotational_symmetry_examples():
+    # SPEC.md:207-209 and PAPER.md:469-473
+    assert rotate(0, 2, 16) == 2 and rotate(1, 2, 16) == 3
+    assert rotate(0, 16, 32) == 16 and rotate(16, 16, 32) == 0
+    assert rotate(0, 8, 16) == 8 and rotate(8, 8, 16) == 0    # Example 3: 0->1 implies 8->9
+    for o, g in ((2, 16), (16, 32), (3, 8)):
+        r = 5
+        for _ in range(g // math.gcd(o, g)):
+            r = rotate(r, o, g)
+        assert r == 5
+
+
+LISTING1 = """{
+    // sketch for intra-node policy
+    "intranode_sketch": {"strategy": "switch", "switches": [[0,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15]],
+                         "switch_hyperedge_strategy": ["uc-min"]},
+    "internode_sketch": {"strategy": "relay",
+        "internode_conn": {"1" : [0], "3" : [2], "5" : [4], "7" : [6], "9" : [8], "11" : [10], "13" : [12], "15" : [14]},
+        "beta_split": {"1": 1, "3": 1, "5": 1, "7" : 1, "9" : 1, "11" : 1, "13" : 1, "15" : 1},
+        "chunk_to_relay_map": [2,1]},
+    "symmetry_offsets": [[2, 16], [16, 32]],
+    "hyperparameters": {"input_chunkup": 2, "input_size": "1M"}
+}"""
+
+
+def test_listing1_sketch_parses_and_prunes():
+    # PAPER.md:1289-1315
+    sk = parse_sketch(LISTING1)
+    assert sk.policy == "uc-min" and sk.input_chunkup == 2 and sk.input_size == 1 << 20
+    assert sk.internode_conn[1] == [0] and sk.chunk_to_relay == (2, 1)
+    assert sk.symmetry_offsets == [(2, 16), (16, 32)]
+    lt = apply_sketch(multinode(2, 16), sk)
+    inter = [(u, v) for (u, v) in lt.links if u // 16 != v // 16]
+    senders = {u for u, _ in inter}
+    assert len([u for u in senders if u < 16]) == 8 and all(u % 2 == 1 for u in senders)
+    assert all(sum(1 for (a, _) in inter if a == u) == 1 for u in senders)
+    with pytest.raises(ValueError):
+        parse_sketch('{"symmetry_offsets": [[0, 16]]}')
+
+
+def test_listing1_sketch_synthesizes_a_correct_allgather():
+    sk = parse_sketch(LISTING1)
+    alg = synthesize("allgather", 32, 2, topology=multinode(2, 16), sketch=sk)
+    from paper_2111_04867_b200.generator.lowering import lower
+    v = oracle.validate(lower(alg))
+    assert v.ok, v.msg
+    inter = [t for t in alg.transfers if t.src // 16 != t.dst // 16]
+    assert all(t.src % 2 == 1 and t.dst % 2 == 0 for t in inter)   # relays: odd -> even
+    # symmetric routing: every chunk crosses nodes exactly once
+    crossings = {}
+    for t in inter:
+        for c in t.chunks:
+            crossings[c] = crossings.get(c, 0) + 1
+    assert set(crossings.values()) == {1} and len(crossings) == 64
+
+
+def test_lowering_threadblock_rule_and_own_copy():
+    # PAPER.md:750, 781-783 (one send peer, one recv peer per tb) and 768-769 (own copy)
+    prog = oracle.parse(generate("allgather", "greedy", 8, 2, 1))
+    for g in prog.gpus:
+        cpy = [s for tb in g.tbs for s in tb.steps if s.type == "cpy"]
+        assert len(cpy) == 1 and cpy[0].srcbuf == "i" and cpy[0].dstoff == g.id * 2
+        for tb in g.tbs:
+            assert all(s.type != "s" or tb.send >= 0 for s in tb.steps)
+
+
+def test_instances_double_threadblocks_and_halve_chunks():
+    # n=2 instances -> tb count doubles, per-step chunk size halves
+    prog = oracle.parse(generate("allgather", "ring", 4, 1, 2))
+    exp = oracle.expand_instances(prog)
+    assert len(exp.gpus[0].tbs) == 2 * len(prog.gpus[0].tbs)
+    assert exp.gpus[0].o_chunks == 2 * prog.gpus[0].o_chunks
+    ins = [np.arange(8, dtype=np.int32) + 100 * r for r in range(4)]
+    a, b = oracle.run(prog, ins, "int32"), oracle.run(exp, ins, "int32")
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
