@@ -259,8 +259,14 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   // CTA (t, c0) runs pieces j = c0, c0 + C, ... of threadblock t, each piece's whole program
   // before the next (every CTA visits pieces in increasing order, so a wait on piece j only
   // ever depends on piece-j work of CTAs that have finished all their pieces < j).
-  Ctx c{&A, &R, local / A.ctas_per_tb, 0, 0};
-  const int c0 = local % A.ctas_per_tb;
+  int t = 0, ct = 0, acc = 0;
+  for (;; ++t) {
+    ct = tb_ctas(R.tbs[t].weight, R.wsum, R.ntb, R.budget, A.split);
+    if (local < acc + ct || t + 1 == R.ntb) break;
+    acc += ct;
+  }
+  Ctx c{&A, &R, t, 0, 0};
+  const int c0 = local - acc;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   const int elt = A.elt;
   const int64_t cbytes = A.chunk_elems * elt;
 
-  for (int j = c0; j < A.split; j += A.ctas_per_tb) {
+  for (int j = c0; j < A.split; j += ct) {
     c.j = j;
     // entry handshake: tell our sender we are in this call (its stores may now land)
     if (tb.recv >= 0 && tid == 0) {
@@ -380,7 +386,8 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   }
   // completion: the rank's last CTA advances the rank's epoch for the next call
   if (tid == 0) {
-    const unsigned total = (unsigned)R.ntb * (unsigned)A.ctas_per_tb;
+    unsigned total = 0;
+    for (int u = 0; u < R.ntb; ++u) total += tb_ctas(R.tbs[u].weight, R.wsum, R.ntb, R.budget, A.split);
     unsigned prev;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctrl->finished) : "memory");
     if (prev == total - 1) {

@@ -219,6 +219,17 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse) {
       }
     }
     for (size_t d = 0; d + 1 < rp.deps.size(); d += 2) rp.steps[flat.at({rp.deps[d], rp.deps[d + 1]})].need_done = 1;
+    // tb weights: data each tb moves (remote pushes dominate)
+    for (KTB& kt : rp.tbs) {
+      long long w = 0;
+      for (int i = 0; i < kt.nsteps; ++i) {
+        const KStep& ks = rp.steps[kt.step_begin + i];
+        const int f = ks.op == K_SEND ? 4 : ks.op == K_CPY ? 1 : ks.op == K_RRC ? 2 :
+                      ks.op == K_RRC_FUSED ? 1 + ks.fuse_count / std::max(1, ks.nparts) : 0;
+        w += (long long)f * ks.cnt;
+      }
+      kt.weight = (int32_t)std::min<long long>(w, 1 << 20);
+    }
     rp.fused_chains = (int)std::count_if(rp.steps.begin(), rp.steps.end(),
                                          [](const KStep& k) { return k.op == K_RRC_FUSED && k.part == 0; });
   }

@@ -61,6 +61,8 @@ struct Algo {
   int max_scratch_chunks = 0, max_stage_chunks = 0, max_steps_cnt = 1;
   std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
   std::vector<int> ntb;         // per rank
+  std::vector<std::vector<int>> weights;  // per rank, per tb
+  std::vector<int> wsum;        // per rank
   int fused_chains = 0;
 };
 
@@ -173,7 +175,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S) {
 
 struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, stripe = 0;
-  int split = 1, ctas_per_tb = 1, grid = 0;
+  int split = 1, grid = 0, budget = 0;
   int64_t scratch_off = 0, staging_off = 0, need = 0;
 };
 
@@ -194,15 +196,22 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   int lanes = 1;
   const size_t forced = env_size("TACCL_LANES", 0);
   const int64_t min_piece = (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
-  // 128 CTAs x 512 threads measured best for both the HBM copy and NVLink pushes (profiles/r01_scan.txt)
+  // 128 CTAs x 512 threads measured best for the HBM copy and 2-GPU pushes (profiles/r01_scan.txt)
   const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", 128));
+  int nlocal = 0, max_ntb = 1;
+  for (int r = 0; r < a->nranks; ++r)
+    if (a->plans[r].mem) {
+      ++nlocal;
+      max_ntb = std::max(max_ntb, a->ntb[r]);
+    }
+  G->budget = std::max(max_ntb, target / std::max(1, nlocal));
   if (forced) {
     lanes = (int)forced;
   } else {
-    // as many pieces as keep every piece >= min_piece, up to `target` CTAs in total
+    // pieces: enough for the busiest tb's CTAs, each piece >= min_piece
     const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes / a->instances;
     const int64_t by_bytes = std::max<int64_t>(1, step_bytes / min_piece);
-    const int by_ctas = std::max(1, target / std::max(1, total_tb * a->instances));
+    const int by_ctas = std::max(1, (G->budget + a->instances - 1) / a->instances);
     lanes = (int)std::max<int64_t>(1, std::min<int64_t>({by_bytes, (int64_t)by_ctas, (int64_t)(kMaxSplit / a->instances)}));
   }
   G->split = a->instances * lanes;
@@ -217,8 +226,11 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   if (G->split > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances x lanes exceeds TACCL_MAX_SPLIT");
   // every CTA of the launch must be co-resident (they wait on each other): pieces beyond the
   // device's capacity are run one after another by the same CTA
-  G->ctas_per_tb = std::max(1, std::min(G->split, g.max_ctas / std::max(1, total_tb)));
-  G->grid = total_tb * G->ctas_per_tb;
+  G->grid = 0;
+  for (int r = 0; r < a->nranks; ++r)
+    if (a->plans[r].mem)
+      for (int t = 0; t < a->ntb[r]; ++t)
+        G->grid += tb_ctas(a->weights[r][t], a->wsum[r], a->ntb[r], G->budget, G->split);
   if (G->grid > g.max_ctas)
     return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
                                            std::to_string(g.max_ctas));
@@ -239,7 +251,6 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   memset(&A, 0, sizeof(A));
   A.nlocal = (int)ranks.size();
   A.split = G.split;
-  A.ctas_per_tb = G.ctas_per_tb;
   A.elt = elt;
   A.dtype = dtype;
   A.chunk_elems = G.ce;
@@ -266,7 +277,9 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     R.rank = r;
     R.ntb = dp.ntb;
     R.cta_begin = cta;
-    cta += dp.ntb * G.ctas_per_tb;
+    R.budget = G.budget;
+    R.wsum = a->wsum[r];
+    for (int t = 0; t < dp.ntb; ++t) cta += tb_ctas(a->weights[r][t], a->wsum[r], dp.ntb, G.budget, G.split);
   }
   std::string err;
   if (launch_executor(A, cta, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -537,6 +550,13 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
   a->ntb.assign(a->nranks, 0);
   for (int r = 0; r < a->nranks; ++r) {
     a->ntb[r] = (int)plans[r].tbs.size();
+    a->weights.emplace_back();
+    long long ws = 0;
+    for (const KTB& kt : plans[r].tbs) {
+      a->weights.back().push_back(kt.weight);
+      ws += kt.weight;
+    }
+    a->wsum.push_back((int)std::min<long long>(ws, 1 << 30));
     a->max_scratch_chunks = std::max(a->max_scratch_chunks, plans[r].scratch_chunks);
     a->max_stage_chunks = std::max(a->max_stage_chunks, plans[r].stage_chunks);
     a->fused_chains += plans[r].fused_chains;

@@ -99,6 +99,7 @@ struct KStep {
 struct KTB {
   int32_t send, recv, chan;
   int32_t step_begin, nsteps;
+  int32_t weight;  // data volume weight used to share the rank's CTAs among its tbs
 };
 
 // ---------------------------------------------------------------- arena layout (bytes)
@@ -148,14 +149,16 @@ struct KRank {
   char* arena;
   char* peer_out[kMaxRanks];    // peer's output buffer (this call's recvbuf on the peer)
   char* peer_arena[kMaxRanks];  // peer's arena (flags, scratch, staging)
-  int32_t rank, ntb, cta_begin, pad;
+  int32_t rank, ntb, cta_begin;
+  int32_t budget;          // CTAs of this rank: tb t gets tb_ctas(weight_t, wsum, ...)
+  int32_t wsum, pad;
 };
 
 struct KArgs {
   KRank r[kMaxRanks];
   int32_t nlocal;          // local ranks in this launch
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
-  int32_t ctas_per_tb;     // CTAs per threadblock (<= split); CTA c runs pieces c, c+C, ...
+  int32_t pad0;
   int32_t elt;             // element bytes
   int32_t dtype;           // taccl_dtype_t
   int64_t chunk_elems;     // c_e
@@ -166,6 +169,15 @@ struct KArgs {
 };
 
 constexpr int kThreads = 512;
+
+// CTAs of one threadblock (same rule on host and device): every tb gets one, the rest of the
+// rank's budget is shared by data-volume weight; never more CTAs than pieces. CTA c of tb t
+// runs pieces c, c + C_t, ...
+TACCL_HD inline int tb_ctas(int weight, int wsum, int ntb, int budget, int split) {
+  const int extra = budget > ntb ? budget - ntb : 0;
+  const int c = 1 + (wsum > 0 ? (int)((long long)extra * weight / wsum) : 0);
+  return c < split ? c : split;
+}
 
 // executor.cu
 int launch_executor(const KArgs& a, int grid, void* stream, std::string* err);
