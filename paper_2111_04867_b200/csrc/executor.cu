@@ -72,21 +72,29 @@ __device__ bool wait_ge(const u64* p, u64 target, u64 timeout_ns) {
 }
 
 // ---------------------------------------------------------------- CTA-wide data movement
-constexpr int kUnroll = 8;
+__device__ __forceinline__ void st_v4_cs(int4* p, int4 v) {
+  asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 
-__device__ void cta_copy(char* __restrict__ dst, const char* __restrict__ src, int64_t n) {
+// U 16-byte vectors in flight per thread; CS: streaming (evict-first) stores
+template <int U, bool CS>
+__device__ __noinline__ void cta_copy_t(char* __restrict__ dst, const char* __restrict__ src, int64_t n) {
   const int tid = threadIdx.x, nt = blockDim.x;
   if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
     const int64_t nv = n >> 4;
     const int4* s = reinterpret_cast<const int4*>(src);
     int4* d = reinterpret_cast<int4*>(dst);
     int64_t i = tid;
-    for (; i + (int64_t)(kUnroll - 1) * nt < nv; i += (int64_t)kUnroll * nt) {
-      int4 v[kUnroll];
+    for (; i + (int64_t)(U - 1) * nt < nv; i += (int64_t)U * nt) {
+      int4 v[U];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = ld_cg(s + i + (int64_t)u * nt);
+      for (int u = 0; u < U; ++u) v[u] = ld_cg(s + i + (int64_t)u * nt);
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) st_v4(d + i + (int64_t)u * nt, v[u]);
+      for (int u = 0; u < U; ++u) {
+        if (CS) st_v4_cs(d + i + (int64_t)u * nt, v[u]);
+        else st_v4(d + i + (int64_t)u * nt, v[u]);
+      }
     }
     for (; i < nv; i += nt) st_v4(d + i, ld_cg(s + i));
     for (int64_t b = (nv << 4) + tid; b < n; b += nt) dst[b] = src[b];
@@ -98,6 +106,16 @@ __device__ void cta_copy(char* __restrict__ dst, const char* __restrict__ src, i
     for (int64_t b = (nw << 2) + tid; b < n; b += nt) dst[b] = src[b];
   } else {
     for (int64_t b = tid; b < n; b += nt) dst[b] = src[b];
+  }
+}
+
+// copy variants (KArgs.variant, env TACCL_COPY_VARIANT; profiles/r01_scan.txt)
+__device__ __forceinline__ void cta_copy(int variant, char* dst, const char* src, int64_t n) {
+  switch (variant) {
+    case 1: cta_copy_t<4, false>(dst, src, n); break;
+    case 2: cta_copy_t<16, false>(dst, src, n); break;
+    case 3: cta_copy_t<8, true>(dst, src, n); break;
+    default: cta_copy_t<8, false>(dst, src, n); break;
   }
 }
 
@@ -160,7 +178,7 @@ struct Elt<TACCL_BFLOAT16> {
 };
 
 template <int DT>
-__device__ void cta_reduce(char* dst, const char* src0, const char* const* stages, int ns,
+__device__ __noinline__ void cta_reduce(char* dst, const char* src0, const char* const* stages, int ns,
                            int64_t soff, int64_t nelem) {
   using E = Elt<DT>;
   constexpr int V = E::V;
@@ -326,13 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
         case K_SEND: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
-          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(dst + off, src + off, len); });
+          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
         case K_CPY: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(dst + off, src + off, len); });
+          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
         case K_RRC: {

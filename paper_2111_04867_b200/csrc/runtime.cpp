@@ -255,6 +255,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.dtype = dtype;
   A.chunk_elems = G.ce;
   A.stripe = G.stripe;
+  A.variant = (int)env_size("TACCL_COPY_VARIANT", 0);
   A.scratch_off = G.scratch_off;
   A.staging_off = G.staging_off;
   A.timeout_ns = g.timeout_ns;

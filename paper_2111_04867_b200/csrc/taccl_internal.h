@@ -158,7 +158,7 @@ struct KArgs {
   KRank r[kMaxRanks];
   int32_t nlocal;          // local ranks in this launch
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
-  int32_t pad0;
+  int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT)
   int32_t elt;             // element bytes
   int32_t dtype;           // taccl_dtype_t
   int64_t chunk_elems;     // c_e
