@@ -114,8 +114,8 @@ __device__ __forceinline__ void cta_copy(int variant, char* dst, const char* src
   switch (variant) {
     case 1: cta_copy_t<4, false>(dst, src, n); break;
     case 2: cta_copy_t<16, false>(dst, src, n); break;
-    case 3: cta_copy_t<8, true>(dst, src, n); break;
-    default: cta_copy_t<8, false>(dst, src, n); break;
+    case 3: cta_copy_t<8, false>(dst, src, n); break;
+    default: cta_copy_t<8, true>(dst, src, n); break;
   }
 }
 
@@ -178,15 +178,44 @@ struct Elt<TACCL_BFLOAT16> {
 };
 
 template <int DT>
-__device__ __noinline__ void cta_reduce(char* dst, const char* src0, const char* const* stages, int ns,
-                           int64_t soff, int64_t nelem) {
+__device__ __noinline__ void cta_reduce(char* dst, char* dst2, const char* src0, const char* const* stages,
+                                        int ns, int64_t soff, int64_t nelem) {
+  // dst (and dst2, the forward destination of a fused rrc+send, when non-null) =
+  // src0 + stages[0] + ... ; RU vectors per thread in flight per input
   using E = Elt<DT>;
-  constexpr int V = E::V;
+  constexpr int V = E::V, RU = 4;
   const int tid = threadIdx.x, nt = blockDim.x;
-  uintptr_t align = (uintptr_t)dst | (uintptr_t)src0;
+  uintptr_t align = (uintptr_t)dst | (uintptr_t)src0 | (uintptr_t)dst2;
   for (int s = 0; s < ns; ++s) align |= (uintptr_t)(stages[s] + soff);
   const int64_t nv = (align & 15) ? 0 : nelem / V;
-  for (int64_t v = tid; v < nv; v += nt) {
+  int64_t v = tid;
+  for (; v + (int64_t)(RU - 1) * nt < nv; v += (int64_t)RU * nt) {
+    typename E::acc acc[RU][V], in[V];
+    int4 raw[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) raw[u] = ld_cg(reinterpret_cast<const int4*>(src0 + (v + (int64_t)u * nt) * 16));
+#pragma unroll
+    for (int u = 0; u < RU; ++u) E::unpack(raw[u], acc[u]);
+    for (int s = 0; s < ns; ++s) {
+      const char* st = stages[s] + soff;
+#pragma unroll
+      for (int u = 0; u < RU; ++u) raw[u] = ld_cg(reinterpret_cast<const int4*>(st + (v + (int64_t)u * nt) * 16));
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        E::unpack(raw[u], in);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[u][e] = E::add(acc[u][e], in[e]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int4 o = E::pack(acc[u]);
+      const int64_t off = (v + (int64_t)u * nt) * 16;
+      st_v4(reinterpret_cast<int4*>(dst + off), o);
+      if (dst2) st_v4(reinterpret_cast<int4*>(dst2 + off), o);
+    }
+  }
+  for (; v < nv; v += nt) {
     const int64_t off = v * 16;
     typename E::acc acc[V], in[V];
     E::unpack(ld_cg(reinterpret_cast<const int4*>(src0 + off)), acc);
@@ -195,21 +224,24 @@ __device__ __noinline__ void cta_reduce(char* dst, const char* src0, const char*
 #pragma unroll
       for (int e = 0; e < V; ++e) acc[e] = E::add(acc[e], in[e]);
     }
-    st_v4(reinterpret_cast<int4*>(dst + off), E::pack(acc));
+    const int4 o = E::pack(acc);
+    st_v4(reinterpret_cast<int4*>(dst + off), o);
+    if (dst2) st_v4(reinterpret_cast<int4*>(dst2 + off), o);
   }
   for (int64_t e = nv * V + tid; e < nelem; e += nt) {
     const int64_t off = e * E::bytes;
     typename E::acc acc = E::load(src0 + off);
     for (int s = 0; s < ns; ++s) acc = E::add(acc, E::load(stages[s] + soff + off));
     E::store(dst + off, acc);
+    if (dst2) E::store(dst2 + off, acc);
   }
 }
 
-__device__ void reduce_dispatch(int dtype, char* dst, const char* src0, const char* const* stages,
+__device__ void reduce_dispatch(int dtype, char* dst, char* dst2, const char* src0, const char* const* stages,
                                 int ns, int64_t soff, int64_t nelem) {
-  if (dtype == TACCL_INT32) cta_reduce<TACCL_INT32>(dst, src0, stages, ns, soff, nelem);
-  else if (dtype == TACCL_FLOAT32) cta_reduce<TACCL_FLOAT32>(dst, src0, stages, ns, soff, nelem);
-  else cta_reduce<TACCL_BFLOAT16>(dst, src0, stages, ns, soff, nelem);
+  if (dtype == TACCL_INT32) cta_reduce<TACCL_INT32>(dst, dst2, src0, stages, ns, soff, nelem);
+  else if (dtype == TACCL_FLOAT32) cta_reduce<TACCL_FLOAT32>(dst, dst2, src0, stages, ns, soff, nelem);
+  else cta_reduce<TACCL_BFLOAT16>(dst, dst2, src0, stages, ns, soff, nelem);
 }
 
 // ---------------------------------------------------------------- the interpreter
@@ -317,11 +349,11 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           const int dt = R.deps[2 * (st.dep_begin + d)], dk = R.deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
-        if (ok && st.op == K_SEND && !sender_ready) {
+        if (ok && (st.op == K_SEND || st.op == K_RRCS) && !sender_ready) {
           ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
           sender_ready = true;
         }
-        if (ok && (st.op == K_RECV || st.op == K_RRC))
+        if (ok && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS))
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
         if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
@@ -331,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
             s_stage[f] = local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
           }
         }
-        if (ok && st.op == K_RRC) s_stage[0] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
+        if (ok && (st.op == K_RRC || st.op == K_RRCS)) s_stage[0] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
         if (!ok) {
           record_error(c, st.op, k);
           s_abort = 1;
@@ -353,11 +385,13 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
-        case K_RRC: {
+        case K_RRC:
+        case K_RRCS: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+          char* fwd = st.op == K_RRCS ? remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes : nullptr;
           for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) {
-            reduce_dispatch(A.dtype, dst + off, src + off, s_stage, 1, off, len / elt);
+            reduce_dispatch(A.dtype, dst + off, fwd ? fwd + off : nullptr, src + off, s_stage, 1, off, len / elt);
           });
           break;
         }
@@ -369,11 +403,11 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
             const int64_t nu = len / unit;
             const int64_t a = off + nu * st.part / st.nparts * unit;
             const int64_t b = (st.part + 1 == st.nparts) ? off + len : off + nu * (st.part + 1) / st.nparts * unit;
-            if (b > a) reduce_dispatch(A.dtype, dst + a, src + a, s_stage, st.fuse_count, a, (b - a) / elt);
+            if (b > a) reduce_dispatch(A.dtype, dst + a, nullptr, src + a, s_stage, st.fuse_count, a, (b - a) / elt);
           });
           break;
         }
-        default:  // K_RECV, K_NOP: no data work on this side
+        default:  // K_RECV, K_NOP, K_SENT: no data work on this side
           break;
       }
       __syncthreads();
@@ -387,12 +421,12 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           record_error(c, st.op, k);
           s_abort = 1;
         }
-        if (st.op == K_SEND) {
+        if (st.op == K_SEND || st.op == K_RRCS) {
           // all threads' peer stores are ordered before this by bar.sync (causality order);
           // the system-scope acq_rel fence makes them visible before the flag (cumulativity)
           asm volatile("fence.acq_rel.sys;" ::: "memory");
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
-          st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)(st.seq + 1));
+          st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)((st.op == K_RRCS ? st.fwd_seq : st.seq) + 1));
         }
         if (st.need_done && ok) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
       }

@@ -123,7 +123,7 @@ void fuse_chains(const Gpu& g, const HB& hb, const std::map<std::pair<int, int>,
   }
 }
 
-std::vector<RankPlan> build_plans(const Program& P, bool fuse) {
+std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
   // per-step seq numbers and staging offsets
@@ -219,12 +219,31 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse) {
       }
     }
     for (size_t d = 0; d + 1 < rp.deps.size(); d += 2) rp.steps[flat.at({rp.deps[d], rp.deps[d + 1]})].need_done = 1;
+    // recv-reduce-copy-send (the fused instruction whose absence the
+    // paper blames for its >=512 MB Allreduce gap): an rrc immediately
+    // followed in its tb by a send of exactly its result, the send waiting on nothing else
+    if (fuse_rrcs) {
+      for (const KTB& kt : rp.tbs) {
+        for (int i = 0; i + 1 < kt.nsteps; ++i) {
+          KStep& a = rp.steps[kt.step_begin + i];
+          KStep& b = rp.steps[kt.step_begin + i + 1];
+          if (a.op == K_RRC && b.op == K_SEND && b.srcbuf == a.dstbuf && b.srcoff == a.dstoff &&
+              b.cnt == a.cnt && b.dep_count == 0 && b.post_count == 0) {
+            a.op = K_RRCS;
+            a.rbuf = b.rbuf;
+            a.roff = b.roff;
+            a.fwd_seq = b.seq;
+            b.op = K_SENT;
+          }
+        }
+      }
+    }
     // tb weights: data each tb moves (remote pushes dominate)
     for (KTB& kt : rp.tbs) {
       long long w = 0;
       for (int i = 0; i < kt.nsteps; ++i) {
         const KStep& ks = rp.steps[kt.step_begin + i];
-        const int f = ks.op == K_SEND ? 4 : ks.op == K_CPY ? 1 : ks.op == K_RRC ? 2 :
+        const int f = ks.op == K_SEND ? 4 : ks.op == K_CPY ? 1 : ks.op == K_RRC ? 2 : ks.op == K_RRCS ? 6 :
                       ks.op == K_RRC_FUSED ? 1 + ks.fuse_count / std::max(1, ks.nparts) : 0;
         w += (long long)f * ks.cnt;
       }

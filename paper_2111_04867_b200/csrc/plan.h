@@ -16,7 +16,8 @@ struct RankPlan {
   int fused_chains = 0;
 };
 
-// `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables).
-std::vector<RankPlan> build_plans(const Program& P, bool fuse);
+// `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables);
+// `fuse_rrcs`: fuse rrc + send-of-its-result into one pass (env TACCL_NO_RRCS=1 disables).
+std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs);
 
 }  // namespace taccl

@@ -536,7 +536,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
       }
     }
     if (P.instances > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances > TACCL_MAX_SPLIT");
-    plans = build_plans(P, env_size("TACCL_NO_FUSE", 0) == 0);
+    plans = build_plans(P, env_size("TACCL_NO_FUSE", 0) == 0, env_size("TACCL_NO_RRCS", 0) == 0);
     a->name = P.name;
     a->coll = P.coll;
     a->nranks = P.nranks;

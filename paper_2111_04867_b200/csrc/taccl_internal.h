@@ -76,8 +76,11 @@ enum KOp : int8_t {
   K_RRC = 2,       // wait data flag, dst = src + staging
   K_CPY = 3,       // local copy
   K_NOP = 4,       // deps only
-  K_RRC_FUSED = 5  // chain member: wait all chain flags, reduce its portion of
+  K_RRC_FUSED = 5, // chain member: wait all chain flags, reduce its portion of
                    // dst = src + sum(staging_i) (fp32 accumulation for bf16)
+  K_RRCS = 6,      // rrc fused with the next step's send of its result (recv-reduce-copy-send):
+                   // one pass writes dst locally and the send's destination on the peer
+  K_SENT = 7       // a send already performed (and published) by the preceding K_RRCS
 };
 enum KBuf : int8_t { KB_I = 0, KB_O = 1, KB_S = 2, KB_STAGE = 3 };
 
@@ -86,7 +89,8 @@ struct KStep {
   int8_t srcbuf, dstbuf;  // KBuf
   int8_t rbuf;            // K_SEND: destination buffer on the peer (KB_O / KB_S / KB_STAGE)
   int32_t srcoff, dstoff, cnt;  // chunk units
-  int32_t roff;           // K_SEND: destination offset on the peer (chunk units)
+  int32_t roff;           // K_SEND/K_RRCS: destination offset on the peer (chunk units)
+  int32_t fwd_seq;        // K_RRCS: message index of the fused send
   int32_t seq;            // message index on the tb's connection (K_SEND/K_RECV/K_RRC)
   int32_t soff;           // K_RRC: this rank's staging offset (chunk units)
   int32_t dep_begin, dep_count;  // into KRankPlan.deps (pairs tb, step)
