@@ -273,14 +273,14 @@ __device__ __forceinline__ char* remote_base(const Ctx& c, int peer, int buf) {
 // A.stripe bytes and piece j owns stripes j, j + split, ... of each chunk, so at any moment
 // all CTAs of a threadblock stream through one window of memory.
 template <typename F>
-__device__ __forceinline__ void for_piece(const KArgs& a, int j, int cnt, int64_t cbytes, F&& f) {
-  if (a.split == 1) {
+__device__ __forceinline__ void for_piece(const KArgs& a, int j, int split, int cnt, int64_t cbytes, F&& f) {
+  if (split == 1) {
     f((int64_t)0, (int64_t)cnt * cbytes);
     return;
   }
   const int64_t nb = (cbytes + a.stripe - 1) / a.stripe;
   for (int q = 0; q < cnt; ++q)
-    for (int64_t b = j; b < nb; b += a.split) {
+    for (int64_t b = j; b < nb; b += split) {
       const int64_t off = b * a.stripe;
       f((int64_t)q * cbytes + off, min(a.stripe, cbytes - off));
     }
@@ -311,10 +311,11 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   // ever depends on piece-j work of CTAs that have finished all their pieces < j).
   int t = 0, ct = 0, acc = 0;
   for (;; ++t) {
-    ct = tb_ctas(R.tbs[t].weight, R.wsum, R.ntb, R.budget, A.split);
+    ct = R.tbs[t].indep ? tb_pieces(1, R.tbs[t].weight, R.wsum, R.budget, A.split) : A.dep_ctas;
     if (local < acc + ct || t + 1 == R.ntb) break;
     acc += ct;
   }
+  const int nsplit = R.tbs[t].indep ? ct : A.split;  // this tb's piece count
   Ctx c{&A, &R, t, 0, 0};
   const int c0 = local - acc;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   const int elt = A.elt;
   const int64_t cbytes = A.chunk_elems * elt;
 
-  for (int j = c0; j < A.split; j += ct) {
+  for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
     // entry handshake: tell our sender we are in this call (its stores may now land)
     if (tb.recv >= 0 && tid == 0) {
@@ -376,13 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
         case K_SEND: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
-          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
         case K_CPY: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
         case K_RRC:
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           char* fwd = st.op == K_RRCS ? remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes : nullptr;
-          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             reduce_dispatch(A.dtype, dst + off, fwd ? fwd + off : nullptr, src + off, s_stage, 1, off, len / elt);
           });
           break;
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           const int64_t unit = (cbytes % 16 == 0) ? 16 : elt;
-          for_piece(A, j, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             const int64_t nu = len / unit;
             const int64_t a = off + nu * st.part / st.nparts * unit;
             const int64_t b = (st.part + 1 == st.nparts) ? off + len : off + nu * (st.part + 1) / st.nparts * unit;
@@ -439,7 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   // completion: the rank's last CTA advances the rank's epoch for the next call
   if (tid == 0) {
     unsigned total = 0;
-    for (int u = 0; u < R.ntb; ++u) total += tb_ctas(R.tbs[u].weight, R.wsum, R.ntb, R.budget, A.split);
+    for (int u = 0; u < R.ntb; ++u)
+      total += R.tbs[u].indep ? tb_pieces(1, R.tbs[u].weight, R.wsum, R.budget, A.split) : A.dep_ctas;
     unsigned prev;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctrl->finished) : "memory");
     if (prev == total - 1) {

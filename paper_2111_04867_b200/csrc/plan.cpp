@@ -248,6 +248,12 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
         w += (long long)f * ks.cnt;
       }
       kt.weight = (int32_t)std::min<long long>(w, 1 << 20);
+      bool indep = kt.send < 0 && kt.recv < 0;
+      for (int i = 0; i < kt.nsteps && indep; ++i) {
+        const KStep& ks = rp.steps[kt.step_begin + i];
+        indep = ks.dep_count == 0 && ks.post_count == 0 && !ks.need_done;
+      }
+      kt.indep = indep;
     }
     rp.fused_chains = (int)std::count_if(rp.steps.begin(), rp.steps.end(),
                                          [](const KStep& k) { return k.op == K_RRC_FUSED && k.part == 0; });

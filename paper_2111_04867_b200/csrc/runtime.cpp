@@ -62,6 +62,7 @@ struct Algo {
   std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
   std::vector<int> ntb;         // per rank
   std::vector<std::vector<int>> weights;  // per rank, per tb
+  std::vector<std::vector<int>> indep;    // per rank, per tb
   std::vector<int> wsum;        // per rank
   int fused_chains = 0;
 };
@@ -175,7 +176,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S) {
 
 struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, stripe = 0;
-  int split = 1, grid = 0, budget = 0;
+  int split = 1, grid = 0, budget = 0, dep_ctas = 1;
   int64_t scratch_off = 0, staging_off = 0, need = 0;
 };
 
@@ -198,20 +199,28 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   const int64_t min_piece = (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
   // 128 CTAs x 512 threads measured best for the HBM copy and 2-GPU pushes (profiles/r01_scan.txt)
   const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", 128));
-  int nlocal = 0, max_ntb = 1;
+  int nlocal = 0;
   for (int r = 0; r < a->nranks; ++r)
-    if (a->plans[r].mem) {
-      ++nlocal;
-      max_ntb = std::max(max_ntb, a->ntb[r]);
+    if (a->plans[r].mem) ++nlocal;
+  G->budget = std::max(1, target / std::max(1, nlocal));
+  // CTAs left for the dependent tbs once independent tbs took their weight share
+  int per_dep = kMaxSplit;
+  for (int r = 0; r < a->nranks; ++r) {
+    if (!a->plans[r].mem) continue;
+    int used = 0, ndep = 0;
+    for (int t = 0; t < a->ntb[r]; ++t) {
+      if (a->indep[r][t]) used += tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, 1);
+      else ++ndep;
     }
-  G->budget = std::max(max_ntb, target / std::max(1, nlocal));
+    if (ndep) per_dep = std::min(per_dep, std::max(1, (G->budget - used) / ndep));
+  }
   if (forced) {
     lanes = (int)forced;
   } else {
-    // pieces: enough for the busiest tb's CTAs, each piece >= min_piece
+    // pieces = CTAs of each dependent tb, each piece >= min_piece
     const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes / a->instances;
     const int64_t by_bytes = std::max<int64_t>(1, step_bytes / min_piece);
-    const int by_ctas = std::max(1, (G->budget + a->instances - 1) / a->instances);
+    const int by_ctas = std::max(1, per_dep / a->instances);
     lanes = (int)std::max<int64_t>(1, std::min<int64_t>({by_bytes, (int64_t)by_ctas, (int64_t)(kMaxSplit / a->instances)}));
   }
   G->split = a->instances * lanes;
@@ -226,11 +235,12 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   if (G->split > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances x lanes exceeds TACCL_MAX_SPLIT");
   // every CTA of the launch must be co-resident (they wait on each other): pieces beyond the
   // device's capacity are run one after another by the same CTA
+  G->dep_ctas = std::min(G->split, per_dep);
   G->grid = 0;
   for (int r = 0; r < a->nranks; ++r)
     if (a->plans[r].mem)
       for (int t = 0; t < a->ntb[r]; ++t)
-        G->grid += tb_ctas(a->weights[r][t], a->wsum[r], a->ntb[r], G->budget, G->split);
+        G->grid += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, G->split) : G->dep_ctas;
   if (G->grid > g.max_ctas)
     return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
                                            std::to_string(g.max_ctas));
@@ -251,6 +261,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   memset(&A, 0, sizeof(A));
   A.nlocal = (int)ranks.size();
   A.split = G.split;
+  A.dep_ctas = G.dep_ctas;
   A.elt = elt;
   A.dtype = dtype;
   A.chunk_elems = G.ce;
@@ -280,7 +291,8 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     R.cta_begin = cta;
     R.budget = G.budget;
     R.wsum = a->wsum[r];
-    for (int t = 0; t < dp.ntb; ++t) cta += tb_ctas(a->weights[r][t], a->wsum[r], dp.ntb, G.budget, G.split);
+    for (int t = 0; t < dp.ntb; ++t)
+      cta += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G.budget, G.split) : G.dep_ctas;
   }
   std::string err;
   if (launch_executor(A, cta, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -552,9 +564,11 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
   for (int r = 0; r < a->nranks; ++r) {
     a->ntb[r] = (int)plans[r].tbs.size();
     a->weights.emplace_back();
+    a->indep.emplace_back();
     long long ws = 0;
     for (const KTB& kt : plans[r].tbs) {
       a->weights.back().push_back(kt.weight);
+      a->indep.back().push_back(kt.indep);
       ws += kt.weight;
     }
     a->wsum.push_back((int)std::min<long long>(ws, 1 << 30));

@@ -104,6 +104,7 @@ struct KTB {
   int32_t send, recv, chan;
   int32_t step_begin, nsteps;
   int32_t weight;  // data volume weight used to share the rank's CTAs among its tbs
+  int32_t indep;   // no peers and no dependencies in or out: may use its own piece count
 };
 
 // ---------------------------------------------------------------- arena layout (bytes)
@@ -163,6 +164,7 @@ struct KArgs {
   int32_t nlocal;          // local ranks in this launch
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
   int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT)
+  int32_t dep_ctas;        // CTAs per dependent tb (<= split; CTA c runs pieces c, c+dep_ctas, ...)
   int32_t elt;             // element bytes
   int32_t dtype;           // taccl_dtype_t
   int64_t chunk_elems;     // c_e
@@ -174,13 +176,14 @@ struct KArgs {
 
 constexpr int kThreads = 512;
 
-// CTAs of one threadblock (same rule on host and device): every tb gets one, the rest of the
-// rank's budget is shared by data-volume weight; never more CTAs than pieces. CTA c of tb t
-// runs pieces c, c + C_t, ...
-TACCL_HD inline int tb_ctas(int weight, int wsum, int ntb, int budget, int split) {
-  const int extra = budget > ntb ? budget - ntb : 0;
-  const int c = 1 + (wsum > 0 ? (int)((long long)extra * weight / wsum) : 0);
-  return c < split ? c : split;
+// Pieces of one threadblock = its CTAs (same rule on host and device). Dependent tbs share
+// the launch-wide split (a dependency or a connection pairs piece j with piece j); an
+// independent tb (e.g. the own-chunk copy) gets its own count from its data-volume share
+// of the rank's CTA budget.
+TACCL_HD inline int tb_pieces(int indep, int weight, int wsum, int budget, int split) {
+  if (!indep) return split;  // (run by min(split, KArgs.dep_ctas) CTAs)
+  long long c = wsum > 0 ? (long long)budget * weight / wsum : 1;
+  return c < 1 ? 1 : c > kMaxSplit ? kMaxSplit : (int)c;
 }
 
 // executor.cu

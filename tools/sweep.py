@@ -2,7 +2,7 @@
 """1 KB - 1 GB sweep of our executor vs NCCL (via torch.distributed) on the same box.
 
   torchrun --nproc-per-node N tools/sweep.py [--colls allgather,alltoall,allreduce]
-           [--min 10 --max 30] [--out gpurun_out/sweep_nN.jsonl]
+           [--size-lo 10 --size-hi 30] [--out gpurun_out/sweep_nN.jsonl]
 
 Per size: barrier, 5 warm-up calls, I = max(20, ~50 ms worth) calls between CUDA events on
 the launching stream; t = elapsed / I; max over ranks (SURVEY.md §8(d) timing protocol).
@@ -69,8 +69,8 @@ def timeit(fn, stream, world, target_ms=50.0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--colls", default="allgather,alltoall,allreduce")
-    ap.add_argument("--min", type=int, default=10)
-    ap.add_argument("--max", type=int, default=30)
+    ap.add_argument("--size-lo", type=int, default=10, help="smallest size 2^lo bytes")
+    ap.add_argument("--size-hi", type=int, default=30, help="largest size 2^hi bytes")
     ap.add_argument("--dtype", default="bfloat16")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-nccl", action="store_true")
@@ -82,7 +82,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    S_max = 1 << a.max
+    S_max = 1 << a.size_hi
     comm = taccl.Comm(rank=rank, nranks=n, device=local, scratch_bytes=S_max + (64 << 20))
     dt = torch.bfloat16 if a.dtype == "bfloat16" else torch.float32
     es = 2 if dt == torch.bfloat16 else 4
@@ -95,7 +95,7 @@ def main():
     for coll in a.colls.split(","):
         algos = ALGOS[coll] if n > 1 else ["direct"]
         handles = {al: comm.load(generate(coll, al, n, 1, 1)) for al in algos}
-        for k in range(a.min, a.max + 1):
+        for k in range(a.size_lo, a.size_hi + 1):
             S = 1 << k
             if coll == "allgather":
                 count = S // es // n
