@@ -332,11 +332,15 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   u64* my_done = reinterpret_cast<u64*>(R.arena + kOffDone);
   const int elt = A.elt;
   const int64_t cbytes = A.chunk_elems * elt;
+  // staged mode: this call's parity region (fixed place, so reuse two calls later is safe:
+  // every rank heard from every other rank during the call in between)
+  const int64_t parity_off = kOffScratch + (int64_t)(c.epoch & 1) * A.staged_bytes;
+  char* const my_staged = R.arena + parity_off;
 
   for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
     // entry handshake: tell our sender we are in this call (its stores may now land)
-    if (tb.recv >= 0 && tid == 0) {
+    if (!A.staged && tb.recv >= 0 && tid == 0) {
       u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
       st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
     }
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           const int dt = R.deps[2 * (st.dep_begin + d)], dk = R.deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
-        if (ok && (st.op == K_SEND || st.op == K_RRCS) && !sender_ready) {
+        if (ok && !A.staged && (st.op == K_SEND || st.op == K_RRCS) && !sender_ready) {
           ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
           sender_ready = true;
         }
@@ -358,13 +362,14 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
         if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
-            const int* fz = R.fused + 3 * (st.fuse_begin + f);
+            const int* fz = R.fused + 4 * (st.fuse_begin + f);
             const KTB o = R.tbs[fz[0]];
             ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
-            s_stage[f] = local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
+            s_stage[f] = A.staged ? my_staged + (int64_t)fz[3] * cbytes : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
           }
         }
-        if (ok && (st.op == K_RRC || st.op == K_RRCS)) s_stage[0] = local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
+        if (ok && (st.op == K_RRC || st.op == K_RRCS))
+          s_stage[0] = A.staged ? my_staged + (int64_t)st.soff2 * cbytes : local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
         if (!ok) {
           record_error(c, st.op, k);
           s_abort = 1;
@@ -376,7 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
       switch (st.op) {
         case K_SEND: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
-          char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
+          char* dst = A.staged ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * cbytes
+                               : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
           for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
@@ -390,7 +396,9 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
         case K_RRCS: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          char* fwd = st.op == K_RRCS ? remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes : nullptr;
+          char* fwd = st.op != K_RRCS ? nullptr
+                      : A.staged ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * cbytes
+                                 : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
           for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             reduce_dispatch(A.dtype, dst + off, fwd ? fwd + off : nullptr, src + off, s_stage, 1, off, len / elt);
           });
@@ -408,7 +416,15 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           });
           break;
         }
-        default:  // K_RECV, K_NOP, K_SENT: no data work on this side
+        case K_RECV: {  // zero-copy: the bytes are already in place; staged: copy them out
+          if (A.staged) {
+            const char* src = my_staged + (int64_t)st.soff2 * cbytes;
+            char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+            for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+          }
+          break;
+        }
+        default:  // K_NOP, K_SENT: no data work on this side
           break;
       }
       __syncthreads();

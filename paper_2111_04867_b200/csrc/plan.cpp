@@ -93,12 +93,13 @@ void fuse_chains(const Gpu& g, const HB& hb, const std::map<std::pair<int, int>,
     const int K = (int)chain.size();
     std::vector<std::pair<int, int>> head_in = first.deps;
     if (head.second > 0) head_in.emplace_back(head.first, head.second - 1);
-    const int fb = (int32_t)rp.fused.size() / 3;
+    const int fb = (int32_t)rp.fused.size() / 4;
     for (int i = 0; i < K; ++i) {
       const KStep& x = rp.steps[flat.at(chain[i])];
       rp.fused.push_back(chain[i].first);
       rp.fused.push_back(x.seq);
       rp.fused.push_back(x.soff);
+      rp.fused.push_back(x.soff2);
     }
     for (int i = 0; i < K; ++i) {
       const int fi = flat.at(chain[i]);
@@ -127,8 +128,8 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
   // per-step seq numbers and staging offsets
-  std::map<std::tuple<int, int, int>, int> seq, soff;
-  std::vector<int> stage_total(n, 0);
+  std::map<std::tuple<int, int, int>, int> seq, soff, soff2;
+  std::vector<int> stage_total(n, 0), stage2_total(n, 0);
   for (const Gpu& g : P.gpus) {
     for (const TB& tb : g.tbs) {
       int ns = 0, nr = 0;
@@ -138,6 +139,10 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
         if (st.type == ST_RRC) {
           soff[{g.id, tb.id, st.s}] = stage_total[g.id];
           stage_total[g.id] += st.cnt;
+        }
+        if (st.type == ST_R || st.type == ST_RRC) {  // staged mode: every receive has a slot
+          soff2[{g.id, tb.id, st.s}] = stage2_total[g.id];
+          stage2_total[g.id] += st.cnt;
         }
       }
     }
@@ -152,6 +157,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
   for (const Gpu& g : P.gpus) {
     RankPlan& rp = plans[g.id];
     rp.stage_chunks = stage_total[g.id];
+    rp.stage2_chunks = stage2_total[g.id];
     rp.scratch_chunks = g.s_chunks;
     std::map<std::pair<int, int>, int> flat;  // (tb, step) -> index in rp.steps
     std::vector<std::vector<std::pair<int, int>>> deps, post;  // per flat step
@@ -176,6 +182,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
             const TB& ptb = P.gpus[tb.send].tbs[pt];
             for (const Step& ps : ptb.steps) {
               if ((ps.type == ST_R || ps.type == ST_RRC) && seq[{tb.send, pt, ps.s}] == ks.seq) {
+                ks.roff2 = soff2[{tb.send, pt, ps.s}];
                 if (ps.type == ST_R) {
                   ks.rbuf = kbuf(ps.dstbuf);
                   ks.roff = ps.dstoff;
@@ -188,11 +195,16 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
             }
             break;
           }
-          case ST_R: ks.op = K_RECV; ks.seq = seq[{g.id, tb.id, st.s}]; break;
+          case ST_R:
+            ks.op = K_RECV;
+            ks.seq = seq[{g.id, tb.id, st.s}];
+            ks.soff2 = soff2[{g.id, tb.id, st.s}];
+            break;
           case ST_RRC:
             ks.op = K_RRC;
             ks.seq = seq[{g.id, tb.id, st.s}];
             ks.soff = soff[{g.id, tb.id, st.s}];
+            ks.soff2 = soff2[{g.id, tb.id, st.s}];
             break;
           case ST_CPY: ks.op = K_CPY; break;
           default: ks.op = K_NOP; break;
@@ -233,6 +245,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
             a.rbuf = b.rbuf;
             a.roff = b.roff;
             a.fwd_seq = b.seq;
+            a.roff2 = b.roff2;
             b.op = K_SENT;
           }
         }

@@ -58,7 +58,7 @@ struct Algo {
   Coll coll;
   int nranks, p, instances;
   uint64_t min_bytes, max_bytes;
-  int max_scratch_chunks = 0, max_stage_chunks = 0, max_steps_cnt = 1;
+  int max_scratch_chunks = 0, max_stage_chunks = 0, max_stage2_chunks = 0, max_steps_cnt = 1;
   std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
   std::vector<int> ntb;         // per rank
   std::vector<std::vector<int>> weights;  // per rank, per tb
@@ -84,6 +84,7 @@ struct Comm {
   int max_ctas = 0;
   uint64_t launches = 0;
   uint64_t timeout_ns = 0;
+  int64_t staged_bytes = 0;  // one staged-mode parity region (identical on all ranks)
   // host-run staging (taccl_run_host): library-owned pinned bounce is the user's job
 };
 
@@ -97,6 +98,10 @@ size_t env_size(const char* name, size_t dflt) {
   if (!v || !*v) return dflt;
   return (size_t)strtoull(v, nullptr, 10);
 }
+
+// one parity region of the staged (small-message) mode; both sit at the front of the arena's
+// scratch area at a fixed place for the communicator's lifetime
+int64_t staged_region_bytes() { return g.staged_bytes; }
 
 taccl_result_t alloc_arena(char** out, size_t scratch) {
   char* p = nullptr;
@@ -118,6 +123,8 @@ taccl_result_t comm_common_init(int nranks, int device, size_t scratch) {
   g.device = device;
   g.arena_bytes = kOffScratch + (scratch ? scratch : env_size("TACCL_SCRATCH_BYTES", 256ull << 20));
   g.timeout_ns = (uint64_t)(env_size("TACCL_TIMEOUT_S", 20) * 1000000000ull);
+  g.staged_bytes = std::min<int64_t>((int64_t)env_size("TACCL_STAGED_REGION", 4 << 20),
+                                     (int64_t)(g.arena_bytes - kOffScratch) / 8) & ~(int64_t)4095;
   std::string err;
   g.max_ctas = executor_max_ctas(device, &err);
   if (g.max_ctas <= 0) return fail(TACCL_ERR_CUDA, err);
@@ -176,7 +183,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S) {
 
 struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, stripe = 0;
-  int split = 1, grid = 0, budget = 0, dep_ctas = 1;
+  int split = 1, grid = 0, budget = 0, dep_ctas = 1, staged = 0;
   int64_t scratch_off = 0, staging_off = 0, need = 0;
 };
 
@@ -244,7 +251,12 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   if (G->grid > g.max_ctas)
     return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
                                            std::to_string(g.max_ctas));
-  G->scratch_off = kOffScratch + base_off;
+  // staged mode for small messages (no entry handshake; receivers copy out of a parity slot)
+  const int64_t sb = staged_region_bytes();
+  const int64_t total_bytes = (int64_t)n_out * G->chunk_bytes;
+  G->staged = (int64_t)a->max_stage2_chunks * G->chunk_bytes <= sb &&
+              total_bytes <= (int64_t)env_size("TACCL_STAGED_MAX", 256 << 10) ? 1 : 0;
+  G->scratch_off = kOffScratch + 2 * sb + base_off;
   G->staging_off = G->scratch_off + (((int64_t)a->max_scratch_chunks * G->chunk_bytes + 255) & ~(int64_t)255);
   G->need = G->staging_off + (int64_t)a->max_stage_chunks * G->chunk_bytes;
   if ((size_t)G->need > g.arena_bytes)
@@ -262,6 +274,8 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.nlocal = (int)ranks.size();
   A.split = G.split;
   A.dep_ctas = G.dep_ctas;
+  A.staged = G.staged;
+  A.staged_bytes = staged_region_bytes();
   A.elt = elt;
   A.dtype = dtype;
   A.chunk_elems = G.ce;
@@ -574,6 +588,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->wsum.push_back((int)std::min<long long>(ws, 1 << 30));
     a->max_scratch_chunks = std::max(a->max_scratch_chunks, plans[r].scratch_chunks);
     a->max_stage_chunks = std::max(a->max_stage_chunks, plans[r].stage_chunks);
+    a->max_stage2_chunks = std::max(a->max_stage2_chunks, plans[r].stage2_chunks);
     a->fused_chains += plans[r].fused_chains;
     if (g.emulated || r == g.rank) {
       taccl_result_t rc = upload(plans[r], &a->plans[r]);
@@ -634,9 +649,11 @@ taccl_result_t taccl_run_host(taccl_coll_t coll, const void* host_send, void* ho
   // library-owned device buffers: the front of this rank's (symmetric) arena scratch region
   const int64_t in_off = 0, out_off = ((int64_t)ib + 4095) & ~(int64_t)4095;
   const int64_t base = (out_off + (int64_t)ob + 4095) & ~(int64_t)4095;
-  if ((size_t)(kOffScratch + base) > g.arena_bytes) return fail(TACCL_ERR_INVALID_ARG, "arena too small for host run");
-  char* dev_in = g.arenas[0] + kOffScratch + in_off;
-  char* dev_out = g.arenas[0] + kOffScratch + out_off;
+  if ((size_t)(kOffScratch + 2 * staged_region_bytes() + base) > g.arena_bytes)
+    return fail(TACCL_ERR_INVALID_ARG, "arena too small for host run");
+  const int64_t front = kOffScratch + 2 * staged_region_bytes();
+  char* dev_in = g.arenas[0] + front + in_off;
+  char* dev_out = g.arenas[0] + front + out_off;
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaMemcpyAsync(dev_in, host_send, ib, cudaMemcpyHostToDevice, s));
   if ((rc = run_one(coll, dev_in, dev_out, count, dtype, stream, base, true))) return rc;

@@ -93,6 +93,8 @@ struct KStep {
   int32_t fwd_seq;        // K_RRCS: message index of the fused send
   int32_t seq;            // message index on the tb's connection (K_SEND/K_RECV/K_RRC)
   int32_t soff;           // K_RRC: this rank's staging offset (chunk units)
+  int32_t soff2;          // receives, staged mode: this rank's staged slot (chunk units)
+  int32_t roff2;          // K_SEND/K_RRCS, staged mode: the peer's staged slot (chunk units)
   int32_t dep_begin, dep_count;  // into KRankPlan.deps (pairs tb, step)
   int32_t fuse_begin, fuse_count;  // K_RRC_FUSED: chain members' (tb, seq, soff), chain order
   int32_t part, nparts;   // K_RRC_FUSED: this member reduces portion `part` of `nparts`
@@ -148,7 +150,7 @@ struct KRank {
   const KTB* tbs;
   const KStep* steps;
   const int32_t* deps;     // pairs (tb, step)
-  const int32_t* fused;    // triples (tb, seq, soff) per absorbed rrc of a fused chain
+  const int32_t* fused;    // quadruples (tb, seq, soff, soff2) per member of a fused chain
   const char* in;
   char* out;
   char* arena;
@@ -165,6 +167,10 @@ struct KArgs {
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
   int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT)
   int32_t dep_ctas;        // CTAs per dependent tb (<= split; CTA c runs pieces c, c+dep_ctas, ...)
+  int32_t staged;          // staged mode: sends land in the receiver's parity staging slot,
+                           // receivers copy/reduce from it; no entry handshake
+  int32_t pad1;
+  int64_t staged_bytes;    // size of one parity region (at kOffScratch + parity * staged_bytes)
   int32_t elt;             // element bytes
   int32_t dtype;           // taccl_dtype_t
   int64_t chunk_elems;     // c_e

@@ -35,9 +35,14 @@ def to_host(t, dtype, like):
     return t.cpu().view(tv).numpy().view(like.dtype)
 
 
-def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20):
+MODES = {"direct": "0", "staged": str(1 << 40)}  # TACCL_STAGED_MAX: zero-copy vs staged mode
+
+
+def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20, mode=None):
     if lanes:
         os.environ["TACCL_LANES"] = str(lanes)
+    if mode:
+        os.environ["TACCL_STAGED_MAX"] = MODES[mode]
     comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=scratch)
     try:
         comm.load(text)
@@ -53,6 +58,7 @@ def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20):
     finally:
         comm.destroy()
         os.environ.pop("TACCL_LANES", None)
+        os.environ.pop("TACCL_STAGED_MAX", None)
 
 
 def bits_inputs(coll, n, count, dtype, cfg):
@@ -106,13 +112,33 @@ AGA2A = [
 
 
 @pytest.mark.parametrize("coll,algo,n,p,m,dtype,count", AGA2A)
-@pytest.mark.parametrize("lanes", [None, 4])
-def test_allgather_alltoall_bit_exact(coll, algo, n, p, m, dtype, count, lanes):
+@pytest.mark.parametrize("lanes,mode", [(None, "direct"), (4, "direct"), (None, "staged"), (2, "staged")])
+def test_allgather_alltoall_bit_exact(coll, algo, n, p, m, dtype, count, lanes, mode):
     text = generate(coll, algo, n, p, m)
     ins = bits_inputs(coll, n, count, dtype, cfg=2 if coll == "allgather" else 3)
-    got = run_gpu(text, coll, n, dtype, ins, lanes=lanes)
+    got = run_gpu(text, coll, n, dtype, ins, lanes=lanes, mode=mode)
     assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
     assert_bits_equal(got, oracle.expected_outputs(coll, ins, dtype))
+
+
+GREEDY = [("allgather", 8, 2, {"policy": "uc-max"}), ("allgather", 8, 1, {"policy": "uc-min"}),
+          ("alltoall", 8, 2, {"topology": "2x4"}), ("allreduce", 8, 1, {"policy": "uc-min"}),
+          ("allreduce", 4, 2, {"policy": "uc-max"}), ("allgather", 8, 2, {"topology": "2x4"})]
+
+
+@pytest.mark.parametrize("coll,n,p,kw", GREEDY)
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_greedy_schedules_bit_exact(coll, n, p, kw, mode):
+    text = generate(coll, "greedy", n, p, 1, **kw)
+    count = n * p * 997 if coll != "allgather" else p * 997
+    if coll == "allreduce":
+        ins = [allreduce_input(count, "int32", "bits", 10, r) for r in range(n)]
+        got = run_gpu(text, coll, n, "int32", ins, mode=mode)
+        assert_bits_equal(got, oracle.expected_outputs(coll, ins, "int32"))
+    else:
+        ins = bits_inputs(coll, n, count, "bfloat16", 11)
+        got = run_gpu(text, coll, n, "bfloat16", ins, mode=mode)
+        assert_bits_equal(got, oracle.expected_outputs(coll, ins, "bfloat16"))
 
 
 # ---------------------------------------------------------------- AR
@@ -125,12 +151,13 @@ AR = [
 
 @pytest.mark.parametrize("algo,n,p,m", AR)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-def test_allreduce_exact(algo, n, p, m, dtype):
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_allreduce_exact(algo, n, p, m, dtype, mode):
     count = n * p * 1013 if dtype == "bfloat16" else n * p * 2051
     text = generate("allreduce", algo, n, p, m)
     kind = "bits" if dtype == "int32" else "intval"
     ins = [allreduce_input(count, dtype, kind, 4, r) for r in range(n)]
-    got = run_gpu(text, "allreduce", n, dtype, ins)
+    got = run_gpu(text, "allreduce", n, dtype, ins, mode=mode)
     if dtype == "int32":
         assert_bits_equal(got, oracle.expected_outputs("allreduce", ins, "int32"))
     # integer-valued floats: every order is exact, so the oracle's schedule result is the answer
@@ -203,6 +230,56 @@ def test_invalid_schedule_rejected_at_load():
         with pytest.raises(taccl.TacclError) as e:
             comm.load(bad)
         assert e.value.code == 2
+    finally:
+        comm.destroy()
+
+
+@pytest.mark.parametrize("sizes", [[4096, 1 << 20, 4096, 8, 1 << 22, 4096], [64, 64, 1 << 21, 64]])
+def test_mode_and_size_changes_between_calls(sizes):
+    # consecutive calls alternate between staged and zero-copy mode and between sizes (the
+    # staged parity regions have a fixed place; flags are epoch-monotone)
+    n = 4
+    text = generate("allreduce", "direct", n, 1, 1)
+    comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=64 << 20)
+    try:
+        comm.load(text)
+        for it, count in enumerate(sizes * 3):
+            count = n * max(1, count // n)
+            ins = [allreduce_input(count, "int32", "bits", 30 + it, r) for r in range(n)]
+            dev_in = [to_dev(x, "int32") for x in ins]
+            dev_out = [torch.empty(count, dtype=torch.int32, device="cuda") for _ in range(n)]
+            comm.run_emulated("allreduce", dev_out, dev_in)
+            torch.cuda.synchronize()
+            assert_bits_equal([to_host(o, "int32", ins[0]) for o in dev_out], oracle.expected_outputs("allreduce", ins, "int32"))
+        comm.check()
+    finally:
+        comm.destroy()
+
+
+def test_cuda_graph_capture_replays_correctly():
+    # taccl_run is capturable: epochs live on the device, so graph replays advance them
+    n, count = 4, 4 * 8192
+    comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=16 << 20)
+    try:
+        comm.load(generate("allgather", "direct", n, 1, 1))
+        ins = bits_inputs("allgather", n, count, "bfloat16", 12)
+        dev_in = [to_dev(x, "bfloat16") for x in ins]
+        dev_out = [torch.empty(n * count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            comm.run_emulated("allgather", dev_out, dev_in, stream=s)  # warm
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            comm.run_emulated("allgather", dev_out, dev_in, stream=s)
+        for it in range(5):
+            for o in dev_out:
+                o.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert_bits_equal([to_host(o, "bfloat16", ins[0]) for o in dev_out],
+                              oracle.expected_outputs("allgather", ins, "bfloat16"))
+        comm.check()
     finally:
         comm.destroy()
 
