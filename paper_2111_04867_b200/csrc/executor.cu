@@ -301,32 +301,45 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   __shared__ int s_abort;
   __shared__ u64 s_epoch;
   __shared__ const char* s_stage[kMaxRanks + 1];
+  extern __shared__ int4 s_plan[];
   const int tid = threadIdx.x;
   int lr = 0;
   while (lr + 1 < A.nlocal && (int)blockIdx.x >= A.r[lr + 1].cta_begin) ++lr;
   const KRank& R = A.r[lr];
   const int local = blockIdx.x - R.cta_begin;
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
+  // the rank's plan (a few KB) moves to shared memory in one cooperative pass, overlapped
+  // with the epoch load, instead of a chain of dependent global loads per step
+  const char* planp = R.plan;
+  if (tid == 0) {
+    s_epoch = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
+    s_abort = 0;
+  }
+  if (A.plan_smem) {
+    const int4* g = reinterpret_cast<const int4*>(R.plan);
+    for (int i = tid; i < R.plan_bytes / 16; i += blockDim.x) s_plan[i] = __ldg(g + i);
+    planp = reinterpret_cast<const char*>(s_plan);
+  }
+  __syncthreads();
+  const KTB* tbs = reinterpret_cast<const KTB*>(planp);
+  const KStep* steps = reinterpret_cast<const KStep*>(planp + R.steps_off);
+  const int32_t* deps = reinterpret_cast<const int32_t*>(planp + R.deps_off);
+  const int32_t* fused = reinterpret_cast<const int32_t*>(planp + R.fused_off);
   // CTA (t, c0) runs pieces j = c0, c0 + C, ... of threadblock t, each piece's whole program
   // before the next (every CTA visits pieces in increasing order, so a wait on piece j only
   // ever depends on piece-j work of CTAs that have finished all their pieces < j).
   int t = 0, ct = 0, acc = 0;
   for (;; ++t) {
-    ct = R.tbs[t].indep ? tb_pieces(1, R.tbs[t].weight, R.wsum, R.budget, A.split) : A.dep_ctas;
+    ct = tbs[t].indep ? tb_pieces(1, tbs[t].weight, R.wsum, R.budget, A.split, A.indep_cap) : A.dep_ctas;
     if (local < acc + ct || t + 1 == R.ntb) break;
     acc += ct;
   }
-  const int nsplit = R.tbs[t].indep ? ct : A.split;  // this tb's piece count
+  const int nsplit = tbs[t].indep ? ct : A.split;  // this tb's piece count
   Ctx c{&A, &R, t, 0, 0};
   const int c0 = local - acc;
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
-  if (tid == 0) {
-    s_epoch = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
-    s_abort = 0;
-  }
-  __syncthreads();
   c.epoch = s_epoch;
   const u64 E = c.epoch << 24;
-  const KTB tb = R.tbs[c.t];
+  const KTB tb = tbs[c.t];
   u64* my_data = reinterpret_cast<u64*>(R.arena + kOffData);
   u64* my_ready = reinterpret_cast<u64*>(R.arena + kOffReady);
   u64* my_done = reinterpret_cast<u64*>(R.arena + kOffDone);
@@ -347,11 +360,11 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
     bool sender_ready = false;
 
     for (int k = 0; k < tb.nsteps; ++k) {
-      const KStep st = R.steps[tb.step_begin + k];
+      const KStep st = steps[tb.step_begin + k];
       if (tid == 0) {
         bool ok = true;
         for (int d = 0; d < st.dep_count && ok; ++d) {
-          const int dt = R.deps[2 * (st.dep_begin + d)], dk = R.deps[2 * (st.dep_begin + d) + 1];
+          const int dt = deps[2 * (st.dep_begin + d)], dk = deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
         if (ok && !A.staged && (st.op == K_SEND || st.op == K_RRCS) && !sender_ready) {
@@ -362,8 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
         if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
-            const int* fz = R.fused + 4 * (st.fuse_begin + f);
-            const KTB o = R.tbs[fz[0]];
+            const int* fz = fused + 4 * (st.fuse_begin + f);
+            const KTB o = tbs[fz[0]];
             ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
             s_stage[f] = A.staged ? my_staged + (int64_t)fz[3] * cbytes : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
           }
@@ -431,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
       if (tid == 0) {
         bool ok = true;  // post-dependencies: the other members of a fused chain
         for (int d = 0; d < st.post_count && ok; ++d) {
-          const int dt = R.deps[2 * (st.post_begin + d)], dk = R.deps[2 * (st.post_begin + d) + 1];
+          const int dt = deps[2 * (st.post_begin + d)], dk = deps[2 * (st.post_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
         if (!ok) {
@@ -441,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
         if (st.op == K_SEND || st.op == K_RRCS) {
           // all threads' peer stores are ordered before this by bar.sync (causality order);
           // the system-scope acq_rel fence makes them visible before the flag (cumulativity)
-          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          if (A.variant != 9) asm volatile("fence.acq_rel.sys;" ::: "memory");  // 9: timing probe only
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)((st.op == K_RRCS ? st.fwd_seq : st.seq) + 1));
         }
@@ -457,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   if (tid == 0) {
     unsigned total = 0;
     for (int u = 0; u < R.ntb; ++u)
-      total += R.tbs[u].indep ? tb_pieces(1, R.tbs[u].weight, R.wsum, R.budget, A.split) : A.dep_ctas;
+      total += tbs[u].indep ? tb_pieces(1, tbs[u].weight, R.wsum, R.budget, A.split, A.indep_cap) : A.dep_ctas;
     unsigned prev;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctrl->finished) : "memory");
     if (prev == total - 1) {
@@ -469,8 +482,8 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
 
 }  // namespace
 
-int launch_executor(const KArgs& a, int grid, void* stream, std::string* err) {
-  taccl_exec_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::string* err) {
+  taccl_exec_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("kernel launch: ") + cudaGetErrorString(e);

@@ -44,12 +44,9 @@ struct HandleBlob {  // TACCL_HANDLE_BYTES
 };
 static_assert(sizeof(HandleBlob) == TACCL_HANDLE_BYTES, "blob size");
 
-struct DevPlan {  // one rank's plan in device memory
+struct DevPlan {  // one rank's plan blob in device memory
   void* mem = nullptr;
-  const KTB* tbs = nullptr;
-  const KStep* steps = nullptr;
-  const int32_t* deps = nullptr;
-  const int32_t* fused = nullptr;
+  int bytes = 0, steps_off = 0, deps_off = 0, fused_off = 0;
   int ntb = 0;
 };
 
@@ -183,7 +180,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S) {
 
 struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, stripe = 0;
-  int split = 1, grid = 0, budget = 0, dep_ctas = 1, staged = 0;
+  int split = 1, grid = 0, budget = 0, dep_ctas = 1, staged = 0, indep_cap = 1;
   int64_t scratch_off = 0, staging_off = 0, need = 0;
 };
 
@@ -209,6 +206,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   int nlocal = 0;
   for (int r = 0; r < a->nranks; ++r)
     if (a->plans[r].mem) ++nlocal;
+  G->indep_cap = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxSplit, (int64_t)a->max_steps_cnt * G->chunk_bytes / min_piece));
   G->budget = std::max(1, target / std::max(1, nlocal));
   // CTAs left for the dependent tbs once independent tbs took their weight share
   int per_dep = kMaxSplit;
@@ -216,7 +214,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
     if (!a->plans[r].mem) continue;
     int used = 0, ndep = 0;
     for (int t = 0; t < a->ntb[r]; ++t) {
-      if (a->indep[r][t]) used += tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, 1);
+      if (a->indep[r][t]) used += tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, 1, G->indep_cap);
       else ++ndep;
     }
     if (ndep) per_dep = std::min(per_dep, std::max(1, (G->budget - used) / ndep));
@@ -247,7 +245,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   for (int r = 0; r < a->nranks; ++r)
     if (a->plans[r].mem)
       for (int t = 0; t < a->ntb[r]; ++t)
-        G->grid += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, G->split) : G->dep_ctas;
+        G->grid += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, G->split, G->indep_cap) : G->dep_ctas;
   if (G->grid > g.max_ctas)
     return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
                                            std::to_string(g.max_ctas));
@@ -274,6 +272,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.nlocal = (int)ranks.size();
   A.split = G.split;
   A.dep_ctas = G.dep_ctas;
+  A.indep_cap = G.indep_cap;
   A.staged = G.staged;
   A.staged_bytes = staged_region_bytes();
   A.elt = elt;
@@ -284,15 +283,17 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.scratch_off = G.scratch_off;
   A.staging_off = G.staging_off;
   A.timeout_ns = g.timeout_ns;
-  int cta = 0;
+  int cta = 0, smem = 0;
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
     KRank& R = A.r[i];
     const DevPlan& dp = a->plans[r];
-    R.tbs = dp.tbs;
-    R.steps = dp.steps;
-    R.deps = dp.deps;
-    R.fused = dp.fused;
+    R.plan = (const char*)dp.mem;
+    R.plan_bytes = dp.bytes;
+    R.steps_off = dp.steps_off;
+    R.deps_off = dp.deps_off;
+    R.fused_off = dp.fused_off;
+    smem = std::max(smem, dp.bytes);
     R.in = (const char*)sends[i];
     R.out = (char*)recvs[i];
     R.arena = g.peer_arena[r];
@@ -306,10 +307,11 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     R.budget = G.budget;
     R.wsum = a->wsum[r];
     for (int t = 0; t < dp.ntb; ++t)
-      cta += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G.budget, G.split) : G.dep_ctas;
+      cta += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G.budget, G.split, G.indep_cap) : G.dep_ctas;
   }
+  A.plan_smem = smem <= kPlanSmemMax ? 1 : 0;
   std::string err;
-  if (launch_executor(A, cta, stream, &err)) return fail(TACCL_ERR_CUDA, err);
+  if (launch_executor(A, cta, A.plan_smem ? smem : 0, stream, &err)) return fail(TACCL_ERR_CUDA, err);
   ++g.launches;
   ++g_launches;
   return TACCL_SUCCESS;
@@ -366,26 +368,23 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
 }
 
 taccl_result_t upload(const RankPlan& rp, DevPlan* dp) {
-  const size_t b1 = rp.tbs.size() * sizeof(KTB), b2 = rp.steps.size() * sizeof(KStep);
-  const size_t b3 = rp.deps.size() * 4, b4 = rp.fused.size() * 4;
-  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t total = al(b1) + al(b2) + al(b3) + al(b4) + 256;
+  auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const size_t b1 = al(rp.tbs.size() * sizeof(KTB)), b2 = al(rp.steps.size() * sizeof(KStep));
+  const size_t b3 = al(rp.deps.size() * 4), b4 = al(rp.fused.size() * 4);
+  const size_t total = b1 + b2 + b3 + b4 + 16;
+  std::vector<char> host(total, 0);
+  if (!rp.tbs.empty()) memcpy(host.data(), rp.tbs.data(), rp.tbs.size() * sizeof(KTB));
+  if (!rp.steps.empty()) memcpy(host.data() + b1, rp.steps.data(), rp.steps.size() * sizeof(KStep));
+  if (!rp.deps.empty()) memcpy(host.data() + b1 + b2, rp.deps.data(), rp.deps.size() * 4);
+  if (!rp.fused.empty()) memcpy(host.data() + b1 + b2 + b3, rp.fused.data(), rp.fused.size() * 4);
   char* m = nullptr;
   CUDA_TRY(cudaMalloc(&m, total));
-  std::vector<char> host(total, 0);
-  size_t o = 0;
-  auto put = [&](const void* src, size_t bytes) {
-    if (bytes) memcpy(host.data() + o, src, bytes);
-    size_t at = o;
-    o += al(bytes);
-    return m + at;
-  };
-  dp->tbs = (const KTB*)put(rp.tbs.data(), b1);
-  dp->steps = (const KStep*)put(rp.steps.data(), b2);
-  dp->deps = (const int32_t*)put(rp.deps.data(), b3);
-  dp->fused = (const int32_t*)put(rp.fused.data(), b4);
   CUDA_TRY(cudaMemcpy(m, host.data(), total, cudaMemcpyHostToDevice));
   dp->mem = m;
+  dp->bytes = (int)total;
+  dp->steps_off = (int)b1;
+  dp->deps_off = (int)(b1 + b2);
+  dp->fused_off = (int)(b1 + b2 + b3);
   dp->ntb = (int)rp.tbs.size();
   return TACCL_SUCCESS;
 }

@@ -147,10 +147,8 @@ namespace taccl {
 // ---------------------------------------------------------------- kernel arguments
 // Per local rank (one in multi-process mode, all ranks when emulated). Passed by value.
 struct KRank {
-  const KTB* tbs;
-  const KStep* steps;
-  const int32_t* deps;     // pairs (tb, step)
-  const int32_t* fused;    // quadruples (tb, seq, soff, soff2) per member of a fused chain
+  const char* plan;        // the rank's plan blob: [KTB...][KStep...][deps][fused], 16-B aligned
+  int32_t plan_bytes, steps_off, deps_off, fused_off;  // blob size and section offsets
   const char* in;
   char* out;
   char* arena;
@@ -167,6 +165,8 @@ struct KArgs {
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
   int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT)
   int32_t dep_ctas;        // CTAs per dependent tb (<= split; CTA c runs pieces c, c+dep_ctas, ...)
+  int32_t plan_smem;       // copy the rank's plan blob into shared memory at kernel start
+  int32_t indep_cap;       // max pieces of an independent tb (bytes / min piece)
   int32_t staged;          // staged mode: sends land in the receiver's parity staging slot,
                            // receivers copy/reduce from it; no entry handshake
   int32_t pad1;
@@ -186,14 +186,16 @@ constexpr int kThreads = 512;
 // the launch-wide split (a dependency or a connection pairs piece j with piece j); an
 // independent tb (e.g. the own-chunk copy) gets its own count from its data-volume share
 // of the rank's CTA budget.
-TACCL_HD inline int tb_pieces(int indep, int weight, int wsum, int budget, int split) {
+TACCL_HD inline int tb_pieces(int indep, int weight, int wsum, int budget, int split, int cap) {
   if (!indep) return split;  // (run by min(split, KArgs.dep_ctas) CTAs)
   long long c = wsum > 0 ? (long long)budget * weight / wsum : 1;
+  if (c > cap) c = cap;
   return c < 1 ? 1 : c > kMaxSplit ? kMaxSplit : (int)c;
 }
 
 // executor.cu
-int launch_executor(const KArgs& a, int grid, void* stream, std::string* err);
+int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::string* err);
+constexpr int kPlanSmemMax = 48 << 10;  // plans up to this size are staged in shared memory
 int executor_max_ctas(int device, std::string* err);  // co-resident CTA capacity
 
 }  // namespace taccl

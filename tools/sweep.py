@@ -33,6 +33,34 @@ def factor(coll, n):
     return 2.0 * (n - 1) / n if coll == "allreduce" else (n - 1) / n
 
 
+def timeit_graph(fn, stream, world, iters=200):
+    """Capture `iters` calls into one CUDA graph and time its replay: per-call device time
+    without host launch overhead (both our executor and NCCL are capturable)."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(iters):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del g
+    return ms, iters
+
+
 def timeit(fn, stream, world, target_ms=50.0):
     for _ in range(5):
         fn()
@@ -74,6 +102,7 @@ def main():
     ap.add_argument("--dtype", default="bfloat16")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (no host overhead)")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -90,7 +119,9 @@ def main():
     big_in = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
     big_out = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
     comm.register(big_out)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream() if a.graph else torch.cuda.current_stream()
+    torch.cuda.set_stream(stream)
+    tf = (lambda f, st, w: timeit_graph(f, st, w)) if a.graph else timeit
     out_f = open(a.out or os.path.join(ROOT, "gpurun_out", f"sweep_n{n}.jsonl"), "a") if rank == 0 else None
     for coll in a.colls.split(","):
         algos = ALGOS[coll] if n > 1 else ["direct"]
@@ -109,12 +140,12 @@ def main():
             if count == 0 or (coll != "allgather" and count % n):
                 continue
             inp.copy_(torch.randint(-8, 8, inp.shape, device="cuda").to(dt))
-            rec = {"coll": coll, "n": n, "S": S, "dtype": a.dtype}
+            rec = {"coll": coll, "n": n, "S": S, "dtype": a.dtype, "graph": a.graph}
             for al in algos:
                 # select this algorithm: load order decides (latest wins) -> reload on top
                 comm.free(handles[al])
                 handles[al] = comm.load(generate(coll, al, n, 1, 1))
-                ms, it = timeit(lambda: comm.run(coll, out, inp), stream, world)
+                ms, it = tf(lambda: comm.run(coll, out, inp, stream), stream, world)
                 rec[f"taccl_{al}_us"] = round(ms * 1e3, 3)
                 rec[f"taccl_{al}_busbw"] = round(S / (ms / 1e3) * factor(coll, n) / 1e9, 2)
                 # check once (bits for AG/A2A, int-valued sum for AR)
@@ -130,11 +161,11 @@ def main():
                     f = lambda: dist.all_to_all_single(out, inp)  # noqa: E731
                 else:
                     f = lambda: dist.all_reduce(out, op=dist.ReduceOp.SUM)  # noqa: E731
-                ms, it = timeit(f, stream, world)
+                ms, it = tf(f, stream, world)
                 rec["nccl_us"] = round(ms * 1e3, 3)
                 rec["nccl_busbw"] = round(S / (ms / 1e3) * factor(coll, n) / 1e9, 2)
             elif n == 1:
-                ms, it = timeit(lambda: out.copy_(inp), stream, world)
+                ms, it = tf(lambda: out.copy_(inp), stream, world)
                 rec["torch_copy_us"] = round(ms * 1e3, 3)
                 rec["torch_copy_gbs"] = round(S / (ms / 1e3) * 2 / 1e9, 2)
             best = min((rec[f"taccl_{al}_us"], al) for al in algos)
