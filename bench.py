@@ -229,9 +229,10 @@ def main():
         value = n * busbw
         egress = S * (n - 1) / n  # algorithmic NVLink bytes per launch per GPU
         ach = egress / t_step / 1e9
-        roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_NOMINAL, "unit": "GB/s",
-                "frac": round(ach / NVLINK_NOMINAL, 4),
-                "peak_source": f"nominal NVLink 5 per direction (north star); guide-measured peer copy {NVLINK_MEASURED_REF}"}
+        roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_REF, "unit": "GB/s",
+                "frac": round(ach / NVLINK_MEASURED_REF, 4), "frac_of_nominal_900": round(ach / NVLINK_NOMINAL, 4),
+                "peak_source": "measured peer copy per direction per GPU (B200_PROFILING.md fallback; "
+                               "MEASURED_PEAKS.json has no NVLink figure); nominal 900 for context"}
     roof["traffic"] = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
