@@ -1,7 +1,8 @@
 /*
  * taccl.h — C ABI of the B200 executor for TACCL-EF chunk schedules (arXiv 2111.04867).
  *
- * The library runs synthesized collective algorithms (Allgather, Alltoall, Allreduce):
+ * The library runs synthesized collective algorithms (Allgather, Alltoall, Allreduce,
+ * ReduceScatter):
  * every GPU executes per-threadblock programs of send / recv / recvReduceCopy / copy steps
  * over chunk indices with cross-step dependencies, the paper's runtime model
  * (§6.1), in ONE kernel launch per collective call. Bytes
@@ -39,7 +40,14 @@ typedef enum {
   TACCL_ERR_NOT_REGISTERED = 8    /* buffer not registered with taccl_register_buffer         */
 } taccl_result_t;
 
-typedef enum { TACCL_ALLGATHER = 0, TACCL_ALLTOALL = 1, TACCL_ALLREDUCE = 2 } taccl_coll_t;
+/* ReduceScatter ("an inverse of Allgather"): rank r receives the
+ * element-wise sum over ranks of elements [r*count, (r+1)*count) of every sendbuf. */
+typedef enum {
+  TACCL_ALLGATHER = 0,
+  TACCL_ALLTOALL = 1,
+  TACCL_ALLREDUCE = 2,
+  TACCL_REDUCESCATTER = 3
+} taccl_coll_t;
 
 /* Element types. AG/A2A move raw bytes (dtype only sets the element size); AR sums:
  * INT32 wraps mod 2^32, FLOAT32 is IEEE binary32 round-to-nearest-even, BFLOAT16
@@ -114,9 +122,10 @@ taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* 
 taccl_result_t taccl_load_algo(const char* schedule_text, size_t len, taccl_algo_t* out);
 
 /* Run the collective with the loaded algorithm selected by (coll, nranks, S) where S =
- * output bytes (AG), per-rank send bytes (A2A), buffer bytes (AR). NCCL count convention:
- * AG count = elements per rank (recvbuf holds nranks*count), A2A count = elements per
- * peer (both buffers hold nranks*count), AR count = total elements. sendbuf/recvbuf are
+ * output bytes (AG), per-rank send bytes (A2A), buffer bytes (AR), send bytes (RS). NCCL
+ * count convention: AG count = elements per rank (recvbuf holds nranks*count), A2A count =
+ * elements per peer (both buffers hold nranks*count), AR count = total elements, RS count =
+ * elements per rank (sendbuf holds nranks*count, recvbuf count). sendbuf/recvbuf are
  * device pointers; recvbuf must be registered (taccl_register_buffer) unless emulated.
  * Out-of-place only (in-place -> UNSUPPORTED). Enqueues ONE kernel on `stream`
  * (a cudaStream_t; NULL = legacy default stream); returns without synchronizing. The

@@ -8,7 +8,7 @@ from the product: the two share no parser, validator, geometry or arithmetic.
 It is a plain, slow, obviously-correct restatement of what the paper says a schedule
 computes:
 
-* `collectives` — the collectives' definitions (§2) and their chunk
+* `collectives` — the collectives' definitions (§2; ReduceScatter 722–727) and their chunk
   pre/postconditions (App. B, PAPER.md:1324–1330).
 * `ef` — an independent parser for the EF v1 text (docs/SCHEDULE.md).
 * `validate` — structure, send/recv matching, the happens-before DAG, races.
@@ -22,7 +22,7 @@ the instance invariant, involution of Alltoall, library bf16 rounding, mutation 
 Parity unpinned: nothing in this package — see DESIGN.md §"Oracle pins".
 """
 from .ef import Program, ScheduleError, parse  # noqa: F401
-from .collectives import chunk_elems, expected_outputs, expected_allreduce_f64  # noqa: F401
+from .collectives import chunk_elems, expected_outputs, expected_allreduce_f64, expected_reducescatter_f64  # noqa: F401
 from .validate import validate, Verdict  # noqa: F401
 from .simulate import run, run_symbolic  # noqa: F401
 from .instances import expand_instances  # noqa: F401

@@ -5,6 +5,8 @@ GPUs. In Alltoall, every GPU receives different parts, or chunks, of the data bu
 present on all GPUs. This effectively transposes the data chunk from buffer index to GPU
 index ... In Allreduce, every GPU ends up with a data buffer that has the results of
 performing a point-wise computation (e.g. sum ...) over the same data index of all GPUs."
+ReduceScatter (§5.3): Allreduce's point-wise sum of which each GPU
+keeps only its own part (NCCL convention: rank r keeps elements [r·count, (r+1)·count)).
 Chunk-level pre/postconditions: App. B; chunk-id layout SPEC.md:142.
 """
 from __future__ import annotations
@@ -27,16 +29,18 @@ def buffer_chunks(coll: str, n: int, p: int):
         return p, n * p
     if coll in ("alltoall", "allreduce"):
         return n * p, n * p
+    if coll == "reducescatter":
+        return n * p, p
     raise ScheduleError("syntax", f"unknown collective {coll}")
 
 
 def input_elems(coll: str, n: int, count: int) -> int:
     """E_in: elements of the input buffer for NCCL-style `count` (reading G8)."""
-    return n * count if coll == "alltoall" else count
+    return n * count if coll in ("alltoall", "reducescatter") else count
 
 
 def output_elems(coll: str, n: int, count: int) -> int:
-    return count if coll == "allreduce" else n * count
+    return count if coll in ("allreduce", "reducescatter") else n * count
 
 
 def chunk_elems(coll: str, n: int, p: int, count: int) -> int:
@@ -52,7 +56,7 @@ def chunk_elems(coll: str, n: int, p: int, count: int) -> int:
 
 def precondition(coll: str, n: int, p: int):
     """{rank: {input chunk index: token}}; AG/A2A tokens are global chunk ids,
-    AR tokens are (chunk index, contribution counts per rank)."""
+    AR/RS tokens are (chunk index, contribution counts per rank)."""
     pre = {}
     for r in range(n):
         if coll == "allgather":
@@ -72,6 +76,8 @@ def postcondition(coll: str, n: int, p: int):
             post[r] = {g: g for g in range(n * p)}
         elif coll == "alltoall":
             post[r] = {s * p + k: (s * n + r) * p + k for s in range(n) for k in range(p)}
+        elif coll == "reducescatter":
+            post[r] = {k: (r * p + k, tuple([1] * n)) for k in range(p)}
         else:
             post[r] = {k: (k, tuple([1] * n)) for k in range(n * p)}
     return post
@@ -85,6 +91,7 @@ def expected_outputs(coll: str, inputs, dtype: str):
     AG: out_r = in_0 ++ in_1 ++ ... ++ in_{n-1}.
     A2A: out_r[s*count + i] = in_s[r*count + i].
     AR (int32 only here; floats use expected_allreduce_f64): out_r[i] = sum_s in_s[i] mod 2^32.
+    RS (int32 only): out_r[i] = sum_s in_s[r*count + i] mod 2^32.
     """
     n = len(inputs)
     if coll == "allgather":
@@ -104,6 +111,17 @@ def expected_outputs(coll: str, inputs, dtype: str):
             acc += x.astype(np.int64)
         out = (acc & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
         return [out.copy() for _ in range(n)]
+    if coll == "reducescatter":
+        if dtype != "int32":
+            raise ValueError("float reducescatter has no single exact result; use expected_reducescatter_f64")
+        count = inputs[0].size // n
+        outs = []
+        for r in range(n):
+            acc = np.zeros(count, dtype=np.int64)
+            for x in inputs:
+                acc += x[r * count:(r + 1) * count].astype(np.int64)
+            outs.append((acc & 0xFFFFFFFF).astype(np.uint32).view(np.int32))
+        return outs
     raise ValueError(coll)
 
 
@@ -124,3 +142,11 @@ def expected_allreduce_f64(inputs, dtype: str) -> np.ndarray:
     for x in inputs:
         acc += to_f64(x, dtype)
     return acc
+
+
+def expected_reducescatter_f64(inputs, dtype: str):
+    """fp64 reference for float reducescatter: out_r[i] = sum_s (double) in_s[r*count + i]."""
+    n = len(inputs)
+    count = inputs[0].size // n
+    full = expected_allreduce_f64(inputs, dtype)
+    return [full[r * count:(r + 1) * count].copy() for r in range(n)]

@@ -24,7 +24,7 @@ class ScheduleError(Exception):
         self.msg = msg
 
 
-COLLS = ("allgather", "alltoall", "allreduce")
+COLLS = ("allgather", "alltoall", "allreduce", "reducescatter")
 STEP_TYPES = ("s", "r", "rrc", "cpy", "nop")
 BUFS = ("i", "o", "s")
 

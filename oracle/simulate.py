@@ -93,7 +93,7 @@ def run_symbolic(prog: Program, graph=None, order=None, check=True):
         buf[off:off + cnt] = vals
 
     def reduce(mine, got, where):
-        if prog.coll != "allreduce":
+        if prog.coll not in ("allreduce", "reducescatter"):
             raise ScheduleError("structure", "rank %d tb%d:s%d reduces in a non-reducing "
                                              "collective" % where)
         out = []
@@ -117,7 +117,7 @@ def run_symbolic(prog: Program, graph=None, order=None, check=True):
 
 
 def _post_msg(coll, r, k, want, got):
-    if coll != "allreduce":
+    if coll not in ("allreduce", "reducescatter"):
         return f"(chunk {want}, rank {r}) missing: o[{k}] holds {got!r}"
     if got is BOTTOM:
         return f"(chunk {k}, rank {r}) missing: o[{k}] never written"
@@ -163,7 +163,7 @@ def run(prog: Program, inputs, dtype: str, graph=None, order=None):
     n, p = prog.nranks, prog.chunks_per_rank
     np_dt, _ = DTYPES[dtype]
     e_in = inputs[0].size
-    count = e_in // n if prog.coll == "alltoall" else e_in
+    count = e_in // n if prog.coll in ("alltoall", "reducescatter") else e_in
     ce = chunk_elems(prog.coll, n, p, count)
     bufs = []
     for g in prog.gpus:

@@ -289,7 +289,7 @@ void symbolic(const Program& P, const Graph& G, const std::vector<int>& order) {
         std::vector<Tok> got = q.front();
         q.pop_front();
         std::vector<Tok> mine = rd(st.srcbuf, st.srcoff);
-        if (P.coll != C_AR) fail("structure", where(r, t, k) + " reduces in a non-reducing collective");
+        if (P.coll != C_AR && P.coll != C_RS) fail("structure", where(r, t, k) + " reduces in a non-reducing collective");
         for (int i = 0; i < st.cnt; ++i) {
           if (mine[i].chunk != got[i].chunk)
             fail("postcondition", where(r, t, k) + " reduces chunk " + std::to_string(mine[i].chunk) + " with chunk " + std::to_string(got[i].chunk));
@@ -307,12 +307,12 @@ void symbolic(const Program& P, const Graph& G, const std::vector<int>& order) {
       Tok want;
       if (P.coll == C_AG) want.chunk = g;
       else if (P.coll == C_A2A) want.chunk = ((g / p) * n + r) * p + g % p;
-      else {
-        want.chunk = g;
+      else {  // AR: o[g] = chunk g; RS: o[g] = chunk r*p + g (the rank's own part)
+        want.chunk = P.coll == C_RS ? r * p + g : g;
         want.contrib.assign(n, 1);
       }
       if (out[g] == want) continue;
-      if (P.coll != C_AR)
+      if (P.coll != C_AR && P.coll != C_RS)
         fail("postcondition", "(chunk " + std::to_string(want.chunk) + ", rank " + std::to_string(r) + ") missing");
       if (out[g].chunk < 0)
         fail("postcondition", "(chunk " + std::to_string(g) + ", rank " + std::to_string(r) + ") missing: never written");

@@ -160,6 +160,9 @@ void buffer_chunks(Coll c, int n, int p, int* n_in, int* n_out) {
   if (c == C_AG) {
     *n_in = p;
     *n_out = n * p;
+  } else if (c == C_RS) {  // ReduceScatter: n*p input chunks, the rank's own p outputs
+    *n_in = n * p;
+    *n_out = p;
   } else {
     *n_in = n * p;
     *n_out = n * p;
@@ -176,6 +179,7 @@ Program parse_ef(const char* text, size_t len) {
   if (coll == "allgather") prog.coll = C_AG;
   else if (coll == "alltoall") prog.coll = C_A2A;
   else if (coll == "allreduce") prog.coll = C_AR;
+  else if (coll == "reducescatter") prog.coll = C_RS;
   else fail("coll=\"" + coll + "\" unsupported");
   prog.name = t.attrs.count("name") ? t.attrs["name"] : "";
   prog.nranks = (int)to_int(t, "nranks", 1);

@@ -165,6 +165,7 @@ taccl_result_t open_handle(const cudaIpcMemHandle_t& h, char** out) {
 // message bytes S used for algorithm selection (SURVEY.md §8(b) convention 4, reading G8)
 uint64_t select_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
   if (coll == TACCL_ALLREDUCE) return (uint64_t)count * elt;
+  // RS: nccl-tests convention, S = send bytes = n * recvcount * elt (like AG's output bytes)
   return (uint64_t)n * count * elt;
 }
 
@@ -188,7 +189,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
                         int64_t base_off, Geometry* G) {
   int n_in, n_out;
   buffer_chunks(a->coll, a->nranks, a->p, &n_in, &n_out);
-  const int64_t e_in = coll == TACCL_ALLTOALL ? (int64_t)a->nranks * count : (int64_t)count;
+  const int64_t e_in = (coll == TACCL_ALLTOALL || coll == TACCL_REDUCESCATTER) ? (int64_t)a->nranks * count : (int64_t)count;
   if (e_in % n_in)
     return fail(TACCL_ERR_INVALID_ARG, "count " + std::to_string(count) + " does not split into " +
                                            std::to_string(n_in) + " equal chunks (reading G2)");
@@ -320,17 +321,17 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
 taccl_result_t check_common(taccl_coll_t coll, size_t count, taccl_dtype_t dtype) {
   if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
   if (!g.emulated && !g.peers_set && g.nranks > 1) return fail(TACCL_ERR_NOT_INITIALIZED, "peers not set");
-  if (coll < TACCL_ALLGATHER || coll > TACCL_ALLREDUCE) return fail(TACCL_ERR_INVALID_ARG, "bad collective");
+  if (coll < TACCL_ALLGATHER || coll > TACCL_REDUCESCATTER) return fail(TACCL_ERR_INVALID_ARG, "bad collective");
   if (dtype < TACCL_INT32 || dtype > TACCL_BFLOAT16) return fail(TACCL_ERR_INVALID_ARG, "bad dtype");
   (void)count;
   return TACCL_SUCCESS;
 }
 
 size_t in_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
-  return coll == TACCL_ALLTOALL ? (size_t)n * count * elt : count * elt;
+  return (coll == TACCL_ALLTOALL || coll == TACCL_REDUCESCATTER) ? (size_t)n * count * elt : count * elt;
 }
 size_t out_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
-  return coll == TACCL_ALLREDUCE ? count * elt : (size_t)n * count * elt;
+  return (coll == TACCL_ALLREDUCE || coll == TACCL_REDUCESCATTER) ? count * elt : (size_t)n * count * elt;
 }
 
 taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, size_t count,

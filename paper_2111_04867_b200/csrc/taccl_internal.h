@@ -14,7 +14,7 @@ namespace taccl {
 // ---------------------------------------------------------------- parsed program (host)
 enum StepType : int8_t { ST_S = 0, ST_R = 1, ST_RRC = 2, ST_CPY = 3, ST_NOP = 4 };
 enum BufId : int8_t { B_NONE = -1, B_I = 0, B_O = 1, B_S = 2 };
-enum Coll : int8_t { C_AG = 0, C_A2A = 1, C_AR = 2 };
+enum Coll : int8_t { C_AG = 0, C_A2A = 1, C_AR = 2, C_RS = 3 };
 
 struct Step {
   int s = 0;

@@ -214,6 +214,9 @@ def synthesize(coll, nranks, chunks=1, policy="uc-max", topology=None, sketch=No
         ag = synthesize("allgather", nranks, chunks, policy, topo, sk, size)
         ag_rev = synthesize("allgather", nranks, chunks, policy, topo, sk, size, _reverse=True)
         return templates.allreduce(templates.invert_allgather(ag_rev), ag, f"ar_greedy_{sk.policy}_n{nranks}_p{chunks}")
+    if coll == "reducescatter":
+        ag_rev = synthesize("allgather", nranks, chunks, policy, topo, sk, size, _reverse=True)
+        return templates.invert_allgather(ag_rev, f"rs_greedy_{sk.policy}_n{nranks}_p{chunks}", coll="reducescatter")
     lt = apply_sketch(topo, sk)
     if _reverse:
         lt.links = {(v, u): l for (u, v), l in lt.links.items()}

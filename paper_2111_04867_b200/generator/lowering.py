@@ -37,7 +37,7 @@ def _initial(alg: Algorithm, r: int):
         return {r * p + k: ("i", k) for k in range(p)}
     if alg.coll == "alltoall":
         return {(r * n + d) * p + k: ("i", d * p + k) for d in range(n) for k in range(p)}
-    return {k: ("i", k) for k in range(n * p)}
+    return {k: ("i", k) for k in range(n * p)}  # allreduce, reducescatter
 
 
 def _dst_locations(alg: Algorithm):
@@ -52,6 +52,13 @@ def _dst_locations(alg: Algorithm):
                 locs.append(("o", c))
             elif alg.coll == "allreduce":
                 locs.append(("o", c))
+            elif alg.coll == "reducescatter":
+                # the owner (c // p) reduces into its output; relays keep partials in scratch
+                if t.dst == c // p:
+                    locs.append(("o", c % p))
+                else:
+                    sl = scratch[t.dst].setdefault(c, len(scratch[t.dst]))
+                    locs.append(("s", sl))
             else:
                 s, d, k = a2a_parts(c, n, p)
                 if t.dst == d:
@@ -129,6 +136,9 @@ def _instructions(alg: Algorithm):
             instrs[r].append(dict(type="cpy", peer=-1, src=("i", 0), dst=("o", r * p), cnt=p))
         elif alg.coll == "alltoall":
             instrs[r].append(dict(type="cpy", peer=-1, src=("i", r * p), dst=("o", r * p), cnt=p))
+        elif n == 1:  # one rank: the reduction of one contribution is a copy
+            instrs[r].append(dict(type="cpy", peer=-1, src=("i", 0),
+                                  dst=("o", 0), cnt=p))
     return instrs, n_scratch
 
 
@@ -201,7 +211,7 @@ def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, n
     n, p = alg.nranks, alg.chunks_per_rank
     instrs, n_scratch = _instructions(alg)
     _check_pairing(instrs)
-    n_in, n_out = (p, n * p) if alg.coll == "allgather" else (n * p, n * p)
+    n_in, n_out = {"allgather": (p, n * p), "reducescatter": (n * p, p)}.get(alg.coll, (n * p, n * p))
     mx = "inf" if max_bytes == math.inf else str(int(max_bytes))
     out = [f'<algo name="{name or alg.name}" coll="{alg.coll}" nranks="{n}" chunks_per_rank="{p}" '
            f'instances="{instances}" minBytes="{int(min_bytes)}" maxBytes="{mx}" inplace="0">']

@@ -9,7 +9,8 @@
   chunks, then an intra-node all-pairs Allgather of the chunks that arrived from the other
   node; Alltoall coalesces all chunks for the other node over that one link
    and relays them.
-* reduce-scatter as the inverse of an Allgather, Allreduce as reduce-scatter followed by
+* reduce-scatter as the inverse of an Allgather (also the standalone ReduceScatter
+  collective), Allreduce as reduce-scatter followed by
   Allgather with per-chunk chaining.
 Times are abstract (unit per hop; `inter_lat` for emulated inter-node hops).
 """
@@ -96,12 +97,13 @@ def hier_alltoall(nodes_k, p=1, inter_lat=3.0):
 
 # ------------------------------------------------------------------------------ combining
 
-def invert_allgather(ag: Algorithm, name=None) -> Algorithm:
+def invert_allgather(ag: Algorithm, name=None, coll="allreduce") -> Algorithm:
     """ReduceScatter from an Allgather: every send (c, u->v) becomes a
     reduce-receive (c, v->u) and time runs backwards, so contributions flow toward the
-    chunk's owner along the reversed multicast tree."""
-    T = max(t.arrive_time for t in ag.transfers)
-    rs = Algorithm(name or ag.name.replace("ag_", "rs_"), "allreduce", ag.nranks, ag.chunks_per_rank)
+    chunk's owner along the reversed multicast tree. coll="allreduce" gives the first phase
+    of an Allreduce; coll="reducescatter" the standalone collective (owner keeps its part)."""
+    T = max((t.arrive_time for t in ag.transfers), default=0.0)
+    rs = Algorithm(name or ag.name.replace("ag_", "rs_"), coll, ag.nranks, ag.chunks_per_rank)
     for t in sorted(ag.transfers, key=lambda t: (-t.arrive_time, t.src, t.dst)):
         rs.add(t.chunks, t.dst, t.src, T - t.arrive_time, reduce=True, arrive=T - t.send_time)
     return rs
@@ -111,12 +113,20 @@ def allreduce(rs: Algorithm, ag: Algorithm, name) -> Algorithm:
     """Allreduce = ReduceScatter ++ Allgather; AR chunk k is AG chunk k (owner
     k // p). The Allgather phase is shifted after the last reduce so each chunk's phase-2
     sends follow its reduction (per-chunk chaining via lowering's dependencies)."""
-    T = max(t.arrive_time for t in rs.transfers)
+    T = max((t.arrive_time for t in rs.transfers), default=0.0)
     ar = Algorithm(name, "allreduce", rs.nranks, rs.chunks_per_rank)
     ar.transfers = list(rs.transfers)
     for t in ag.transfers:
         ar.add(t.chunks, t.src, t.dst, t.send_time + T, arrive=t.arrive_time + T)
     return ar
+
+
+def ring_reducescatter(n, p=1):
+    return invert_allgather(ring_allgather(n, p), coll="reducescatter")
+
+
+def direct_reducescatter(n, p=1):
+    return invert_allgather(direct_allgather(n, p), coll="reducescatter")
 
 
 def ring_allreduce(n, p=1):
@@ -137,4 +147,6 @@ TEMPLATES = {
     ("alltoall", "direct"): direct_alltoall,
     ("allreduce", "ring"): ring_allreduce,
     ("allreduce", "direct"): direct_allreduce,
+    ("reducescatter", "ring"): ring_reducescatter,
+    ("reducescatter", "direct"): direct_reducescatter,
 }

@@ -13,9 +13,10 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtaccl.so")
 
-ALLGATHER, ALLTOALL, ALLREDUCE = 0, 1, 2
+ALLGATHER, ALLTOALL, ALLREDUCE, REDUCESCATTER = 0, 1, 2, 3
 INT32, FLOAT32, BFLOAT16 = 0, 1, 2
-COLLS = {"allgather": ALLGATHER, "alltoall": ALLTOALL, "allreduce": ALLREDUCE}
+COLLS = {"allgather": ALLGATHER, "alltoall": ALLTOALL, "allreduce": ALLREDUCE, "reducescatter": REDUCESCATTER}
+REDUCING = (ALLREDUCE, REDUCESCATTER)
 ERRORS = {0: "SUCCESS", 1: "INVALID_ARG", 2: "INVALID_SCHEDULE", 3: "NO_ALGO", 4: "CUDA",
           5: "UNSUPPORTED", 6: "TIMEOUT", 7: "NOT_INITIALIZED", 8: "NOT_REGISTERED"}
 HANDLE_BYTES = 128
@@ -88,10 +89,10 @@ def validate(text: str, direct: bool = True):
 
 def dtype_code(t, coll):
     import torch
-    if coll == ALLREDUCE:
+    if coll in REDUCING:
         m = {torch.int32: INT32, torch.float32: FLOAT32, torch.bfloat16: BFLOAT16}
         if t.dtype not in m:
-            raise TypeError(f"allreduce supports int32/float32/bfloat16, got {t.dtype}")
+            raise TypeError(f"allreduce/reducescatter support int32/float32/bfloat16, got {t.dtype}")
         return m[t.dtype]
     # AG / A2A move raw bytes: only the element size matters
     es = t.element_size()
@@ -160,7 +161,7 @@ class Comm:
         """One collective call; `coll` in COLLS. Tensors are contiguous CUDA tensors."""
         c = COLLS[coll] if isinstance(coll, str) else coll
         n = self.nranks
-        count = inp.numel() if c != ALLTOALL else inp.numel() // n
+        count = inp.numel() // n if c in (ALLTOALL, REDUCESCATTER) else inp.numel()
         self.register(out)
         _check(lib().taccl_run(c, ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                count, dtype_code(inp, c), _stream(stream)))
@@ -168,7 +169,7 @@ class Comm:
     def run_emulated(self, coll, outs, inps, stream=None):
         c = COLLS[coll] if isinstance(coll, str) else coll
         n = self.nranks
-        count = inps[0].numel() if c != ALLTOALL else inps[0].numel() // n
+        count = inps[0].numel() // n if c in (ALLTOALL, REDUCESCATTER) else inps[0].numel()
         S = (ctypes.c_void_p * n)(*[x.data_ptr() for x in inps])
         R = (ctypes.c_void_p * n)(*[x.data_ptr() for x in outs])
         _check(lib().taccl_run_emulated(c, S, R, count, dtype_code(inps[0], c), _stream(stream)))
@@ -177,7 +178,7 @@ class Comm:
         """End-to-end: host input -> device -> collective -> host output (numpy or pinned torch)."""
         c = COLLS[coll] if isinstance(coll, str) else coll
         n = self.nranks
-        count = host_in.numel() if c != ALLTOALL else host_in.numel() // n
+        count = host_in.numel() // n if c in (ALLTOALL, REDUCESCATTER) else host_in.numel()
         _check(lib().taccl_run_host(c, ctypes.c_void_p(host_in.data_ptr()), ctypes.c_void_p(host_out.data_ptr()),
                                     count, dtype_code(host_in, c), _stream(stream)))
 
@@ -202,6 +203,9 @@ class Comm:
 
     def all_reduce(self, out, inp, stream=None):
         self.run(ALLREDUCE, out, inp, stream)
+
+    def reduce_scatter(self, out, inp, stream=None):
+        self.run(REDUCESCATTER, out, inp, stream)
 
 
 def launch_count() -> int:

@@ -47,7 +47,7 @@ def test_named_mutations_cpp(f, op, sem, direct, cite):
 
 GEN = [(c, a, n, p) for c, a in [("allgather", "ring"), ("allgather", "direct"), ("alltoall", "direct"),
                                  ("allreduce", "ring"), ("allreduce", "direct"), ("allgather", "hier"),
-                                 ("alltoall", "hier")]
+                                 ("alltoall", "hier"), ("reducescatter", "ring"), ("reducescatter", "direct")]
        for n in (2, 4, 8) for p in (1, 2)]
 
 
@@ -100,7 +100,7 @@ def test_mutation_corpus_verdicts_agree():
     bases = [golden("c1_ag_ring_n2_p2.xml"), golden("ar_rsag_n2_p1.xml")]
     for c, a, n, p in [("allgather", "ring", 3, 1), ("allgather", "direct", 3, 2), ("alltoall", "direct", 3, 1),
                        ("allreduce", "ring", 3, 1), ("allreduce", "direct", 4, 1), ("alltoall", "hier", 4, 1),
-                       ("allgather", "hier", 4, 1)]:
+                       ("allgather", "hier", 4, 1), ("reducescatter", "ring", 3, 1), ("reducescatter", "direct", 3, 2)]:
         bases.append(generate(c, a, n, p, 1))
     total, kinds = 0, {}
     for base in bases:

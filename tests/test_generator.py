@@ -21,6 +21,11 @@ MATRIX = [(c, a, n, p, kw)
           if (c, a) != ("alltoall", "ring")]
 MATRIX += [(c, "hier", n, p, {}) for c in ("allgather", "alltoall") for n in (4, 8) for p in (1, 2)]
 MATRIX += [(c, "greedy", 8, p, {"topology": "2x4"}) for c in ("allgather", "alltoall", "allreduce") for p in (1, 2)]
+MATRIX += [("reducescatter", a, n, p, kw) for a, kw in (("ring", {}), ("direct", {}), ("greedy", {"policy": "uc-max"}),
+                                                        ("greedy", {"policy": "uc-min"}))
+           for n in (2, 3, 4, 8) for p in (1, 2)]
+MATRIX += [("reducescatter", "direct", 1, p, {}) for p in (1, 2)]
+MATRIX += [("reducescatter", "greedy", 8, p, {"topology": "2x4"}) for p in (1, 2)]
 
 
 @pytest.mark.parametrize("coll,algo,n,p,kw", MATRIX, ids=[f"{m[0]}-{m[1]}-n{m[2]}-p{m[3]}-{m[4]}" for m in MATRIX])
@@ -32,7 +37,7 @@ def test_generated_schedule_is_correct(coll, algo, n, p, kw):
     prog = oracle.parse(text)
     rng = np.random.default_rng(n * 100 + p)
     count = (n * p if coll != "allgather" else p) * 3
-    e_in = n * count if coll == "alltoall" else count
+    e_in = n * count if coll in ("alltoall", "reducescatter") else count
     ins = [rng.integers(-1000, 1000, e_in).astype(np.int32) for _ in range(n)]
     outs = oracle.run(prog, ins, "int32")
     want = oracle.expected_outputs(coll, ins, "int32")

@@ -40,13 +40,13 @@ def _worker(rank, n, port, cases, q):
         for (coll, algo, p, m, dtype, count, kind) in cases:
             text = generate(coll, algo, n, p, m)
             h = comm.load(text)
-            e_in = n * count if coll == "alltoall" else count
-            if coll == "allreduce":
+            e_in = n * count if coll in ("alltoall", "reducescatter") else count
+            if coll in ("allreduce", "reducescatter"):
                 ins = [allreduce_input(e_in, dtype, kind, 21, r) for r in range(n)]
             else:
                 ins = [random_bits(e_in, dtype, 22, r) for r in range(n)]
             x = torch.from_numpy(ins[rank].view(view[dtype])).view(tdt[dtype]).cuda()
-            e_out = n * count if coll != "allreduce" else count
+            e_out = count if coll in ("allreduce", "reducescatter") else n * count
             out = torch.empty(e_out, dtype=tdt[dtype], device="cuda")
             for _ in range(3):  # repeated calls exercise epochs / entry handshakes
                 out.view(torch.uint8).fill_(0xA5)
@@ -73,6 +73,8 @@ CASES = [
     ("allreduce", "ring", 2, 1, "bfloat16", 8 * 4099, "intval"),
     ("allreduce", "direct", 1, 2, "float32", 2 * (1 << 18), "intval"),
     ("allgather", "direct", 1, 1, "bfloat16", 3, None),
+    ("reducescatter", "direct", 1, 1, "float32", 1 << 17, "intval"),
+    ("reducescatter", "ring", 2, 2, "int32", 2 * 3001, "bits"),
 ]
 
 

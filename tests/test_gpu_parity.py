@@ -47,7 +47,7 @@ def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20, mode=None):
     try:
         comm.load(text)
         dev_in = [to_dev(x, dtype) for x in ins]
-        e_out = ins[0].size * n if coll == "allgather" else ins[0].size
+        e_out = {"allgather": ins[0].size * n, "reducescatter": ins[0].size // n}.get(coll, ins[0].size)
         dev_out = [torch.full((e_out,), 0, dtype=TDT[dtype], device="cuda") for _ in range(n)]
         for o in dev_out:  # poison, like the oracle's 0xA5 output
             o.view(torch.uint8).fill_(0xA5)
@@ -199,6 +199,40 @@ def test_allreduce_tolerance_normal_normwise(dtype, tol):
     got = run_gpu(text, "allreduce", n, dtype, ins)
     for g in got:
         assert (np.abs(oracle.collectives.to_f64(g, dtype) - ref) / scale).max() <= tol
+
+
+# ---------------------------------------------------------------- ReduceScatter
+
+RS = [("ring", 2, 1, 1), ("ring", 4, 2, 2), ("ring", 8, 1, 4), ("direct", 2, 1, 1), ("direct", 4, 2, 1),
+      ("direct", 8, 1, 8), ("direct", 1, 1, 1), ("greedy", 8, 2, 1)]
+
+
+@pytest.mark.parametrize("algo,n,p,m", RS)
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_reducescatter_exact(algo, n, p, m, dtype, mode):
+    # ReduceScatter as the inverse of an Allgather; count = elements per rank
+    count = p * 1013 if dtype == "bfloat16" else p * 2051
+    text = generate("reducescatter", algo, n, p, m)
+    kind = "bits" if dtype == "int32" else "intval"
+    ins = [allreduce_input(n * count, dtype, kind, 12, r) for r in range(n)]
+    got = run_gpu(text, "reducescatter", n, dtype, ins, mode=mode)
+    if dtype == "int32":
+        assert_bits_equal(got, oracle.expected_outputs("reducescatter", ins, "int32"))
+    assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
+
+
+@pytest.mark.parametrize("algo,n,dtype,tol", [("direct", 8, "float32", 1e-6), ("ring", 4, "float32", 1e-6),
+                                              ("direct", 8, "bfloat16", 1e-2), ("ring", 4, "bfloat16", 1e-2)])
+def test_reducescatter_tolerance_uniform(algo, n, dtype, tol):
+    count = 30000
+    text = generate("reducescatter", algo, n, 1, 1)
+    ins = [allreduce_input(n * count, dtype, "uniform", 13, r) for r in range(n)]
+    ref = oracle.expected_reducescatter_f64(ins, dtype)
+    got = run_gpu(text, "reducescatter", n, dtype, ins)
+    for g, w in zip(got, ref):
+        rel = np.abs(oracle.collectives.to_f64(g, dtype) - w) / np.abs(w)
+        assert rel.max() <= tol, rel.max()
 
 
 # ---------------------------------------------------------------- edge cases

@@ -66,6 +66,40 @@ def test_allreduce_int32_wraps_like_bigint(n):
             assert int(o[i]) == s
 
 
+@pytest.mark.parametrize("n,count", [(1, 4), (2, 3), (3, 5), (8, 2)])
+def test_reducescatter_definition_elementwise(n, count):
+    # ReduceScatter: rank r keeps the point-wise sum of part r,
+    # written out with Python big integers and reduced mod 2^32 (reading G13)
+    ins = _rand(n, n * count, 6)
+    outs = C.expected_outputs("reducescatter", ins, "int32")
+    for r in range(n):
+        assert outs[r].size == count
+        for i in range(count):
+            s = sum(int(x[r * count + i]) for x in ins) % 2**32
+            assert int(outs[r][i]) == (s - 2**32 if s >= 2**31 else s)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_allgather_of_reducescatter_is_allreduce(n):
+    # Allreduce = ReduceScatter followed by Allgather
+    ins = _rand(n, n * 3, 7)
+    rs = C.expected_outputs("reducescatter", ins, "int32")
+    ag = C.expected_outputs("allgather", rs, "int32")
+    ar = C.expected_outputs("allreduce", ins, "int32")
+    for a, b in zip(ag, ar):
+        assert np.array_equal(a, b)
+
+
+def test_reducescatter_f64_matches_fsum():
+    rng = np.random.default_rng(8)
+    n, count = 4, 25
+    ins = [rng.standard_normal(n * count).astype(np.float32) for _ in range(n)]
+    ref = C.expected_reducescatter_f64(ins, "float32")
+    for r in range(n):
+        for i in range(count):
+            assert ref[r][i] == pytest.approx(math.fsum(float(x[r * count + i]) for x in ins), rel=1e-15, abs=1e-15)
+
+
 def test_allreduce_f64_matches_fsum():
     rng = np.random.default_rng(5)
     ins = [rng.standard_normal(100).astype(np.float32) for _ in range(8)]
@@ -83,6 +117,10 @@ def test_chunk_geometry_table():
     assert C.chunk_elems("allreduce", 8, 1, 8 * 1000) == 1000
     with pytest.raises(ValueError):
         C.chunk_elems("allreduce", 8, 1, 1001)
+    # ReduceScatter: input n*count (n*p chunks), output count (the rank's p chunks)
+    assert C.buffer_chunks("reducescatter", 8, 2) == (16, 2)
+    assert C.chunk_elems("reducescatter", 8, 2, 1000) == 500
+    assert C.postcondition("reducescatter", 4, 2)[3] == {0: (6, (1, 1, 1, 1)), 1: (7, (1, 1, 1, 1))}
 
 
 def test_pre_and_postconditions_shapes():

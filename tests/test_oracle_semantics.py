@@ -49,7 +49,7 @@ def linear_extensions(graph, limit):
 def _inputs(prog, count, dtype, seed):
     rng = np.random.default_rng(seed)
     n = prog.nranks
-    e_in = n * count if prog.coll == "alltoall" else count
+    e_in = n * count if prog.coll in ("alltoall", "reducescatter") else count
     if dtype == "int32":
         return [rng.integers(-2**31, 2**31, e_in, dtype=np.int64).astype(np.int32) for _ in range(n)]
     return [rng.integers(0, 1 << 16, e_in).astype(np.uint16) for _ in range(n)]
@@ -77,6 +77,18 @@ def test_all_linearisations_c1():
 def test_all_linearisations_gar():
     total = _check_all_orders(oracle.parse(golden("ar_rsag_n2_p1.xml")), 6, "int32")
     assert total > 1
+
+
+@pytest.mark.parametrize("algo,n", [("ring", 3), ("direct", 2)])
+def test_all_linearisations_reducescatter(algo, n):
+    # generator text is only an input here: every order must give the definition's result
+    from paper_2111_04867_b200.generator import generate
+    prog = oracle.parse(generate("reducescatter", algo, n, 1, 1))
+    total = _check_all_orders(prog, 4, "int32")
+    assert total > 1
+    ins = _inputs(prog, 4, "int32", 11)
+    want = oracle.expected_outputs("reducescatter", ins, "int32")
+    assert all(np.array_equal(a, b) for a, b in zip(oracle.run(prog, ins, "int32"), want))
 
 
 def test_allgather_output_matches_definition_on_golden():

@@ -24,7 +24,8 @@ import torch.distributed as dist  # noqa: E402
 from paper_2111_04867_b200 import taccl  # noqa: E402
 from paper_2111_04867_b200.generator import generate  # noqa: E402
 
-ALGOS = {"allgather": ["direct", "ring"], "alltoall": ["direct"], "allreduce": ["direct", "ring"]}
+ALGOS = {"allgather": ["direct", "ring"], "alltoall": ["direct"], "allreduce": ["direct", "ring"],
+         "reducescatter": ["direct", "ring"]}
 
 
 def factor(coll, n):
@@ -96,7 +97,7 @@ def timeit(fn, stream, world, target_ms=50.0):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--colls", default="allgather,alltoall,allreduce")
+    ap.add_argument("--colls", default="allgather,alltoall,allreduce,reducescatter")
     ap.add_argument("--size-lo", type=int, default=10, help="smallest size 2^lo bytes")
     ap.add_argument("--size-hi", type=int, default=30, help="largest size 2^hi bytes")
     ap.add_argument("--dtype", default="bfloat16")
@@ -134,10 +135,13 @@ def main():
             elif coll == "alltoall":
                 count = S // es // n
                 inp, out = big_in[:n * count], big_out[:n * count]
+            elif coll == "reducescatter":  # S = send bytes (nccl-tests)
+                count = S // es // n
+                inp, out = big_in[:n * count], big_out[:count]
             else:
                 count = S // es
                 inp, out = big_in[:count], big_out[:count]
-            if count == 0 or (coll != "allgather" and count % n):
+            if count == 0 or (coll in ("alltoall", "allreduce") and count % n):
                 continue
             inp.copy_(torch.randint(-8, 8, inp.shape, device="cuda").to(dt))
             rec = {"coll": coll, "n": n, "S": S, "dtype": a.dtype, "graph": a.graph}
@@ -159,6 +163,8 @@ def main():
                     f = lambda: dist.all_gather_into_tensor(out, inp)  # noqa: E731
                 elif coll == "alltoall":
                     f = lambda: dist.all_to_all_single(out, inp)  # noqa: E731
+                elif coll == "reducescatter":
+                    f = lambda: dist.reduce_scatter_tensor(out, inp)  # noqa: E731
                 else:
                     f = lambda: dist.all_reduce(out, op=dist.ReduceOp.SUM)  # noqa: E731
                 ms, it = tf(f, stream, world)
