@@ -157,6 +157,15 @@ taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dt
 /* Number of executor kernel launches issued by this process so far. */
 uint64_t taccl_launch_count(void);
 
+/* Device-side step timeline (SURVEY.md §5 tracing). `dev_buf` is a device buffer of `bytes`
+ * bytes owned by the caller; while set, every launch overwrites it with TACCL_TRACE_SLOTS
+ * u64 %globaltimer stamps (ns) per CTA, CTA-major (layout in taccl_internal.h): entry,
+ * prologue end, then per step start / waits satisfied / done, identity word, exit. CTAs
+ * beyond bytes / (8 * TACCL_TRACE_SLOTS) are not traced. NULL disables (the default).
+ * Returns INVALID_ARG if bytes is smaller than one CTA's record. */
+#define TACCL_TRACE_SLOTS 64
+taccl_result_t taccl_trace(void* dev_buf, size_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -244,6 +244,168 @@ __device__ void reduce_dispatch(int dtype, char* dst, char* dst2, const char* sr
   else cta_reduce<TACCL_BFLOAT16>(dst, dst2, src0, stages, ns, soff, nelem);
 }
 
+// ---------------------------------------------------------------- LL (small-message) protocol
+// Staged mode moves payload in 16-byte LL lines {p0, flag, p1, flag}: 8 payload bytes and
+// the call's flag twice, written with ONE 16-byte store into the receiver's parity slot.
+// A line is valid when both flags equal the call's flag, so no memory fence and no
+// separate flag message is needed per hop (a fence.acq_rel.sys costs ~1.5 us on B200,
+// tools/lat_probe.cu); the price is 2x bytes, paid only below TACCL_STAGED_MAX.
+__device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile_v4(void* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+// wait until line p carries `flag` in both flag words; false on timeout
+__device__ __forceinline__ bool ll_wait(const char* p, unsigned flag, uint4* out, u64 timeout_ns) {
+  uint4 v = ld_volatile_v4(p);
+  if (v.y == flag && v.w == flag) {
+    *out = v;
+    return true;
+  }
+  const u64 t0 = globaltimer();
+  for (;;) {
+    for (int i = 0; i < 64; ++i) {
+      v = ld_volatile_v4(p);
+      if (v.y == flag && v.w == flag) {
+        *out = v;
+        return true;
+      }
+    }
+    if (globaltimer() - t0 > timeout_ns) return false;
+  }
+}
+// nb payload bytes at p (any alignment; nb <= 8) <-> one u64 (little-endian byte order)
+__device__ __forceinline__ u64 ld_bytes(const char* p, int nb) {
+  if (nb == 8 && ((uintptr_t)p & 7) == 0) return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+  u64 v = 0;
+  if (((uintptr_t)p & 1) == 0 && (nb & 1) == 0) {
+    for (int b = 0; b < nb; b += 2) v |= (u64)__ldcg(reinterpret_cast<const unsigned short*>(p + b)) << (8 * b);
+  } else {
+    for (int b = 0; b < nb; ++b) v |= (u64)(unsigned char)p[b] << (8 * b);
+  }
+  return v;
+}
+__device__ __forceinline__ void st_bytes(char* p, u64 v, int nb) {
+  if (nb == 8 && ((uintptr_t)p & 7) == 0) {
+    *reinterpret_cast<u64*>(p) = v;
+  } else if (((uintptr_t)p & 1) == 0 && (nb & 1) == 0) {
+    for (int b = 0; b < nb; b += 2) *reinterpret_cast<unsigned short*>(p + b) = (unsigned short)(v >> (8 * b));
+  } else {
+    for (int b = 0; b < nb; ++b) p[b] = (char)(v >> (8 * b));
+  }
+}
+__device__ __forceinline__ uint4 ll_line(u64 v, unsigned flag) {
+  return make_uint4((unsigned)v, flag, (unsigned)(v >> 32), flag);
+}
+
+// One LL step: lines [l0, l1) of every one of the message's cnt chunks (chunk-relative, so
+// piece j covers the same bytes of a chunk in every message, as for_piece does), every thread
+// its own lines. Chunk q's payload is bytes [q*cb, (q+1)*cb) of src/dst and LL lines
+// [q*llcb, (q+1)*llcb) of a slot. out = (src if given) (+) in_0 (+) ... (+) in_{nin-1}; the
+// reduction (+) runs only when `reduce` (else the single input or src moves as raw bits).
+// out goes to dst (local, if given) and/or fwd (a peer LL slot, if given). Returns false if
+// a wait timed out.
+template <int DT>
+__device__ __noinline__ bool ll_lines(bool reduce, const char* src, char* dst, const char* const* ins, int nin, char* fwd,
+                         int64_t cb, int64_t llcb, int cnt, int64_t l0, int64_t l1, unsigned flag, u64 timeout_ns) {
+  using Et = Elt<DT>;
+  constexpr int EB = Et::bytes, NE = 8 / EB, U = 4;  // U lines in flight per thread
+  constexpr unsigned MASK = EB == 4 ? 0xffffffffu : 0xffffu;
+  const int nt = blockDim.x;
+  for (int q = 0; q < cnt; ++q)
+  for (int64_t base = l0 + threadIdx.x; base < l1; base += U * nt) {
+    int64_t pb[U], lb[U];
+    int vb[U];
+    u64 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t ll = base + u * nt;
+      pb[u] = q * cb + 8 * ll;    // payload byte offset
+      lb[u] = q * llcb + 16 * ll;  // LL byte offset
+      vb[u] = ll < l1 ? (int)min((int64_t)8, cb - 8 * ll) : 0;  // valid payload bytes
+      v[u] = (src && vb[u]) ? ld_bytes(src + pb[u], vb[u]) : 0;
+    }
+    if (!reduce) {
+      if (nin) {
+        uint4 w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (vb[u]) w[u] = ld_volatile_v4(ins[0] + lb[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (vb[u]) {
+            if ((w[u].y != flag || w[u].w != flag) && !ll_wait(ins[0] + lb[u], flag, &w[u], timeout_ns)) return false;
+            v[u] = (u64)w[u].x | ((u64)w[u].z << 32);
+          }
+      }
+    } else {
+      typename Et::acc acc[U][NE];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const unsigned r = (unsigned)(v[u] >> (8 * EB * e)) & MASK;
+          if constexpr (DT == TACCL_BFLOAT16) acc[u][e] = __uint_as_float(r << 16);
+          else if constexpr (DT == TACCL_FLOAT32) acc[u][e] = __uint_as_float(r);
+          else acc[u][e] = r;
+        }
+      for (int i = 0; i < nin; ++i) {
+        uint4 w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (vb[u]) w[u] = ld_volatile_v4(ins[i] + lb[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!vb[u]) continue;
+          if ((w[u].y != flag || w[u].w != flag) && !ll_wait(ins[i] + lb[u], flag, &w[u], timeout_ns)) return false;
+          const u64 y = (u64)w[u].x | ((u64)w[u].z << 32);
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            const unsigned r = (unsigned)(y >> (8 * EB * e)) & MASK;
+            typename Et::acc x;
+            if constexpr (DT == TACCL_BFLOAT16) x = __uint_as_float(r << 16);
+            else if constexpr (DT == TACCL_FLOAT32) x = __uint_as_float(r);
+            else x = r;
+            acc[u][e] = Et::add(acc[u][e], x);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = 0;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          u64 r;
+          if constexpr (DT == TACCL_BFLOAT16) r = Et::rn(acc[u][e]);
+          else if constexpr (DT == TACCL_FLOAT32) r = __float_as_uint(acc[u][e]);
+          else r = (unsigned)acc[u][e];
+          v[u] |= r << (8 * EB * e);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!vb[u]) continue;
+      if (dst) st_bytes(dst + pb[u], v[u], vb[u]);
+      if (fwd) st_volatile_v4(fwd + lb[u], ll_line(v[u], flag));
+    }
+  }
+  return true;
+}
+
+__device__ bool ll_dispatch(int dtype, bool reduce, const char* src, char* dst, const char* const* ins, int nin,
+                            char* fwd, int64_t cb, int64_t llcb, int cnt, int64_t l0, int64_t l1, unsigned flag,
+                            u64 timeout_ns) {
+  if (!reduce || dtype == TACCL_INT32)
+    return ll_lines<TACCL_INT32>(reduce, src, dst, ins, nin, fwd, cb, llcb, cnt, l0, l1, flag, timeout_ns);
+  if (dtype == TACCL_FLOAT32)
+    return ll_lines<TACCL_FLOAT32>(true, src, dst, ins, nin, fwd, cb, llcb, cnt, l0, l1, flag, timeout_ns);
+  return ll_lines<TACCL_BFLOAT16>(true, src, dst, ins, nin, fwd, cb, llcb, cnt, l0, l1, flag, timeout_ns);
+}
+
 // ---------------------------------------------------------------- the interpreter
 struct Ctx {
   const KArgs* a;
@@ -297,23 +459,36 @@ __device__ void record_error(const Ctx& c, int what, int step) {
   }
 }
 
+// LL = staged (small-message) mode, a compile-time specialisation so each variant carries
+// only its own data path (register pressure: the LL variant inlines its line loop).
+template <bool LL>
 __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_constant__ KArgs A) {
   __shared__ int s_abort;
   __shared__ u64 s_epoch;
   __shared__ const char* s_stage[kMaxRanks + 1];
   extern __shared__ int4 s_plan[];
   const int tid = threadIdx.x;
-  int lr = 0;
-  while (lr + 1 < A.nlocal && (int)blockIdx.x >= A.r[lr + 1].cta_begin) ++lr;
+  u64 t_entry = 0;
+  if (A.trace && tid == 0) t_entry = globaltimer();
+  // this CTA's (local rank, threadblock, first piece, CTAs of the tb), computed on the host
+  const unsigned me = A.cta_map[blockIdx.x];
+  const int lr = cta_lr(me), t = cta_tb(me), c0 = cta_c0(me), ct = cta_ct(me);
   const KRank& R = A.r[lr];
-  const int local = blockIdx.x - R.cta_begin;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
   // the rank's plan (a few KB) moves to shared memory in one cooperative pass, overlapped
   // with the epoch load, instead of a chain of dependent global loads per step
   const char* planp = R.plan;
   if (tid == 0) {
-    s_epoch = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
+    const u64 ep = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
+    s_epoch = ep;
     s_abort = 0;
+    // arrival: the rank's CTA 0 advances the epoch at its end once every other CTA of the
+    // rank has read it. The added value depends on the loaded epoch (always 1), so the
+    // reduction cannot overtake the load.
+    if (c0 != 0 || t != 0) {
+      const unsigned one = 1u + (unsigned)(ep >> 62);
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&ctrl->finished), "r"(one) : "memory");
+    }
   }
   if (A.plan_smem) {
     const int4* g = reinterpret_cast<const int4*>(R.plan);
@@ -328,18 +503,11 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   // CTA (t, c0) runs pieces j = c0, c0 + C, ... of threadblock t, each piece's whole program
   // before the next (every CTA visits pieces in increasing order, so a wait on piece j only
   // ever depends on piece-j work of CTAs that have finished all their pieces < j).
-  int t = 0, ct = 0, acc = 0;
-  for (;; ++t) {
-    ct = tbs[t].indep ? tb_pieces(1, tbs[t].weight, R.wsum, R.budget, A.split, A.indep_cap) : A.dep_ctas;
-    if (local < acc + ct || t + 1 == R.ntb) break;
-    acc += ct;
-  }
-  const int nsplit = tbs[t].indep ? ct : A.split;  // this tb's piece count
+  const int nsplit = cta_indep(me) ? ct : A.split;  // this tb's piece count
   Ctx c{&A, &R, t, 0, 0};
-  const int c0 = local - acc;
   c.epoch = s_epoch;
   const u64 E = c.epoch << 24;
-  const KTB tb = tbs[c.t];
+  const KTB& tb = tbs[c.t];  // plan lives in shared memory (or global): read fields on use
   u64* my_data = reinterpret_cast<u64*>(R.arena + kOffData);
   u64* my_ready = reinterpret_cast<u64*>(R.arena + kOffReady);
   u64* my_done = reinterpret_cast<u64*>(R.arena + kOffDone);
@@ -349,53 +517,85 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
   // every rank heard from every other rank during the call in between)
   const int64_t parity_off = kOffScratch + (int64_t)(c.epoch & 1) * A.staged_bytes;
   char* const my_staged = R.arena + parity_off;
+  const int64_t ll_cb = 16 * ((cbytes + 7) / 8);  // LL bytes per chunk slot
+  const unsigned ll_flag = (unsigned)c.epoch;
+  u64* const trace = (A.trace && tid == 0 && blockIdx.x < A.trace_ctas) ? A.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  if (trace) {
+    trace[0] = t_entry;
+    trace[1] = globaltimer();
+    trace[kTraceSlots - 2] = ((u64)R.rank << 32) | ((u64)c.t << 16) | (u64)c0;
+  }
 
   for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
     // entry handshake: tell our sender we are in this call (its stores may now land)
-    if (!A.staged && tb.recv >= 0 && tid == 0) {
+    if (!LL && tb.recv >= 0 && tid == 0) {
       u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
       st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
     }
     bool sender_ready = false;
 
     for (int k = 0; k < tb.nsteps; ++k) {
-      const KStep st = steps[tb.step_begin + k];
+      const KStep& st = steps[tb.step_begin + k];
+      const bool tr = trace && j == c0 && k < kTraceSteps;
+      if (tr) trace[2 + 3 * k] = globaltimer();
       if (tid == 0) {
         bool ok = true;
         for (int d = 0; d < st.dep_count && ok; ++d) {
           const int dt = deps[2 * (st.dep_begin + d)], dk = deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
-        if (ok && !A.staged && (st.op == K_SEND || st.op == K_RRCS) && !sender_ready) {
+        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS) && !sender_ready) {
           ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
           sender_ready = true;
         }
-        if (ok && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS))
+        // staged (LL) mode: no data flags, every line carries its own (ll_lines)
+        if (ok && !LL && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS))
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
         if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
             const int* fz = fused + 4 * (st.fuse_begin + f);
             const KTB o = tbs[fz[0]];
-            ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
-            s_stage[f] = A.staged ? my_staged + (int64_t)fz[3] * cbytes : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
+            if (!LL) ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
+            s_stage[f] = LL ? my_staged + (int64_t)fz[3] * ll_cb : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
           }
         }
-        if (ok && (st.op == K_RRC || st.op == K_RRCS))
-          s_stage[0] = A.staged ? my_staged + (int64_t)st.soff2 * cbytes : local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
+        if (ok && (st.op == K_RRC || st.op == K_RRCS || st.op == K_RECV))
+          s_stage[0] = LL ? my_staged + (int64_t)st.soff2 * ll_cb : local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
         if (!ok) {
           record_error(c, st.op, k);
           s_abort = 1;
         }
+        if (tr) trace[3 + 3 * k] = globaltimer();
       }
       __syncthreads();
       if (s_abort) return;
 
-      switch (st.op) {
+      if (LL && st.op != K_CPY && st.op != K_NOP && st.op != K_SENT) {
+        // LL path: this piece's lines of every chunk (same split on both sides)
+        const int64_t nl = (cbytes + 7) / 8;
+        int64_t l0 = (int64_t)((unsigned)nl * (unsigned)j / (unsigned)nsplit);  // nl*split < 2^32 (LL sizes)
+        int64_t l1 = (int64_t)((unsigned)nl * (unsigned)(j + 1) / (unsigned)nsplit);
+        if (st.op == K_RRC_FUSED) {  // this member's portion of the piece
+          const int64_t m = l1 - l0, a0 = l0;
+          l0 = a0 + m * st.part / st.nparts;
+          l1 = a0 + m * (st.part + 1) / st.nparts;
+        }
+        const char* src = (st.op == K_RECV) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+        char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+        char* fwd = (st.op == K_SEND || st.op == K_RRCS) ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * ll_cb : nullptr;
+        const bool reduce = st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED;
+        const int nin = st.op == K_SEND ? 0 : st.op == K_RRC_FUSED ? st.fuse_count : 1;
+        const bool ok = ll_dispatch(A.dtype, reduce, src, dst, s_stage, nin, fwd, cbytes, ll_cb, st.cnt, l0, l1, ll_flag,
+                                    A.timeout_ns);
+        if (__syncthreads_or(!ok)) {
+          if (tid == 0) record_error(c, st.op, k);
+          return;
+        }
+      } else switch (st.op) {
         case K_SEND: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
-          char* dst = A.staged ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * cbytes
-                               : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
+          char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
           for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
@@ -409,9 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
         case K_RRCS: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          char* fwd = st.op != K_RRCS ? nullptr
-                      : A.staged ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * cbytes
-                                 : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
+          char* fwd = st.op != K_RRCS ? nullptr : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
           for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             reduce_dispatch(A.dtype, dst + off, fwd ? fwd + off : nullptr, src + off, s_stage, 1, off, len / elt);
           });
@@ -429,14 +627,8 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           });
           break;
         }
-        case K_RECV: {  // zero-copy: the bytes are already in place; staged: copy them out
-          if (A.staged) {
-            const char* src = my_staged + (int64_t)st.soff2 * cbytes;
-            char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-            for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
-          }
+        case K_RECV:  // zero-copy: the bytes are already in place
           break;
-        }
         default:  // K_NOP, K_SENT: no data work on this side
           break;
       }
@@ -451,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           record_error(c, st.op, k);
           s_abort = 1;
         }
-        if (st.op == K_SEND || st.op == K_RRCS) {
+        if (!LL && (st.op == K_SEND || st.op == K_RRCS)) {
           // all threads' peer stores are ordered before this by bar.sync (causality order);
           // the system-scope acq_rel fence makes them visible before the flag (cumulativity)
           if (A.variant != 9) asm volatile("fence.acq_rel.sys;" ::: "memory");  // 9: timing probe only
@@ -459,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)((st.op == K_RRCS ? st.fwd_seq : st.seq) + 1));
         }
         if (st.need_done && ok) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
+        if (tr) trace[4 + 3 * k] = globaltimer();
       }
       if (st.post_count) {
         __syncthreads();
@@ -466,24 +659,32 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
       }
     }
   }
-  // completion: the rank's last CTA advances the rank's epoch for the next call
+  // completion: the rank's CTA 0 advances the rank's epoch for the next call once all other
+  // CTAs of the rank have arrived (read this call's epoch) — by now they normally have, so
+  // this is one L2 read. The next launch is stream-ordered after this one. (A returning
+  // atomic per CTA cost ~0.8 us on the critical path, tools/lat_probe.cu.)
   if (tid == 0) {
-    unsigned total = 0;
-    for (int u = 0; u < R.ntb; ++u)
-      total += tbs[u].indep ? tb_pieces(1, tbs[u].weight, R.wsum, R.budget, A.split, A.indep_cap) : A.dep_ctas;
-    unsigned prev;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctrl->finished) : "memory");
-    if (prev == total - 1) {
+    if (c0 == 0 && t == 0) {
+      const unsigned want = (unsigned)R.ncta - 1;
+      volatile unsigned* fin = &ctrl->finished;
+      const u64 t0 = globaltimer();
+      while (*fin < want)
+        if (globaltimer() - t0 > A.timeout_ns) {
+          record_error(c, K_NOP, -1);
+          break;
+        }
       ctrl->finished = 0;
       *reinterpret_cast<volatile u64*>(&ctrl->epoch) = c.epoch + 1;
     }
+    if (trace) trace[kTraceSlots - 1] = globaltimer();
   }
 }
 
 }  // namespace
 
 int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::string* err) {
-  taccl_exec_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(a);
+  if (a.staged) taccl_exec_kernel<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(a);
+  else taccl_exec_kernel<false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("kernel launch: ") + cudaGetErrorString(e);
@@ -494,7 +695,10 @@ int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::strin
 
 int executor_max_ctas(int device, std::string* err) {
   int per_sm = 0, sms = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, taccl_exec_kernel, kThreads, 0);
+  int per_sm_ll = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, taccl_exec_kernel<false>, kThreads, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ll, taccl_exec_kernel<true>, kThreads, 0);
+  per_sm = per_sm < per_sm_ll ? per_sm : per_sm_ll;
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
     *err = std::string("occupancy query: ") + cudaGetErrorString(e);

@@ -81,6 +81,8 @@ struct Comm {
   int max_ctas = 0;
   uint64_t launches = 0;
   uint64_t timeout_ns = 0;
+  unsigned long long* trace = nullptr;  // taccl_trace buffer (caller-owned)
+  int trace_ctas = 0;
   int64_t staged_bytes = 0;  // one staged-mode parity region (identical on all ranks)
   // host-run staging (taccl_run_host): library-owned pinned bounce is the user's job
 };
@@ -201,7 +203,17 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
     if (a->plans[r].mem) total_tb += a->ntb[r];
   int lanes = 1;
   const size_t forced = env_size("TACCL_LANES", 0);
-  const int64_t min_piece = (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
+  // staged (LL) mode for small messages: no entry handshake, no fences; sends write 16-byte
+  // LL lines (8 payload bytes + flags) into the receiver's parity slot
+  const int64_t sb = staged_region_bytes();
+  const int64_t total_bytes = (int64_t)n_out * G->chunk_bytes;
+  const int64_t ll_cb = 16 * ((G->chunk_bytes + 7) / 8);
+  G->staged = (int64_t)a->max_stage2_chunks * ll_cb <= sb &&
+              total_bytes <= (int64_t)env_size("TACCL_STAGED_MAX", 1 << 20) ? 1 : 0;
+  // bytes per CTA: LL lines are latency-bound, so LL pieces are small (4 KiB of payload per
+  // CTA measured best at n=2 up to 1 MiB, profiles/r01_small_sweep_n2.txt)
+  const int64_t min_piece = G->staged ? (int64_t)env_size("TACCL_LL_MIN_PIECE", 4 << 10)
+                                      : (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
   // 128 CTAs x 512 threads measured best for the HBM copy and 2-GPU pushes (profiles/r01_scan.txt)
   const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", 128));
   int nlocal = 0;
@@ -250,11 +262,6 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   if (G->grid > g.max_ctas)
     return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
                                            std::to_string(g.max_ctas));
-  // staged mode for small messages (no entry handshake; receivers copy out of a parity slot)
-  const int64_t sb = staged_region_bytes();
-  const int64_t total_bytes = (int64_t)n_out * G->chunk_bytes;
-  G->staged = (int64_t)a->max_stage2_chunks * G->chunk_bytes <= sb &&
-              total_bytes <= (int64_t)env_size("TACCL_STAGED_MAX", 256 << 10) ? 1 : 0;
   G->scratch_off = kOffScratch + 2 * sb + base_off;
   G->staging_off = G->scratch_off + (((int64_t)a->max_scratch_chunks * G->chunk_bytes + 255) & ~(int64_t)255);
   G->need = G->staging_off + (int64_t)a->max_stage_chunks * G->chunk_bytes;
@@ -284,6 +291,8 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.scratch_off = G.scratch_off;
   A.staging_off = G.staging_off;
   A.timeout_ns = g.timeout_ns;
+  A.trace = g.trace;
+  A.trace_ctas = g.trace_ctas;
   int cta = 0, smem = 0;
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
@@ -304,12 +313,20 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     }
     R.rank = r;
     R.ntb = dp.ntb;
-    R.cta_begin = cta;
     R.budget = G.budget;
     R.wsum = a->wsum[r];
-    for (int t = 0; t < dp.ntb; ++t)
-      cta += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G.budget, G.split, G.indep_cap) : G.dep_ctas;
+    const int first = cta;
+    for (int t = 0; t < dp.ntb; ++t) {
+      const int ind = a->indep[r][t];
+      const int ct = ind ? tb_pieces(1, a->weights[r][t], a->wsum[r], G.budget, G.split, G.indep_cap) : G.dep_ctas;
+      for (int c = 0; c < ct; ++c) {
+        if (cta >= kMaxGrid) return fail(TACCL_ERR_UNSUPPORTED, "launch exceeds " + std::to_string(kMaxGrid) + " CTAs");
+        A.cta_map[cta++] = cta_pack((int)i, t, c, ct, ind);
+      }
+    }
+    R.ncta = cta - first;
   }
+  A.ncta = cta;
   A.plan_smem = smem <= kPlanSmemMax ? 1 : 0;
   std::string err;
   if (launch_executor(A, cta, A.plan_smem ? smem : 0, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -678,5 +695,19 @@ taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dt
 }
 
 uint64_t taccl_launch_count(void) { return g_launches; }
+
+taccl_result_t taccl_trace(void* dev_buf, size_t bytes) {
+  if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
+  if (!dev_buf) {
+    g.trace = nullptr;
+    g.trace_ctas = 0;
+    return TACCL_SUCCESS;
+  }
+  const size_t per = sizeof(unsigned long long) * kTraceSlots;
+  if (bytes < per) return fail(TACCL_ERR_INVALID_ARG, "trace buffer smaller than one CTA record");
+  g.trace = (unsigned long long*)dev_buf;
+  g.trace_ctas = (int)std::min<size_t>(bytes / per, 1 << 20);
+  return TACCL_SUCCESS;
+}
 
 }  // extern "C"

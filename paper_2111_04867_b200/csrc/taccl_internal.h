@@ -154,7 +154,7 @@ struct KRank {
   char* arena;
   char* peer_out[kMaxRanks];    // peer's output buffer (this call's recvbuf on the peer)
   char* peer_arena[kMaxRanks];  // peer's arena (flags, scratch, staging)
-  int32_t rank, ntb, cta_begin;
+  int32_t rank, ntb, ncta;  // ncta: CTAs of this rank in the launch
   int32_t budget;          // CTAs of this rank: tb t gets tb_ctas(weight_t, wsum, ...)
   int32_t wsum, pad;
 };
@@ -178,7 +178,29 @@ struct KArgs {
   int64_t scratch_off;     // byte offset of the EF scratch buffer inside every arena
   int64_t staging_off;     // byte offset of the rrc staging area inside every arena
   uint64_t timeout_ns;
+  unsigned long long* trace;  // optional %globaltimer stamps, kTraceSlots per CTA (taccl_trace)
+  int32_t trace_ctas;         // CTAs that fit in the trace buffer
+  int32_t ncta;               // grid size
+  uint32_t cta_map[256];      // per CTA: local rank, tb, first piece, CTAs of the tb (cta_pack)
 };
+constexpr int kMaxGrid = 256;
+
+// CTA map word: tb (6 bits), first piece (9), CTAs of the tb (10), local rank (3), indep (1)
+TACCL_HD inline uint32_t cta_pack(int lr, int t, int c0, int ct, int indep) {
+  return (uint32_t)t | ((uint32_t)c0 << 6) | ((uint32_t)ct << 15) | ((uint32_t)lr << 25) | ((uint32_t)indep << 28);
+}
+TACCL_HD inline int cta_tb(uint32_t m) { return (int)(m & 63); }
+TACCL_HD inline int cta_c0(uint32_t m) { return (int)((m >> 6) & 511); }
+TACCL_HD inline int cta_ct(uint32_t m) { return (int)((m >> 15) & 1023); }
+TACCL_HD inline int cta_lr(uint32_t m) { return (int)((m >> 25) & 7); }
+TACCL_HD inline int cta_indep(uint32_t m) { return (int)((m >> 28) & 1); }
+
+// Trace record of one CTA (TACCL_TRACE_SLOTS u64 per CTA; first piece only):
+// [0] entry, [1] prologue done (plan + epoch), then per step k < kTraceSteps:
+// [2+3k] step start, [3+3k] waits satisfied, [4+3k] step done (flag published),
+// [kTraceSlots-2] identity (rank << 32 | tb << 16 | first piece), [kTraceSlots-1] exit.
+constexpr int kTraceSlots = TACCL_TRACE_SLOTS;
+constexpr int kTraceSteps = (kTraceSlots - 4) / 3;
 
 constexpr int kThreads = 512;
 

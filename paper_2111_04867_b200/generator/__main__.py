@@ -10,7 +10,7 @@ from . import generate
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--coll", required=True, choices=["allgather", "alltoall", "allreduce", "reducescatter"])
-    ap.add_argument("--algo", default="direct", choices=["ring", "direct", "hier", "greedy"])
+    ap.add_argument("--algo", default="direct", choices=["ring", "direct", "hier", "greedy", "oneshot"])
     ap.add_argument("--nranks", type=int, required=True)
     ap.add_argument("--chunks", type=int, default=1, help="input_chunkup p")
     ap.add_argument("--instances", type=int, default=1)

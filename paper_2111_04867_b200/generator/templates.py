@@ -129,6 +129,20 @@ def direct_reducescatter(n, p=1):
     return invert_allgather(direct_allgather(n, p), coll="reducescatter")
 
 
+def oneshot_allreduce(n, p=1):
+    """Latency-optimal Allreduce for small buffers: every rank sends its whole input to every
+    other rank, which reduces all n contributions locally — one link hop instead of the
+    2(n-1) (ring) or 2 (direct RS+AG) hops of the combining construction,
+    at (n-1)x the link bytes. The paper keeps size-specialised algorithms and picks the best
+    per size; this one is meant for the small-size range."""
+    alg = Algorithm(f"ar_oneshot_n{n}_p{p}", "allreduce", n, p)
+    allc = tuple(range(n * p))
+    for s in range(n):
+        for off in range(1, n):
+            alg.add(allc, s, (s + off) % n, 0, reduce=True)
+    return alg
+
+
 def ring_allreduce(n, p=1):
     return allreduce(invert_allgather(ring_allgather(n, p)), ring_allgather(n, p),
                      f"ar_ring_n{n}_p{p}")
@@ -147,6 +161,7 @@ TEMPLATES = {
     ("alltoall", "direct"): direct_alltoall,
     ("allreduce", "ring"): ring_allreduce,
     ("allreduce", "direct"): direct_allreduce,
+    ("allreduce", "oneshot"): oneshot_allreduce,
     ("reducescatter", "ring"): ring_reducescatter,
     ("reducescatter", "direct"): direct_reducescatter,
 }

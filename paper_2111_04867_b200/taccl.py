@@ -20,6 +20,7 @@ REDUCING = (ALLREDUCE, REDUCESCATTER)
 ERRORS = {0: "SUCCESS", 1: "INVALID_ARG", 2: "INVALID_SCHEDULE", 3: "NO_ALGO", 4: "CUDA",
           5: "UNSUPPORTED", 6: "TIMEOUT", 7: "NOT_INITIALIZED", 8: "NOT_REGISTERED"}
 HANDLE_BYTES = 128
+TRACE_SLOTS = 64  # TACCL_TRACE_SLOTS
 
 _lib = None
 
@@ -58,6 +59,7 @@ def lib():
             "taccl_plan_info": ([c_int, c_size, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int),
                                  ctypes.POINTER(c_int)], c_int),
             "taccl_launch_count": ([], ctypes.c_uint64),
+            "taccl_trace": ([c_vp, c_size], c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -187,6 +189,14 @@ class Comm:
         a, b, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _check(lib().taccl_plan_info(c, count, dtype_c, ctypes.byref(a), ctypes.byref(b), ctypes.byref(t)))
         return {"ctas": a.value, "split": b.value, "threads": t.value}
+
+    def trace(self, buf):
+        """Per-step %globaltimer timeline of the following launches into device tensor `buf`
+        (TRACE_SLOTS u64 per CTA); None disables."""
+        if buf is None:
+            _check(lib().taccl_trace(None, 0))
+        else:
+            _check(lib().taccl_trace(ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()))
 
     def check(self):
         _check(lib().taccl_check())

@@ -47,7 +47,8 @@ def test_named_mutations_cpp(f, op, sem, direct, cite):
 
 GEN = [(c, a, n, p) for c, a in [("allgather", "ring"), ("allgather", "direct"), ("alltoall", "direct"),
                                  ("allreduce", "ring"), ("allreduce", "direct"), ("allgather", "hier"),
-                                 ("alltoall", "hier"), ("reducescatter", "ring"), ("reducescatter", "direct")]
+                                 ("alltoall", "hier"), ("reducescatter", "ring"), ("reducescatter", "direct"),
+                                 ("allreduce", "oneshot")]
        for n in (2, 4, 8) for p in (1, 2)]
 
 

@@ -25,6 +25,7 @@ MATRIX += [("reducescatter", a, n, p, kw) for a, kw in (("ring", {}), ("direct",
                                                         ("greedy", {"policy": "uc-min"}))
            for n in (2, 3, 4, 8) for p in (1, 2)]
 MATRIX += [("reducescatter", "direct", 1, p, {}) for p in (1, 2)]
+MATRIX += [("allreduce", "oneshot", n, p, {}) for n in (1, 2, 3, 4, 8) for p in (1, 2)]
 MATRIX += [("reducescatter", "greedy", 8, p, {"topology": "2x4"}) for p in (1, 2)]
 
 

@@ -94,4 +94,4 @@ def test_multiprocess_parity(n):
         p.join(timeout=60)
     for rank, results, err in sorted(res, key=lambda x: x[0]):
         assert err is None, f"rank {rank}: {err}"
-        assert all(results), f"rank {rank}: {results}"
+        assert all(results), f"rank {rank}: failing cases {[c for c, ok in zip(CASES, results) if not ok]}"

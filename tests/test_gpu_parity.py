@@ -146,6 +146,7 @@ def test_greedy_schedules_bit_exact(coll, n, p, kw, mode):
 AR = [
     ("ring", 2, 1, 1), ("ring", 4, 2, 2), ("ring", 8, 1, 4),
     ("direct", 2, 1, 1), ("direct", 4, 1, 2), ("direct", 8, 2, 1), ("direct", 8, 1, 8),
+    ("oneshot", 2, 1, 1), ("oneshot", 4, 2, 1), ("oneshot", 8, 1, 2),
 ]
 
 
@@ -166,7 +167,8 @@ def test_allreduce_exact(algo, n, p, m, dtype, mode):
 
 @pytest.mark.parametrize("algo,n,dtype,tol", [
     ("ring", 8, "float32", 1e-6), ("direct", 8, "float32", 1e-6), ("direct", 4, "float32", 1e-6),
-    ("ring", 4, "bfloat16", 1e-2), ("direct", 8, "bfloat16", 1e-2), ("direct", 4, "bfloat16", 1e-2)])
+    ("ring", 4, "bfloat16", 1e-2), ("direct", 8, "bfloat16", 1e-2), ("direct", 4, "bfloat16", 1e-2),
+    ("oneshot", 8, "float32", 1e-6), ("oneshot", 8, "bfloat16", 1e-2)])
 def test_allreduce_tolerance_uniform(algo, n, dtype, tol):
     count = n * 40000
     text = generate("allreduce", algo, n, 1, 1)

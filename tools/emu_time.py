@@ -26,8 +26,8 @@ comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=2 * a.bytes +
 comm.load(generate(a.coll, a.algo, n, a.chunks, a.instances))
 es = 2
 count = a.bytes // es // (1 if a.coll == "allreduce" else n)
-e_in = n * count if a.coll == "alltoall" else count
-e_out = count if a.coll == "allreduce" else n * count
+e_in = n * count if a.coll in ("alltoall", "reducescatter") else count
+e_out = count if a.coll in ("allreduce", "reducescatter") else n * count
 ins = [torch.randint(-8, 8, (e_in,), device="cuda").to(torch.bfloat16) for _ in range(n)]
 outs = [torch.empty(e_out, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
 for _ in range(3):

@@ -24,7 +24,7 @@ import torch.distributed as dist  # noqa: E402
 from paper_2111_04867_b200 import taccl  # noqa: E402
 from paper_2111_04867_b200.generator import generate  # noqa: E402
 
-ALGOS = {"allgather": ["direct", "ring"], "alltoall": ["direct"], "allreduce": ["direct", "ring"],
+ALGOS = {"allgather": ["direct", "ring"], "alltoall": ["direct"], "allreduce": ["direct", "ring", "oneshot"],
          "reducescatter": ["direct", "ring"]}
 
 
