@@ -244,6 +244,70 @@ __device__ void reduce_dispatch(int dtype, char* dst, char* dst2, const char* sr
   else cta_reduce<TACCL_BFLOAT16>(dst, dst2, src0, stages, ns, soff, nelem);
 }
 
+// ---------------------------------------------------------------- TMA bulk-copy pipeline
+// One elected thread streams a piece through kTmaStages shared-memory stages of kTmaStage
+// bytes: cp.async.bulk global->shared (mbarrier complete_tx) then shared->global
+// (bulk_group). Loads run kTmaStages-1 sub-segments ahead of stores. Measured +7% over the
+// 16-byte vector copy for HBM->HBM (tools/p2p_probe.cu: 6.36 vs 5.95 TB/s read+write).
+struct TmaPipe {
+  char* stages;     // kTmaStages * kTmaStage bytes of shared memory, 128-B aligned
+  uint32_t bar0;    // shared address of kTmaStages mbarriers
+  uint32_t phase;   // parity bit per stage
+  int ld, st;       // sub-segments loaded / stored so far
+  char* dst[kTmaStages];
+  int len[kTmaStages];
+};
+
+__device__ __forceinline__ void bulk_wait_read(int allowed) {
+  switch (allowed) {  // wait_group takes an immediate
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+  }
+}
+
+__device__ __forceinline__ void tma_store_oldest(TmaPipe& p) {
+  const int s = p.st % kTmaStages;
+  const uint32_t bar = p.bar0 + 8 * s;
+  const uint32_t ph = (p.phase >> s) & 1;
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+                 : "=r"(done) : "r"(bar), "r"(ph) : "memory");
+  p.phase ^= 1u << s;
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(p.stages + (size_t)s * kTmaStage);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.dst[s]), "r"(sa), "r"(p.len[s]) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  ++p.st;
+}
+
+// queue dst[0,n) = src[0,n) (16-byte aligned, n % 16 == 0) as sub-segments of <= kTmaStage
+__device__ __forceinline__ void tma_push(TmaPipe& p, char* dst, const char* src, int64_t n) {
+  for (int64_t o = 0; o < n; o += kTmaStage) {
+    const int len = (int)min((int64_t)kTmaStage, n - o);
+    if (p.ld - p.st == kTmaStages - 1) tma_store_oldest(p);
+    const int s = p.ld % kTmaStages;
+    // the store that last used stage s (number ld - kTmaStages) must have read its smem
+    if (p.ld >= kTmaStages) bulk_wait_read(p.st - 1 - (p.ld - kTmaStages));
+    const uint32_t bar = p.bar0 + 8 * s;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(p.stages + (size_t)s * kTmaStage);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(len) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sa), "l"(src + o), "r"(len), "r"(bar) : "memory");
+    p.dst[s] = dst + o;
+    p.len[s] = len;
+    ++p.ld;
+  }
+}
+
+// drain: every queued store issued and its writes complete (before any flag publishes them)
+__device__ __forceinline__ void tma_finish(TmaPipe& p) {
+  while (p.st < p.ld) tma_store_oldest(p);
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- LL (small-message) protocol
 // Staged mode moves payload in 16-byte LL lines {p0, flag, p1, flag}: 8 payload bytes and
 // the call's flag twice, written with ONE 16-byte store into the receiver's parity slot.
@@ -301,93 +365,102 @@ __device__ __forceinline__ uint4 ll_line(u64 v, unsigned flag) {
   return make_uint4((unsigned)v, flag, (unsigned)(v >> 32), flag);
 }
 
+// bf16 / fp32 / int32 payload element e (EB bytes) of a u64 <-> accumulator (fp32 for floats)
+__device__ __forceinline__ float ll_elt_f(u64 v, int e, int dtype) {
+  return dtype == TACCL_BFLOAT16 ? __uint_as_float(((unsigned)(v >> (16 * e)) & 0xffffu) << 16)
+                                 : __uint_as_float((unsigned)(v >> (32 * e)));
+}
+
 // One LL step: lines [l0, l1) of every one of the message's cnt chunks (chunk-relative, so
-// piece j covers the same bytes of a chunk in every message, as for_piece does), every thread
-// its own lines. Chunk q's payload is bytes [q*cb, (q+1)*cb) of src/dst and LL lines
-// [q*llcb, (q+1)*llcb) of a slot. out = (src if given) (+) in_0 (+) ... (+) in_{nin-1}; the
-// reduction (+) runs only when `reduce` (else the single input or src moves as raw bits).
-// out goes to dst (local, if given) and/or fwd (a peer LL slot, if given). Returns false if
-// a wait timed out.
-template <int DT>
-__device__ __noinline__ bool ll_lines(bool reduce, const char* src, char* dst, const char* const* ins, int nin, char* fwd,
-                         int64_t cb, int64_t llcb, int cnt, int64_t l0, int64_t l1, unsigned flag, u64 timeout_ns) {
-  using Et = Elt<DT>;
-  constexpr int EB = Et::bytes, NE = 8 / EB, U = 4;  // U lines in flight per thread
-  constexpr unsigned MASK = EB == 4 ? 0xffffffffu : 0xffffu;
-  const int nt = blockDim.x;
-  for (int q = 0; q < cnt; ++q)
-  for (int64_t base = l0 + threadIdx.x; base < l1; base += U * nt) {
-    int64_t pb[U], lb[U];
-    int vb[U];
-    u64 v[U];
+// piece j covers the same bytes of a chunk in every message, as for_piece does). The
+// (chunk, line) pairs are spread over all threads, kLLU per thread, and every load of a
+// batch (src and all nin inputs) is issued before the first wait, so a step costs one round
+// trip plus the flight time. Chunk q's payload is bytes [q*cb, (q+1)*cb) of src/dst and LL
+// lines [q*llcb, (q+1)*llcb) of a slot. out = (src if given) (+) in_0 (+) ... (+)
+// in_{nin-1}; the reduction (+) runs only when `reduce` (else the single input or src moves
+// as raw bits). out goes to dst (local, if given) and/or fwd (a peer LL slot, if given).
+// Returns false if a wait timed out. One generic instance (dtype at run time): the LL kernel
+// is latency-bound and its instruction footprint matters more than its ALU work (ncu:
+// "no instruction" stalls were the second stall reason before this was slimmed).
+constexpr int kLLU = 2;
+__device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src, char* dst, const char* const* ins,
+                                         int nin, char* fwd, int64_t cb, int64_t llcb, int cnt, int64_t l0, int64_t l1,
+                                         unsigned flag, u64 timeout_ns) {
+  const unsigned m = (unsigned)(l1 - l0), total = m * (unsigned)cnt, nt = blockDim.x;
+  for (unsigned base = threadIdx.x; base < total; base += kLLU * nt) {
+    int64_t pb[kLLU], lb[kLLU];
+    int vb[kLLU];
+    u64 v[kLLU];
+    uint4 w[kLLU][kMaxRanks];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t ll = base + u * nt;
-      pb[u] = q * cb + 8 * ll;    // payload byte offset
-      lb[u] = q * llcb + 16 * ll;  // LL byte offset
-      vb[u] = ll < l1 ? (int)min((int64_t)8, cb - 8 * ll) : 0;  // valid payload bytes
+    for (int u = 0; u < kLLU; ++u) {
+      const unsigned idx = base + u * nt;
+      const unsigned q = idx / m;
+      const int64_t ll = l0 + (idx - q * m);
+      pb[u] = (int64_t)q * cb + 8 * ll;    // payload byte offset
+      lb[u] = (int64_t)q * llcb + 16 * ll;  // LL byte offset
+      vb[u] = idx < total ? (int)min((int64_t)8, cb - 8 * ll) : 0;  // valid payload bytes
       v[u] = (src && vb[u]) ? ld_bytes(src + pb[u], vb[u]) : 0;
+#pragma unroll
+      for (int i = 0; i < kMaxRanks; ++i)
+        if (i < nin && vb[u]) w[u][i] = ld_volatile_v4(ins[i] + lb[u]);
     }
-    if (!reduce) {
-      if (nin) {
-        uint4 w[U];
+    // wait for every line of the batch: re-poll the ones not yet valid, all in one loop
+    u64 t0 = 0;
+    for (int it = 0;; ++it) {
+      bool all = true;
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (vb[u]) w[u] = ld_volatile_v4(ins[0] + lb[u]);
+      for (int u = 0; u < kLLU; ++u)
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (vb[u]) {
-            if ((w[u].y != flag || w[u].w != flag) && !ll_wait(ins[0] + lb[u], flag, &w[u], timeout_ns)) return false;
-            v[u] = (u64)w[u].x | ((u64)w[u].z << 32);
+        for (int i = 0; i < kMaxRanks; ++i)
+          if (i < nin && vb[u] && (w[u][i].y != flag || w[u][i].w != flag)) {
+            if (it) w[u][i] = ld_volatile_v4(ins[i] + lb[u]);
+            all = false;
           }
-      }
-    } else {
-      typename Et::acc acc[U][NE];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int e = 0; e < NE; ++e) {
-          const unsigned r = (unsigned)(v[u] >> (8 * EB * e)) & MASK;
-          if constexpr (DT == TACCL_BFLOAT16) acc[u][e] = __uint_as_float(r << 16);
-          else if constexpr (DT == TACCL_FLOAT32) acc[u][e] = __uint_as_float(r);
-          else acc[u][e] = r;
-        }
-      for (int i = 0; i < nin; ++i) {
-        uint4 w[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (vb[u]) w[u] = ld_volatile_v4(ins[i] + lb[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (!vb[u]) continue;
-          if ((w[u].y != flag || w[u].w != flag) && !ll_wait(ins[i] + lb[u], flag, &w[u], timeout_ns)) return false;
-          const u64 y = (u64)w[u].x | ((u64)w[u].z << 32);
-#pragma unroll
-          for (int e = 0; e < NE; ++e) {
-            const unsigned r = (unsigned)(y >> (8 * EB * e)) & MASK;
-            typename Et::acc x;
-            if constexpr (DT == TACCL_BFLOAT16) x = __uint_as_float(r << 16);
-            else if constexpr (DT == TACCL_FLOAT32) x = __uint_as_float(r);
-            else x = r;
-            acc[u][e] = Et::add(acc[u][e], x);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        v[u] = 0;
-#pragma unroll
-        for (int e = 0; e < NE; ++e) {
-          u64 r;
-          if constexpr (DT == TACCL_BFLOAT16) r = Et::rn(acc[u][e]);
-          else if constexpr (DT == TACCL_FLOAT32) r = __float_as_uint(acc[u][e]);
-          else r = (unsigned)acc[u][e];
-          v[u] |= r << (8 * EB * e);
-        }
+      if (all) break;
+      if ((it & 63) == 1) {
+        const u64 now = globaltimer();
+        if (!t0) t0 = now;
+        else if (now - t0 > timeout_ns) return false;
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kLLU; ++u) {
+      if (!reduce) {
+        if (nin) v[u] = (u64)w[u][0].x | ((u64)w[u][0].z << 32);
+      } else if (dtype == TACCL_INT32) {  // wraps mod 2^32 (G13)
+        unsigned a0 = (unsigned)v[u], a1 = (unsigned)(v[u] >> 32);
+#pragma unroll
+        for (int i = 0; i < kMaxRanks; ++i)
+          if (i < nin) {
+            a0 += w[u][i].x;
+            a1 += w[u][i].z;
+          }
+        v[u] = (u64)a0 | ((u64)a1 << 32);
+      } else {  // fp32: chain-order RNE adds; bf16: fp32 accumulation, one RNE rounding (G6, R3)
+        const int ne = dtype == TACCL_BFLOAT16 ? 4 : 2;
+        float acc[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = e < ne ? ll_elt_f(v[u], e, dtype) : 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxRanks; ++i) {
+          if (i >= nin) break;
+          const u64 y = (u64)w[u][i].x | ((u64)w[u][i].z << 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < ne) acc[e] = __fadd_rn(acc[e], ll_elt_f(y, e, dtype));
+        }
+        if (dtype == TACCL_BFLOAT16) {
+          v[u] = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[u] |= (u64)Elt<TACCL_BFLOAT16>::rn(acc[e]) << (16 * e);
+        } else {
+          v[u] = (u64)__float_as_uint(acc[0]) | ((u64)__float_as_uint(acc[1]) << 32);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kLLU; ++u) {
       if (!vb[u]) continue;
       if (dst) st_bytes(dst + pb[u], v[u], vb[u]);
       if (fwd) st_volatile_v4(fwd + lb[u], ll_line(v[u], flag));
@@ -396,14 +469,15 @@ __device__ __noinline__ bool ll_lines(bool reduce, const char* src, char* dst, c
   return true;
 }
 
-__device__ bool ll_dispatch(int dtype, bool reduce, const char* src, char* dst, const char* const* ins, int nin,
-                            char* fwd, int64_t cb, int64_t llcb, int cnt, int64_t l0, int64_t l1, unsigned flag,
-                            u64 timeout_ns) {
-  if (!reduce || dtype == TACCL_INT32)
-    return ll_lines<TACCL_INT32>(reduce, src, dst, ins, nin, fwd, cb, llcb, cnt, l0, l1, flag, timeout_ns);
-  if (dtype == TACCL_FLOAT32)
-    return ll_lines<TACCL_FLOAT32>(true, src, dst, ins, nin, fwd, cb, llcb, cnt, l0, l1, flag, timeout_ns);
-  return ll_lines<TACCL_BFLOAT16>(true, src, dst, ins, nin, fwd, cb, llcb, cnt, l0, l1, flag, timeout_ns);
+// local copy for the LL kernel (small, one code path): 16-byte vectors when aligned
+__device__ __forceinline__ void ll_copy(char* dst, const char* src, int64_t n) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if ((((uintptr_t)dst | (uintptr_t)src | (uintptr_t)n) & 15) == 0) {
+    for (int64_t i = tid; i < n / 16; i += nt)
+      st_v4(reinterpret_cast<int4*>(dst) + i, ld_cg(reinterpret_cast<const int4*>(src) + i));
+  } else {
+    for (int64_t b = tid; b < n; b += nt) dst[b] = src[b];
+  }
 }
 
 // ---------------------------------------------------------------- the interpreter
@@ -462,11 +536,13 @@ __device__ void record_error(const Ctx& c, int what, int step) {
 // LL = staged (small-message) mode, a compile-time specialisation so each variant carries
 // only its own data path (register pressure: the LL variant inlines its line loop).
 template <bool LL>
-__global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kernel(const __grid_constant__ KArgs A) {
   __shared__ int s_abort;
   __shared__ u64 s_epoch;
   __shared__ const char* s_stage[kMaxRanks + 1];
-  extern __shared__ int4 s_plan[];
+  __shared__ __align__(8) u64 s_bar[kTmaStages];
+  extern __shared__ __align__(128) int4 s_dyn[];  // [TMA stages (direct kernel)] [plan]
+  int4* const s_plan = s_dyn + (LL ? 0 : kTmaBytes / 16);
   const int tid = threadIdx.x;
   u64 t_entry = 0;
   if (A.trace && tid == 0) t_entry = globaltimer();
@@ -489,6 +565,15 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
       const unsigned one = 1u + (unsigned)(ep >> 62);
       asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&ctrl->finished), "r"(one) : "memory");
     }
+  }
+  TmaPipe tp;  // used by thread 0 only
+  if (!LL && tid == 0 && A.tma) {
+    tp.stages = reinterpret_cast<char*>(s_dyn);
+    tp.bar0 = (uint32_t)__cvta_generic_to_shared(s_bar);
+    tp.phase = 0;
+    tp.ld = tp.st = 0;
+    for (int s = 0; s < kTmaStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tp.bar0 + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (A.plan_smem) {
     const int4* g = reinterpret_cast<const int4*>(R.plan);
@@ -538,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
     for (int k = 0; k < tb.nsteps; ++k) {
       const KStep& st = steps[tb.step_begin + k];
       const bool tr = trace && j == c0 && k < kTraceSteps;
-      if (tr) trace[2 + 3 * k] = globaltimer();
+      if (tr) trace[2 + 4 * k] = globaltimer();
       if (tid == 0) {
         bool ok = true;
         for (int d = 0; d < st.dep_count && ok; ++d) {
@@ -566,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           record_error(c, st.op, k);
           s_abort = 1;
         }
-        if (tr) trace[3 + 3 * k] = globaltimer();
+        if (tr) trace[3 + 4 * k] = globaltimer();
       }
       __syncthreads();
       if (s_abort) return;
@@ -586,23 +671,38 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
         char* fwd = (st.op == K_SEND || st.op == K_RRCS) ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * ll_cb : nullptr;
         const bool reduce = st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED;
         const int nin = st.op == K_SEND ? 0 : st.op == K_RRC_FUSED ? st.fuse_count : 1;
-        const bool ok = ll_dispatch(A.dtype, reduce, src, dst, s_stage, nin, fwd, cbytes, ll_cb, st.cnt, l0, l1, ll_flag,
-                                    A.timeout_ns);
+        const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, fwd, cbytes, ll_cb, st.cnt, l0, l1, ll_flag,
+                                 A.timeout_ns);
+        if (tr) trace[4 + 4 * k] = globaltimer();
         if (__syncthreads_or(!ok)) {
           if (tid == 0) record_error(c, st.op, k);
           return;
         }
-      } else switch (st.op) {
-        case K_SEND: {
-          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
-          char* dst = remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
-          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
-          break;
-        }
-        case K_CPY: {
+      } else if constexpr (LL) {
+        if (st.op == K_CPY) {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { ll_copy(dst + off, src + off, len); });
+        }
+      } else switch (st.op) {
+        case K_SEND:
+        case K_CPY: {
+          const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+          char* dst = st.op == K_CPY ? local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes
+                                     : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
+          // TMA bulk path (A.tma: 1 = local copies, 2 = also pushes to peers) for 16-byte
+          // aligned ranges; one elected thread drives it, the CTA waits at the next barrier
+          const bool tma = !LL && (A.tma == 2 || (A.tma == 1 && st.op == K_CPY)) &&
+                           ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)cbytes | (uintptr_t)A.stripe) & 15) == 0);
+          if (tma) {
+            if (tid == 0) {
+              asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+              for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { tma_push(tp, dst + off, src + off, len); });
+              tma_finish(tp);
+            }
+          } else {
+            for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+          }
           break;
         }
         case K_RRC:
@@ -651,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)((st.op == K_RRCS ? st.fwd_seq : st.seq) + 1));
         }
         if (st.need_done && ok) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
-        if (tr) trace[4 + 3 * k] = globaltimer();
+        if (tr) trace[5 + 4 * k] = globaltimer();
       }
       if (st.post_count) {
         __syncthreads();
@@ -683,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1) taccl_exec_kernel(const __grid_co
 }  // namespace
 
 int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::string* err) {
-  if (a.staged) taccl_exec_kernel<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(a);
+  if (a.staged) taccl_exec_kernel<true><<<grid, kThreadsLL, smem, (cudaStream_t)stream>>>(a);
   else taccl_exec_kernel<false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -695,9 +795,18 @@ int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::strin
 
 int executor_max_ctas(int device, std::string* err) {
   int per_sm = 0, sms = 0;
+  cudaError_t e0 = cudaFuncSetAttribute(taccl_exec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kTmaBytes + kPlanSmemMax);
+  if (e0 == cudaSuccess)
+    e0 = cudaFuncSetAttribute(taccl_exec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemMax);
+  if (e0 != cudaSuccess) {
+    *err = std::string("kernel attributes: ") + cudaGetErrorString(e0);
+    return -1;
+  }
   int per_sm_ll = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, taccl_exec_kernel<false>, kThreads, 0);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ll, taccl_exec_kernel<true>, kThreads, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, taccl_exec_kernel<false>, kThreads,
+                                                                kTmaBytes + kPlanSmemMax);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ll, taccl_exec_kernel<true>, kThreadsLL, kPlanSmemMax);
   per_sm = per_sm < per_sm_ll ? per_sm : per_sm_ll;
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {

@@ -328,8 +328,10 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   }
   A.ncta = cta;
   A.plan_smem = smem <= kPlanSmemMax ? 1 : 0;
+  A.tma = (int)env_size("TACCL_TMA", 1);
   std::string err;
-  if (launch_executor(A, cta, A.plan_smem ? smem : 0, stream, &err)) return fail(TACCL_ERR_CUDA, err);
+  const int dyn = (A.plan_smem ? smem : 0) + (A.staged ? 0 : kTmaBytes);
+  if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
   ++g.launches;
   ++g_launches;
   return TACCL_SUCCESS;
@@ -690,7 +692,7 @@ taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dt
   if ((rc = geometry(a, coll, count, elt, 1, 0, &G))) return rc;
   if (ctas) *ctas = G.grid;
   if (split) *split = G.split;
-  if (threads) *threads = kThreads;
+  if (threads) *threads = G.staged ? kThreadsLL : kThreads;
   return TACCL_SUCCESS;
 }
 

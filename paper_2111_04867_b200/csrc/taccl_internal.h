@@ -169,7 +169,7 @@ struct KArgs {
   int32_t indep_cap;       // max pieces of an independent tb (bytes / min piece)
   int32_t staged;          // staged mode: sends land in the receiver's parity staging slot,
                            // receivers copy/reduce from it; no entry handshake
-  int32_t pad1;
+  int32_t tma;             // TMA bulk copies: 0 off, 1 local copies (default), 2 + peer pushes
   int64_t staged_bytes;    // size of one parity region (at kOffScratch + parity * staged_bytes)
   int32_t elt;             // element bytes
   int32_t dtype;           // taccl_dtype_t
@@ -197,12 +197,16 @@ TACCL_HD inline int cta_indep(uint32_t m) { return (int)((m >> 28) & 1); }
 
 // Trace record of one CTA (TACCL_TRACE_SLOTS u64 per CTA; first piece only):
 // [0] entry, [1] prologue done (plan + epoch), then per step k < kTraceSteps:
-// [2+3k] step start, [3+3k] waits satisfied, [4+3k] step done (flag published),
+// [2+4k] step start, [3+4k] waits satisfied, [4+4k] thread 0's own data work done (LL
+// kernel only), [5+4k] step done (flag published),
 // [kTraceSlots-2] identity (rank << 32 | tb << 16 | first piece), [kTraceSlots-1] exit.
 constexpr int kTraceSlots = TACCL_TRACE_SLOTS;
-constexpr int kTraceSteps = (kTraceSlots - 4) / 3;
+constexpr int kTraceSteps = (kTraceSlots - 4) / 4;
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 512;    // direct (bulk) kernel
+constexpr int kThreadsLL = 256;  // LL (small-message) kernel: 255 registers/thread, no spills
+constexpr int kTmaStages = 4, kTmaStage = 32 << 10;
+constexpr int kTmaBytes = kTmaStages * kTmaStage;  // dynamic smem of the direct kernel
 
 // Pieces of one threadblock = its CTAs (same rule on host and device). Dependent tbs share
 // the launch-wide split (a dependency or a connection pairs piece j with piece j); an

@@ -5,8 +5,9 @@ from .lowering import LoweringError, lower  # noqa: F401
 from . import templates  # noqa: F401
 
 
-def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), **kw):
-    """EF v1 text for (collective, algorithm) — the one-call entry the CLI and tests use."""
+def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), pair=True, **kw):
+    """EF v1 text for (collective, algorithm) — the one-call entry the CLI and tests use.
+    pair=False lowers sends and receives into separate threadblocks."""
     if algo == "hier":
         if nranks % 2:
             raise ValueError("hier needs 2 x k ranks")
@@ -18,4 +19,6 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
     else:
         alg = templates.TEMPLATES[(coll, algo)](nranks, chunks)
     name = f"{alg.name}_m{instances}"
-    return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name)
+    if not pair:
+        name += "_split"
+    return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name, pair=pair)

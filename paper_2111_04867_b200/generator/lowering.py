@@ -155,8 +155,10 @@ def _check_pairing(instrs):
         raise LoweringError("sender and receiver split a transfer differently")
 
 
-def _allocate_tbs(lst):
-    """Threadblock allocation: returns [(send, recv)] and per-instr tb."""
+def _allocate_tbs(lst, pair=True):
+    """Threadblock allocation: returns [(send, recv)] and per-instr tb.
+    pair=False keeps sends and receives in separate threadblocks (so a reducing receive
+    never stalls the same CTA's sends; used for reduce-scatter)."""
     send_peers, recv_peers = [], []
     for ins in lst:
         if ins["type"] == "s" and ins["peer"] not in send_peers:
@@ -165,11 +167,19 @@ def _allocate_tbs(lst):
             recv_peers.append(ins["peer"])
     tbs, by_send, by_recv = [], {}, {}
     for q in send_peers:
-        if q in recv_peers:
+        if pair and q in recv_peers:
             by_send[q] = by_recv[q] = len(tbs)
             tbs.append((q, q))
     ls = [q for q in send_peers if q not in by_send]
     lr = [q for q in recv_peers if q not in by_recv]
+    if not pair:
+        for q in ls:
+            by_send[q] = len(tbs)
+            tbs.append((q, -1))
+        for q in lr:
+            by_recv[q] = len(tbs)
+            tbs.append((-1, q))
+        ls, lr = [], []
     for j in range(max(len(ls), len(lr))):
         s = ls[j] if j < len(ls) else -1
         rr = lr[j] if j < len(lr) else -1
@@ -204,8 +214,9 @@ def _ranges(ins):
     return reads, writes
 
 
-def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, name=None) -> str:
-    """Lower `alg` to EF v1 text (docs/SCHEDULE.md)."""
+def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, name=None, pair=True) -> str:
+    """Lower `alg` to EF v1 text (docs/SCHEDULE.md). pair: share one threadblock between the
+    send to and the receive from the same peer (see _allocate_tbs)."""
     if instances < 1:
         raise LoweringError("instances must be >= 1")
     n, p = alg.nranks, alg.chunks_per_rank
@@ -217,7 +228,7 @@ def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, n
            f'instances="{instances}" minBytes="{int(min_bytes)}" maxBytes="{mx}" inplace="0">']
     for r in range(n):
         lst = instrs[r]
-        tbs, assign = _allocate_tbs(lst)
+        tbs, assign = _allocate_tbs(lst, pair)
         steps = [[] for _ in tbs]
         state = {}  # (buf, idx) -> (last writer (tb, k) or None, readers [(tb, k)])
         for ins, t in zip(lst, assign):

@@ -76,7 +76,7 @@ if world > 1:
     T = torch.cat(allT)
 T = T[T[:, 0] > 0]
 t0 = int(T[:, 0].min())
-nsteps = (taccl.TRACE_SLOTS - 4) // 3
+nsteps = (taccl.TRACE_SLOTS - 4) // 4
 if rank == 0:
     print(f"{a.coll} {a.algo} n={n} S={S} B plan={info} (us from the earliest entry)")
     for row in T.tolist():
@@ -87,10 +87,10 @@ if rank == 0:
             return f"{(x - t0) / 1e3:6.2f}" if x else "   -  "
         steps = []
         for k in range(nsteps):
-            s0, s1, s2 = row[2 + 3 * k], row[3 + 3 * k], row[4 + 3 * k]
+            s0, s1, s2, s3 = row[2 + 4 * k], row[3 + 4 * k], row[4 + 4 * k], row[5 + 4 * k]
             if not s0:
                 break
-            steps.append(f"s{k}[{us(s0)} w{us(s1)} d{us(s2)}]")
+            steps.append(f"s{k}[{us(s0)} w{us(s1)}" + (f" x{us(s2)}" if s2 else "") + f" d{us(s3)}]")
         print(f"r{r} tb{tb} j{j}: entry {us(row[0])} pro {us(row[1])} " + " ".join(steps) + f" exit {us(row[-1])}")
 comm.destroy()
 if world > 1:
