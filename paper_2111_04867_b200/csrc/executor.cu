@@ -611,13 +611,16 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
     trace[kTraceSlots - 2] = ((u64)R.rank << 32) | ((u64)c.t << 16) | (u64)c0;
   }
 
+  // entry handshake: tell our sender we are in this call, for every piece this CTA owns, up
+  // front — this rank's previous call has fully completed (stream order), so nothing of it
+  // can still read the buffers the sender is about to store into; announcing per piece as
+  // it starts would throttle the sender to this CTA's per-piece progress.
+  if (!LL && tb.recv >= 0 && tid == 0) {
+    u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
+    for (int j = c0; j < nsplit; j += ct) st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
+  }
   for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
-    // entry handshake: tell our sender we are in this call (its stores may now land)
-    if (!LL && tb.recv >= 0 && tid == 0) {
-      u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
-      st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
-    }
     bool sender_ready = false;
 
     for (int k = 0; k < tb.nsteps; ++k) {

@@ -185,6 +185,7 @@ struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, stripe = 0;
   int split = 1, grid = 0, budget = 0, dep_ctas = 1, staged = 0, indep_cap = 1;
   int64_t scratch_off = 0, staging_off = 0, need = 0;
+  std::vector<std::vector<int>> ct;  // [rank][tb] CTAs of the threadblock (0 for non-local ranks)
 };
 
 taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt, int nlocal_ranks,
@@ -221,16 +222,33 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
     if (a->plans[r].mem) ++nlocal;
   G->indep_cap = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxSplit, (int64_t)a->max_steps_cnt * G->chunk_bytes / min_piece));
   G->budget = std::max(1, target / std::max(1, nlocal));
-  // CTAs left for the dependent tbs once independent tbs took their weight share
-  int per_dep = kMaxSplit;
+  // CTAs left for the dependent tbs once independent tbs took their weight share, shared
+  // equally among the dependent tbs (TACCL_DEP_WEIGHTED=1: by data-volume weight — measured
+  // slower for split send/reduce tbs, the reduce side needs its CTAs for HBM bandwidth);
+  // per_dep = the largest share, which sets the piece count
+  int per_dep = 1;
+  const bool weighted = env_size("TACCL_DEP_WEIGHTED", 0) != 0;
+  std::vector<std::vector<int>> share(a->nranks);
   for (int r = 0; r < a->nranks; ++r) {
     if (!a->plans[r].mem) continue;
     int used = 0, ndep = 0;
+    long long wdep = 0;
     for (int t = 0; t < a->ntb[r]; ++t) {
       if (a->indep[r][t]) used += tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, 1, G->indep_cap);
-      else ++ndep;
+      else {
+        ++ndep;
+        wdep += std::max(1, a->weights[r][t]);
+      }
     }
-    if (ndep) per_dep = std::min(per_dep, std::max(1, (G->budget - used) / ndep));
+    const int avail = std::max(ndep, G->budget - used);
+    share[r].assign(a->ntb[r], 0);
+    for (int t = 0; t < a->ntb[r]; ++t)
+      if (!a->indep[r][t]) {
+        const int sh = weighted ? (int)std::max(1LL, (long long)avail * std::max(1, a->weights[r][t]) / std::max(1LL, wdep))
+                                : std::max(1, avail / ndep);
+        share[r][t] = sh;
+        per_dep = std::max(per_dep, sh);
+      }
   }
   if (forced) {
     lanes = (int)forced;
@@ -255,10 +273,16 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   // device's capacity are run one after another by the same CTA
   G->dep_ctas = std::min(G->split, per_dep);
   G->grid = 0;
+  G->ct.assign(a->nranks, {});
   for (int r = 0; r < a->nranks; ++r)
-    if (a->plans[r].mem)
-      for (int t = 0; t < a->ntb[r]; ++t)
-        G->grid += a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, G->split, G->indep_cap) : G->dep_ctas;
+    if (a->plans[r].mem) {
+      G->ct[r].assign(a->ntb[r], 0);
+      for (int t = 0; t < a->ntb[r]; ++t) {
+        G->ct[r][t] = a->indep[r][t] ? tb_pieces(1, a->weights[r][t], a->wsum[r], G->budget, G->split, G->indep_cap)
+                                     : std::min(G->split, share[r][t]);
+        G->grid += G->ct[r][t];
+      }
+    }
   if (G->grid > g.max_ctas)
     return fail(TACCL_ERR_UNSUPPORTED, "launch needs " + std::to_string(G->grid) + " co-resident CTAs, device holds " +
                                            std::to_string(g.max_ctas));
@@ -318,7 +342,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     const int first = cta;
     for (int t = 0; t < dp.ntb; ++t) {
       const int ind = a->indep[r][t];
-      const int ct = ind ? tb_pieces(1, a->weights[r][t], a->wsum[r], G.budget, G.split, G.indep_cap) : G.dep_ctas;
+      const int ct = G.ct[r][t];
       for (int c = 0; c < ct; ++c) {
         if (cta >= kMaxGrid) return fail(TACCL_ERR_UNSUPPORTED, "launch exceeds " + std::to_string(kMaxGrid) + " CTAs");
         A.cta_map[cta++] = cta_pack((int)i, t, c, ct, ind);
