@@ -84,7 +84,9 @@ struct Comm {
   unsigned long long* trace = nullptr;  // taccl_trace buffer (caller-owned)
   int trace_ctas = 0;
   int64_t staged_bytes = 0;  // one staged-mode parity region (identical on all ranks)
-  // host-run staging (taccl_run_host): library-owned pinned bounce is the user's job
+  // host-run pipeline (taccl_run_host): copy streams and events, created on first use
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_k[2] = {}, ev_out[2] = {};
 };
 
 Comm g;
@@ -215,8 +217,9 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   // CTA measured best at n=2 up to 1 MiB, profiles/r01_small_sweep_n2.txt)
   const int64_t min_piece = G->staged ? (int64_t)env_size("TACCL_LL_MIN_PIECE", 4 << 10)
                                       : (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
-  // 128 CTAs x 512 threads measured best for the HBM copy and 2-GPU pushes (profiles/r01_scan.txt)
-  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", 128));
+  // 128 CTAs x 512 threads measured best for the HBM copy and 2-GPU pushes, 148 (one per SM)
+  // for 4 ranks (AR ring +5%, AG/A2A equal; profiles/r01_scan.txt, r01_envscan_n4.txt)
+  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", g.nranks >= 4 ? 148 : 128));
   int nlocal = 0;
   for (int r = 0; r < a->nranks; ++r)
     if (a->plans[r].mem) ++nlocal;
@@ -539,6 +542,15 @@ taccl_result_t taccl_comm_destroy(void) {
   }
   for (auto& kv : g.ipc_open) cudaIpcCloseMemHandle(kv.second);
   for (char* a : g.arenas) cudaFree(a);
+  if (g.h2d) {
+    cudaStreamDestroy(g.h2d);
+    cudaStreamDestroy(g.d2h);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(g.ev_in[i]);
+      cudaEventDestroy(g.ev_k[i]);
+      cudaEventDestroy(g.ev_out[i]);
+    }
+  }
   g = Comm();
   return TACCL_SUCCESS;
 }
@@ -687,20 +699,65 @@ taccl_result_t taccl_run_host(taccl_coll_t coll, const void* host_send, void* ho
   if (rc) return rc;
   if (g.emulated) return fail(TACCL_ERR_INVALID_ARG, "emulated communicator: not supported for host runs");
   if (!host_send || !host_recv) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
+  if (count == 0) return TACCL_SUCCESS;
   const int elt = elt_size(dtype), n = g.nranks;
-  const size_t ib = in_bytes(coll, count, elt, n), ob = out_bytes(coll, count, elt, n);
-  // library-owned device buffers: the front of this rank's (symmetric) arena scratch region
-  const int64_t in_off = 0, out_off = ((int64_t)ib + 4095) & ~(int64_t)4095;
-  const int64_t base = (out_off + (int64_t)ob + 4095) & ~(int64_t)4095;
-  if ((size_t)(kOffScratch + 2 * staged_region_bytes() + base) > g.arena_bytes)
-    return fail(TACCL_ERR_INVALID_ARG, "arena too small for host run");
+  // Pipelined over P pieces of the count axis: H2D of piece q+1, the collective on piece q
+  // and D2H of piece q-1 overlap (PCIe is full duplex). Buffers are 1 or n rows of `count`
+  // elements (rows_in / rows_out); piece q is the column range [q*cq, (q+1)*cq) of every
+  // row, moved with 2-D copies into double-buffered device temps at the front of the
+  // (symmetric) arena scratch, so every rank's temps sit at the same arena offset.
+  const int rows_in = (coll == TACCL_ALLTOALL || coll == TACCL_REDUCESCATTER) ? n : 1;
+  const int rows_out = (coll == TACCL_ALLGATHER || coll == TACCL_ALLTOALL) ? n : 1;
+  const size_t piece_min = env_size("TACCL_HOST_PIECE_BYTES", 32 << 20);  // per row-set
+  int P = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t)rows_out * count * elt / piece_min));
+  while (P > 1 && (count % P || (count / P) % (size_t)(8 * n))) --P;  // whole chunks per piece
+  const size_t cq = count / P;
+  const int64_t in_b = (int64_t)rows_in * cq * elt, out_b = (int64_t)rows_out * cq * elt;
+  auto al = [](int64_t x) { return (x + 4095) & ~(int64_t)4095; };
+  const int nb = P > 1 ? 2 : 1;
   const int64_t front = kOffScratch + 2 * staged_region_bytes();
-  char* dev_in = g.arenas[0] + front + in_off;
-  char* dev_out = g.arenas[0] + front + out_off;
+  const int64_t base = nb * (al(in_b) + al(out_b));
+  if ((size_t)(front + base) > g.arena_bytes) return fail(TACCL_ERR_INVALID_ARG, "arena too small for host run");
+  char* dev_in[2] = {g.arenas[0] + front, g.arenas[0] + front + al(in_b)};
+  char* dev_out[2] = {g.arenas[0] + front + nb * al(in_b), g.arenas[0] + front + nb * al(in_b) + al(out_b)};
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(cudaMemcpyAsync(dev_in, host_send, ib, cudaMemcpyHostToDevice, s));
-  if ((rc = run_one(coll, dev_in, dev_out, count, dtype, stream, base, true))) return rc;
-  CUDA_TRY(cudaMemcpyAsync(host_recv, dev_out, ob, cudaMemcpyDeviceToHost, s));
+  if (P == 1) {
+    CUDA_TRY(cudaMemcpyAsync(dev_in[0], host_send, (size_t)in_b, cudaMemcpyHostToDevice, s));
+    if ((rc = run_one(coll, dev_in[0], dev_out[0], count, dtype, stream, base, true))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(host_recv, dev_out[0], (size_t)out_b, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return TACCL_SUCCESS;
+  }
+  if (!g.h2d) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(cudaEventCreateWithFlags(&g.ev_in[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.ev_k[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.ev_out[i], cudaEventDisableTiming));
+    }
+  }
+  const size_t pitch = count * elt, w = cq * elt;
+  // the copy streams start after everything already enqueued on the user's stream
+  CUDA_TRY(cudaEventRecord(g.ev_k[0], s));
+  CUDA_TRY(cudaStreamWaitEvent(g.h2d, g.ev_k[0], 0));
+  CUDA_TRY(cudaStreamWaitEvent(g.d2h, g.ev_k[0], 0));
+  for (int q = 0; q < P; ++q) {
+    const int b = q & 1;
+    if (q >= 2) CUDA_TRY(cudaStreamWaitEvent(g.h2d, g.ev_k[b], 0));  // kernel q-2 done with dev_in[b]
+    CUDA_TRY(cudaMemcpy2DAsync(dev_in[b], w, (const char*)host_send + q * w, pitch, w, rows_in,
+                               cudaMemcpyHostToDevice, g.h2d));
+    CUDA_TRY(cudaEventRecord(g.ev_in[b], g.h2d));
+    CUDA_TRY(cudaStreamWaitEvent(s, g.ev_in[b], 0));
+    if (q >= 2) CUDA_TRY(cudaStreamWaitEvent(s, g.ev_out[b], 0));  // D2H q-2 done with dev_out[b]
+    if ((rc = run_one(coll, dev_in[b], dev_out[b], cq, dtype, stream, base, true))) return rc;
+    CUDA_TRY(cudaEventRecord(g.ev_k[b], s));
+    CUDA_TRY(cudaStreamWaitEvent(g.d2h, g.ev_k[b], 0));
+    CUDA_TRY(cudaMemcpy2DAsync((char*)host_recv + q * w, pitch, dev_out[b], w, w, rows_out,
+                               cudaMemcpyDeviceToHost, g.d2h));
+    CUDA_TRY(cudaEventRecord(g.ev_out[b], g.d2h));
+  }
+  CUDA_TRY(cudaStreamSynchronize(g.d2h));
   CUDA_TRY(cudaStreamSynchronize(s));
   return TACCL_SUCCESS;
 }

@@ -3,6 +3,7 @@ to EF v1 text (docs/SCHEDULE.md). Not on the timed path."""
 from .algorithm import Algorithm, Transfer  # noqa: F401
 from .lowering import LoweringError, lower  # noqa: F401
 from . import templates  # noqa: F401
+from .tuned import default_schedules  # noqa: F401
 
 
 def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), pair=True, **kw):

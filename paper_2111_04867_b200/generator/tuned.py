@@ -1,0 +1,39 @@
+"""Size-specialised default schedule sets (TACCL keeps
+several algorithms per collective and uses the best one for each buffer size).
+
+Each entry is (algorithm, [minBytes, maxBytes)) in the runtime's selection convention
+(include/taccl.h taccl_run: S = AG output bytes, A2A per-rank send bytes, AR buffer bytes,
+RS send bytes). Crossovers come from the graph-mode sweeps on B200 in profiles/
+(r01_sweep_n2_graph.jsonl, r01_sweep_n4_graph.jsonl, r01_small_sweep_n4.jsonl); n = 8 is
+unmeasured (the pool offers <= 4 GPUs) and extrapolated from n = 4.
+"""
+from __future__ import annotations
+
+import math
+
+MiB = 1 << 20
+INF = math.inf
+
+
+def ranges(coll: str, n: int):
+    """[(algo, min_bytes, max_bytes)] covering [0, inf) for `coll` at n ranks."""
+    if n == 1:
+        return [("direct", 0, INF)]
+    if coll == "allgather":
+        return [("direct", 0, INF)] if n == 2 else [("direct", 0, 128 * MiB), ("ring", 128 * MiB, INF)]
+    if coll == "alltoall":
+        return [("direct", 0, INF)]
+    if coll == "allreduce":
+        if n == 2:
+            return [("oneshot", 0, 16 * MiB), ("direct", 16 * MiB, INF)]
+        small = MiB // 2 if n <= 4 else MiB // 4
+        return [("oneshot", 0, small), ("direct", small, 64 * MiB), ("ring", 64 * MiB, INF)]
+    if coll == "reducescatter":
+        return [("direct", 0, INF)] if n == 2 else [("direct", 0, 32 * MiB), ("ring", 32 * MiB, INF)]
+    raise ValueError(coll)
+
+
+def default_schedules(coll: str, n: int):
+    """EF texts of the default set for (coll, n), each carrying its size range."""
+    from . import generate
+    return [generate(coll, algo, n, 1, 1, min_bytes=lo, max_bytes=hi) for algo, lo, hi in ranges(coll, n)]

@@ -141,6 +141,12 @@ class Comm:
         _check(lib().taccl_load_algo(b, len(b), ctypes.byref(h)))
         return h
 
+    def load_defaults(self, colls=("allgather", "alltoall", "allreduce", "reducescatter")):
+        """Load the size-specialised default schedule set of every collective in `colls`
+        (generator/tuned.py); returns the algorithm handles."""
+        from .generator.tuned import default_schedules
+        return [self.load(t) for c in colls for t in default_schedules(c, self.nranks)]
+
     def free(self, h):
         _check(lib().taccl_free(h))
 

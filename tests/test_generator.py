@@ -191,3 +191,17 @@ def test_instances_double_threadblocks_and_halve_chunks():
     ins = [np.arange(8, dtype=np.int32) + 100 * r for r in range(4)]
     a, b = oracle.run(prog, ins, "int32"), oracle.run(exp, ins, "int32")
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+@pytest.mark.parametrize("coll", ["allgather", "alltoall", "allreduce", "reducescatter"])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+def test_default_sets_cover_all_sizes_once(coll, n):
+    # size-specialised sets: contiguous, disjoint, [0, inf)
+    from paper_2111_04867_b200.generator.tuned import default_schedules, ranges
+    rs = ranges(coll, n)
+    assert rs[0][1] == 0 and rs[-1][2] == math.inf
+    for (_, _, hi), (_, lo, _) in zip(rs, rs[1:]):
+        assert hi == lo
+    for text in default_schedules(coll, n):
+        v = oracle.validate(text)
+        assert v.ok, f"{v.kind}: {v.msg}"

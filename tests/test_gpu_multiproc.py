@@ -55,7 +55,16 @@ def _worker(rank, n, port, cases, q):
             comm.check()
             got = out.cpu().view({"int32": torch.int32, "float32": torch.int32, "bfloat16": torch.int16}[dtype]).numpy()
             want = oracle.run(oracle.parse(text), ins, dtype)[rank]
-            results.append(bool(np.array_equal(got.view(want.dtype), want)))
+            ok = bool(np.array_equal(got.view(want.dtype), want))
+            # the same call through host buffers, pipelined in several pieces (e2e path)
+            os.environ["TACCL_HOST_PIECE_BYTES"] = str(1 << 14)
+            h_in = torch.from_numpy(ins[rank].view(view[dtype])).view(tdt[dtype]).pin_memory()
+            h_out = torch.empty(e_out, dtype=tdt[dtype]).pin_memory()
+            comm.run_host(coll, h_out, h_in)
+            os.environ.pop("TACCL_HOST_PIECE_BYTES")
+            vt = {"int32": torch.int32, "float32": torch.int32, "bfloat16": torch.int16}[dtype]
+            ok = ok and bool(np.array_equal(h_out.view(vt).numpy().view(want.dtype), want))
+            results.append(ok)
             comm.free(h)
         comm.destroy()
         q.put((rank, results, None))

@@ -237,6 +237,59 @@ def test_reducescatter_tolerance_uniform(algo, n, dtype, tol):
         assert rel.max() <= tol, rel.max()
 
 
+# ---------------------------------------------------------------- size-specialised sets
+
+@pytest.mark.parametrize("coll,n,counts", [
+    ("allreduce", 4, [4 * 1000, 4 * 65536, 4 * 262144]),        # oneshot below 512 KiB, direct above
+    ("allreduce", 2, [2 * 1000, 2 * (8 << 20) + 2 * 1024]),       # oneshot below 16 MiB, direct above
+    ("reducescatter", 4, [1000, 5 << 20]),                        # direct below 32 MiB, ring above
+    ("allgather", 4, [1000, 17 << 20])])                          # direct below 128 MiB, ring above
+def test_default_set_selects_by_size(coll, n, counts):
+    from paper_2111_04867_b200.generator import default_schedules
+    comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=1 << 30)
+    try:
+        for t in default_schedules(coll, n):
+            comm.load(t)
+        for count in counts:
+            e_in = n * count if coll == "reducescatter" else count
+            ins = [allreduce_input(e_in, "int32", "bits", 14, r) for r in range(n)]
+            dev_in = [to_dev(x, "int32") for x in ins]
+            e_out = {"allgather": n * count}.get(coll, count)
+            dev_out = [torch.empty(e_out, dtype=torch.int32, device="cuda") for _ in range(n)]
+            comm.run_emulated(coll, dev_out, dev_in)
+            torch.cuda.synchronize()
+            comm.check()
+            got = [to_host(o, "int32", ins[0]) for o in dev_out]
+            assert_bits_equal(got, oracle.expected_outputs(coll, ins, "int32"))
+    finally:
+        comm.destroy()
+
+
+# ---------------------------------------------------------------- host-buffer runs (e2e path)
+
+@pytest.mark.parametrize("coll,count,piece", [("allgather", 1 << 16, 1 << 12), ("allgather", 1000, 0),
+                                              ("allreduce", 3 << 16, 1 << 14), ("reducescatter", 1 << 15, 1 << 12)])
+def test_run_host_pipelined_single_rank(coll, count, piece):
+    # taccl_run_host splits the count axis into pieces (2-D copies, double-buffered temps,
+    # H2D / kernel / D2H overlapped); TACCL_HOST_PIECE_BYTES forces several pieces here
+    from paper_2111_04867_b200.generator import generate
+    os.environ["TACCL_HOST_PIECE_BYTES"] = str(piece or (1 << 30))
+    comm = taccl.Comm(rank=0, nranks=1, device=0, scratch_bytes=64 << 20)
+    try:
+        comm.load(generate(coll, "direct", 1, 1, 1))
+        x = allreduce_input(count, "int32", "bits", 15, 0)
+        h_in = torch.from_numpy(x).pin_memory()
+        h_out = torch.empty(count, dtype=torch.int32).pin_memory()
+        for _ in range(2):
+            h_out.fill_(0)
+            comm.run_host(coll, h_out, h_in)
+            assert np.array_equal(h_out.numpy(), oracle.expected_outputs(coll, [x], "int32")[0])
+        comm.check()
+    finally:
+        comm.destroy()
+        os.environ.pop("TACCL_HOST_PIECE_BYTES", None)
+
+
 # ---------------------------------------------------------------- edge cases
 
 def test_single_rank_copy_path():

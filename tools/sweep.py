@@ -24,11 +24,14 @@ import torch.distributed as dist  # noqa: E402
 from paper_2111_04867_b200 import taccl  # noqa: E402
 from paper_2111_04867_b200.generator import generate  # noqa: E402
 
-ALGOS = {"allgather": ["direct", "ring"], "alltoall": ["direct"], "allreduce": ["direct", "ring", "oneshot"],
-         "reducescatter": ["direct", "ring", "direct_split"]}
+ALGOS = {"allgather": ["direct", "ring", "auto"], "alltoall": ["direct"], "allreduce": ["direct", "ring", "oneshot", "auto"],
+         "reducescatter": ["direct", "ring", "auto"]}
 
 
 def gen(coll, al, n):
+    if al == "auto":  # the size-specialised default set (generator/tuned.py)
+        from paper_2111_04867_b200.generator.tuned import default_schedules
+        return default_schedules(coll, n)
     """algorithm name -> EF text; suffix _split = sends and receives in separate threadblocks"""
     if al.endswith("_split"):
         return generate(coll, al[:-6], n, 1, 1, pair=False)
@@ -130,10 +133,17 @@ def main():
     stream = torch.cuda.Stream() if a.graph else torch.cuda.current_stream()
     torch.cuda.set_stream(stream)
     tf = (lambda f, st, w: timeit_graph(f, st, w)) if a.graph else timeit
+
+    def load(t):  # one EF text or a list of them (a size-ranged set)
+        return [comm.load(x) for x in t] if isinstance(t, list) else [comm.load(t)]
+
+    def free(hs):
+        for h in hs:
+            comm.free(h)
     out_f = open(a.out or os.path.join(ROOT, "gpurun_out", f"sweep_n{n}.jsonl"), "a") if rank == 0 else None
     for coll in a.colls.split(","):
         algos = ALGOS[coll] if n > 1 else ["direct"]
-        handles = {al: comm.load(gen(coll, al, n)) for al in algos}
+        handles = {al: load(gen(coll, al, n)) for al in algos}
         for k in range(a.size_lo, a.size_hi + 1):
             S = 1 << k
             if coll == "allgather":
@@ -156,8 +166,8 @@ def main():
                 if al == "oneshot" and S * (n - 1) > (64 << 20):
                     continue  # (n-1) x S of staging: a small-message schedule
                 # select this algorithm: load order decides (latest wins) -> reload on top
-                comm.free(handles[al])
-                handles[al] = comm.load(gen(coll, al, n))
+                free(handles[al])
+                handles[al] = load(gen(coll, al, n))
                 ms, it = tf(lambda: comm.run(coll, out, inp, stream), stream, world)
                 rec[f"taccl_{al}_us"] = round(ms * 1e3, 3)
                 rec[f"taccl_{al}_busbw"] = round(S / (ms / 1e3) * factor(coll, n) / 1e9, 2)
@@ -193,7 +203,7 @@ def main():
                 print(json.dumps(rec), flush=True)
                 out_f.write(json.dumps(rec) + "\n")
         for h in handles.values():
-            comm.free(h)
+            free(h)
     comm.destroy()
     if world > 1:
         dist.destroy_process_group()
