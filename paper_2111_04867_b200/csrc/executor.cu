@@ -178,15 +178,16 @@ struct Elt<TACCL_BFLOAT16> {
 };
 
 template <int DT>
-__device__ __noinline__ void cta_reduce(char* dst, char* dst2, const char* src0, const char* const* stages,
-                                        int ns, int64_t soff, int64_t nelem) {
-  // dst (and dst2, the forward destination of a fused rrc+send, when non-null) =
-  // src0 + stages[0] + ... ; RU vectors per thread in flight per input
+__device__ __noinline__ void cta_reduce(char* dst, char* const* fwd, int nfwd, const char* src0,
+                                        const char* const* stages, int ns, int64_t soff, int64_t nelem) {
+  // dst (and fwd[0..nfwd) + soff, the forward destinations of a fused rrc+send or chain+sends)
+  // = src0 + stages[0] + ... ; RU vectors per thread in flight per input
   using E = Elt<DT>;
   constexpr int V = E::V, RU = 4;
   const int tid = threadIdx.x, nt = blockDim.x;
-  uintptr_t align = (uintptr_t)dst | (uintptr_t)src0 | (uintptr_t)dst2;
+  uintptr_t align = (uintptr_t)dst | (uintptr_t)src0;
   for (int s = 0; s < ns; ++s) align |= (uintptr_t)(stages[s] + soff);
+  for (int f = 0; f < nfwd; ++f) align |= (uintptr_t)(fwd[f] + soff);
   const int64_t nv = (align & 15) ? 0 : nelem / V;
   int64_t v = tid;
   for (; v + (int64_t)(RU - 1) * nt < nv; v += (int64_t)RU * nt) {
@@ -212,7 +213,7 @@ __device__ __noinline__ void cta_reduce(char* dst, char* dst2, const char* src0,
       const int4 o = E::pack(acc[u]);
       const int64_t off = (v + (int64_t)u * nt) * 16;
       st_v4(reinterpret_cast<int4*>(dst + off), o);
-      if (dst2) st_v4(reinterpret_cast<int4*>(dst2 + off), o);
+      for (int f = 0; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
     }
   }
   for (; v < nv; v += nt) {
@@ -226,22 +227,22 @@ __device__ __noinline__ void cta_reduce(char* dst, char* dst2, const char* src0,
     }
     const int4 o = E::pack(acc);
     st_v4(reinterpret_cast<int4*>(dst + off), o);
-    if (dst2) st_v4(reinterpret_cast<int4*>(dst2 + off), o);
+    for (int f = 0; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
   }
   for (int64_t e = nv * V + tid; e < nelem; e += nt) {
     const int64_t off = e * E::bytes;
     typename E::acc acc = E::load(src0 + off);
     for (int s = 0; s < ns; ++s) acc = E::add(acc, E::load(stages[s] + soff + off));
     E::store(dst + off, acc);
-    if (dst2) E::store(dst2 + off, acc);
+    for (int f = 0; f < nfwd; ++f) E::store(fwd[f] + soff + off, acc);
   }
 }
 
-__device__ void reduce_dispatch(int dtype, char* dst, char* dst2, const char* src0, const char* const* stages,
-                                int ns, int64_t soff, int64_t nelem) {
-  if (dtype == TACCL_INT32) cta_reduce<TACCL_INT32>(dst, dst2, src0, stages, ns, soff, nelem);
-  else if (dtype == TACCL_FLOAT32) cta_reduce<TACCL_FLOAT32>(dst, dst2, src0, stages, ns, soff, nelem);
-  else cta_reduce<TACCL_BFLOAT16>(dst, dst2, src0, stages, ns, soff, nelem);
+__device__ void reduce_dispatch(int dtype, char* dst, char* const* fwd, int nfwd, const char* src0,
+                                const char* const* stages, int ns, int64_t soff, int64_t nelem) {
+  if (dtype == TACCL_INT32) cta_reduce<TACCL_INT32>(dst, fwd, nfwd, src0, stages, ns, soff, nelem);
+  else if (dtype == TACCL_FLOAT32) cta_reduce<TACCL_FLOAT32>(dst, fwd, nfwd, src0, stages, ns, soff, nelem);
+  else cta_reduce<TACCL_BFLOAT16>(dst, fwd, nfwd, src0, stages, ns, soff, nelem);
 }
 
 // ---------------------------------------------------------------- TMA bulk-copy pipeline
@@ -378,13 +379,14 @@ __device__ __forceinline__ float ll_elt_f(u64 v, int e, int dtype) {
 // trip plus the flight time. Chunk q's payload is bytes [q*cb, (q+1)*cb) of src/dst and LL
 // lines [q*llcb, (q+1)*llcb) of a slot. out = (src if given) (+) in_0 (+) ... (+)
 // in_{nin-1}; the reduction (+) runs only when `reduce` (else the single input or src moves
-// as raw bits). out goes to dst (local, if given) and/or fwd (a peer LL slot, if given).
+// as raw bits). out goes to dst (local, if given) and/or fwd[0..nfwd) (peer LL slots).
 // Returns false if a wait timed out. One generic instance (dtype at run time): the LL kernel
 // is latency-bound and its instruction footprint matters more than its ALU work (ncu:
 // "no instruction" stalls were the second stall reason before this was slimmed).
 constexpr int kLLU = 2;
 __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src, char* dst, const char* const* ins,
-                                         int nin, char* fwd, int64_t cb, int64_t llcb, int cnt, int64_t l0, int64_t l1,
+                                         int nin, char* const* fwd, int nfwd, int64_t cb, int64_t llcb, int cnt,
+                                         int64_t l0, int64_t l1,
                                          unsigned flag, u64 timeout_ns) {
   const unsigned m = (unsigned)(l1 - l0), total = m * (unsigned)cnt, nt = blockDim.x;
   for (unsigned base = threadIdx.x; base < total; base += kLLU * nt) {
@@ -463,7 +465,7 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
     for (int u = 0; u < kLLU; ++u) {
       if (!vb[u]) continue;
       if (dst) st_bytes(dst + pb[u], v[u], vb[u]);
-      if (fwd) st_volatile_v4(fwd + lb[u], ll_line(v[u], flag));
+      for (int f = 0; f < nfwd; ++f) st_volatile_v4(fwd[f] + lb[u], ll_line(v[u], flag));
     }
   }
   return true;
@@ -540,6 +542,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
   __shared__ int s_abort;
   __shared__ u64 s_epoch;
   __shared__ const char* s_stage[kMaxRanks + 1];
+  __shared__ char* s_fwd[kMaxRanks];  // forward destinations of this step (RRCS / chain sends)
   __shared__ __align__(8) u64 s_bar[kTmaStages];
   extern __shared__ __align__(128) int4 s_dyn[];  // [TMA stages (direct kernel)] [plan]
   int4* const s_plan = s_dyn + (LL ? 0 : kTmaBytes / 16);
@@ -650,6 +653,18 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
         }
         if (ok && (st.op == K_RRC || st.op == K_RRCS || st.op == K_RECV))
           s_stage[0] = LL ? my_staged + (int64_t)st.soff2 * ll_cb : local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
+        if (ok && (st.op == K_SEND || st.op == K_RRCS))
+          s_fwd[0] = LL ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * ll_cb
+                        : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
+        if (ok && st.op == K_RRC_FUSED) {  // fused sends of the chain's result (fuse_chain_sends)
+          for (int f = 0; f < st.fwd_count && ok; ++f) {
+            const int* fw = fused + st.fwd_begin + 6 * f;  // peer, chan, rbuf, roff, roff2, seq
+            // entry handshake of that send's connection: its receiver is in this call
+            if (!LL) ok = wait_ge<true>(my_ready + flag_slot(fw[0], fw[1], j), c.epoch, A.timeout_ns);
+            s_fwd[f] = LL ? R.peer_arena[fw[0]] + parity_off + (int64_t)fw[4] * ll_cb
+                          : remote_base(c, fw[0], fw[2]) + (int64_t)fw[3] * cbytes;
+          }
+        }
         if (!ok) {
           record_error(c, st.op, k);
           s_abort = 1;
@@ -659,7 +674,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
       __syncthreads();
       if (s_abort) return;
 
-      if (LL && st.op != K_CPY && st.op != K_NOP && st.op != K_SENT) {
+      if (LL && (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED)) {
         // LL path: this piece's lines of every chunk (same split on both sides)
         const int64_t nl = (cbytes + 7) / 8;
         int64_t l0 = (int64_t)((unsigned)nl * (unsigned)j / (unsigned)nsplit);  // nl*split < 2^32 (LL sizes)
@@ -671,11 +686,11 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
         }
         const char* src = (st.op == K_RECV) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
         char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-        char* fwd = (st.op == K_SEND || st.op == K_RRCS) ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * ll_cb : nullptr;
+        const int nfwd = (st.op == K_SEND || st.op == K_RRCS) ? 1 : st.op == K_RRC_FUSED ? st.fwd_count : 0;
         const bool reduce = st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED;
         const int nin = st.op == K_SEND ? 0 : st.op == K_RRC_FUSED ? st.fuse_count : 1;
-        const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, fwd, cbytes, ll_cb, st.cnt, l0, l1, ll_flag,
-                                 A.timeout_ns);
+        const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt, l0, l1,
+                                 ll_flag, A.timeout_ns);
         if (tr) trace[4 + 4 * k] = globaltimer();
         if (__syncthreads_or(!ok)) {
           if (tid == 0) record_error(c, st.op, k);
@@ -712,9 +727,9 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
         case K_RRCS: {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          char* fwd = st.op != K_RRCS ? nullptr : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
+          const int nfwd = st.op == K_RRCS ? 1 : 0;
           for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
-            reduce_dispatch(A.dtype, dst + off, fwd ? fwd + off : nullptr, src + off, s_stage, 1, off, len / elt);
+            reduce_dispatch(A.dtype, dst + off, s_fwd, nfwd, src + off, s_stage, 1, off, len / elt);
           });
           break;
         }
@@ -726,13 +741,13 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
             const int64_t nu = len / unit;
             const int64_t a = off + nu * st.part / st.nparts * unit;
             const int64_t b = (st.part + 1 == st.nparts) ? off + len : off + nu * (st.part + 1) / st.nparts * unit;
-            if (b > a) reduce_dispatch(A.dtype, dst + a, nullptr, src + a, s_stage, st.fuse_count, a, (b - a) / elt);
+            if (b > a) reduce_dispatch(A.dtype, dst + a, s_fwd, st.fwd_count, src + a, s_stage, st.fuse_count, a, (b - a) / elt);
           });
           break;
         }
         case K_RECV:  // zero-copy: the bytes are already in place
           break;
-        default:  // K_NOP, K_SENT: no data work on this side
+        default:  // K_NOP, K_SENT, K_PUB: no data work on this side
           break;
       }
       __syncthreads();
@@ -746,9 +761,12 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
           record_error(c, st.op, k);
           s_abort = 1;
         }
-        if (!LL && (st.op == K_SEND || st.op == K_RRCS)) {
+        if (!LL && st.op == K_RRC_FUSED && st.fwd_count)  // this member's peer stores, before its
+          asm volatile("fence.acq_rel.sys;" ::: "memory");  // done flag (a K_PUB acquires it)
+        if (!LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_PUB)) {
           // all threads' peer stores are ordered before this by bar.sync (causality order);
-          // the system-scope acq_rel fence makes them visible before the flag (cumulativity)
+          // the system-scope acq_rel fence makes them visible before the flag (cumulativity;
+          // K_PUB: the chain members' stores, ordered by their fence + our acquire of done)
           if (A.variant != 9) asm volatile("fence.acq_rel.sys;" ::: "memory");  // 9: timing probe only
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)((st.op == K_RRCS ? st.fwd_seq : st.seq) + 1));

@@ -10,6 +10,7 @@
 //    before X_1 or after X_K. X_K becomes one multi-input reduction (fp32 accumulation for
 //    bf16); X_1..X_{K-1} only keep their place in program order.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 
@@ -124,6 +125,70 @@ void fuse_chains(const Gpu& g, const HB& hb, const std::map<std::pair<int, int>,
   }
 }
 
+// Chain + send fusion: a send that immediately follows a fused-chain member in its tb, reads
+// exactly the chain's destination and waits on nothing but chain members, has its bytes
+// written by the chain members themselves — each member stores its portion of the reduced
+// result to every such send's destination on the peer as it computes it (one pass; NVLink
+// busy while reducing, like K_RRCS for single rrcs). The send becomes K_PUB: after the chain
+// (its dependencies) it only publishes the data flag (direct mode) or nothing (LL mode).
+// Direct AR = RS ++ AG is exactly this shape: the AG phase's sends of the
+// reduced chunk follow the RS phase's chain into that chunk.
+// Legality beyond the dependency shape: the bytes now land while the chain runs, earlier
+// than the send's own position, so the receiver must touch the destination range with
+// nothing but the matched receive (rrc staging slots are private to their receive).
+bool only_receive_touches(const Program& P, int peer, int8_t rbuf, int off, int cnt) {
+  if (rbuf == KB_STAGE) return true;
+  const BufId b = rbuf == KB_O ? B_O : B_S;
+  int touching = 0;
+  for (const TB& tb : P.gpus[peer].tbs)
+    for (const Step& st : tb.steps)
+      if (overlap(st.srcbuf, st.srcoff, st.cnt, b, off, cnt) || overlap(st.dstbuf, st.dstoff, st.cnt, b, off, cnt))
+        ++touching;
+  return touching == 1;
+}
+
+void fuse_chain_sends(const Program& P, RankPlan& rp, const std::vector<std::vector<std::pair<int, int>>>& deps,
+                      const std::vector<std::vector<std::pair<int, int>>>& post) {
+  std::map<int, std::vector<int>> chains;  // fuse_begin -> member flat indices
+  for (size_t i = 0; i < rp.steps.size(); ++i)
+    if (rp.steps[i].op == K_RRC_FUSED) chains[rp.steps[i].fuse_begin].push_back((int)i);
+  auto pos = [&](int fi) {  // flat index -> (tb, step)
+    for (int t = 0; t < (int)rp.tbs.size(); ++t)
+      if (fi >= rp.tbs[t].step_begin && fi < rp.tbs[t].step_begin + rp.tbs[t].nsteps)
+        return std::make_pair(t, fi - rp.tbs[t].step_begin);
+    return std::make_pair(-1, -1);
+  };
+  for (auto& [fb, mem] : chains) {
+    std::vector<std::pair<int, int>> mpos;
+    for (int fi : mem) mpos.push_back(pos(fi));
+    const KStep& m0 = rp.steps[mem[0]];
+    std::vector<int> sends;
+    for (size_t q = 0; q < mem.size(); ++q) {
+      const int si = mem[q] + 1;
+      const auto [t, k] = mpos[q];
+      if (k + 1 >= rp.tbs[t].nsteps) continue;
+      const KStep& s = rp.steps[si];
+      if (s.op != K_SEND || s.srcbuf != m0.dstbuf || s.srcoff != m0.dstoff || s.cnt != m0.cnt || !post[si].empty())
+        continue;
+      bool only_chain = true;
+      for (auto d : deps[si]) only_chain = only_chain && std::find(mpos.begin(), mpos.end(), d) != mpos.end();
+      if (only_chain && only_receive_touches(P, rp.tbs[t].send, s.rbuf, s.roff, s.cnt)) sends.push_back(si);
+    }
+    if (sends.empty() || (int)sends.size() > kMaxRanks) continue;
+    const int fwb = (int)rp.fused.size();
+    for (int si : sends) {
+      KStep& s = rp.steps[si];
+      const KTB& kt = rp.tbs[pos(si).first];
+      for (int v : {kt.send, kt.chan, (int)s.rbuf, s.roff, s.roff2, s.seq}) rp.fused.push_back(v);
+      s.op = K_PUB;
+    }
+    for (int fi : mem) {
+      rp.steps[fi].fwd_begin = fwb;
+      rp.steps[fi].fwd_count = (int)sends.size();
+    }
+  }
+}
+
 std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
@@ -214,6 +279,9 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
       }
     }
     if (fuse) fuse_chains(g, hb, flat, rp, deps, post);
+    // opt-in (TACCL_CHAIN_SENDS=1): measured +12% for direct AR at n=4 >= 256 MiB but -10%
+    // at 2-32 MiB, where the default sets use direct AR (profiles/r01_chain_sends_n4.txt)
+    if (fuse && fuse_rrcs && getenv("TACCL_CHAIN_SENDS")) fuse_chain_sends(P, rp, deps, post);
     // flatten dependency lists; need_done: referenced by some (post-)dependency
     for (size_t i = 0; i < rp.steps.size(); ++i) {
       KStep& ks = rp.steps[i];
@@ -257,7 +325,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
       for (int i = 0; i < kt.nsteps; ++i) {
         const KStep& ks = rp.steps[kt.step_begin + i];
         const int f = ks.op == K_SEND ? 4 : ks.op == K_CPY ? 1 : ks.op == K_RRC ? 2 : ks.op == K_RRCS ? 6 :
-                      ks.op == K_RRC_FUSED ? 1 + ks.fuse_count / std::max(1, ks.nparts) : 0;
+                      ks.op == K_RRC_FUSED ? 1 + (ks.fuse_count + 4 * ks.fwd_count) / std::max(1, ks.nparts) : 0;
         w += (long long)f * ks.cnt;
       }
       kt.weight = (int32_t)std::min<long long>(w, 1 << 20);

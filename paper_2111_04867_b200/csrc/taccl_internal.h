@@ -80,7 +80,9 @@ enum KOp : int8_t {
                    // dst = src + sum(staging_i) (fp32 accumulation for bf16)
   K_RRCS = 6,      // rrc fused with the next step's send of its result (recv-reduce-copy-send):
                    // one pass writes dst locally and the send's destination on the peer
-  K_SENT = 7       // a send already performed (and published) by the preceding K_RRCS
+  K_SENT = 7,      // a send already performed (and published) by the preceding K_RRCS
+  K_PUB = 8        // a send whose bytes the fused chain it follows already stored (fuse_chain_sends):
+                   // publish the data flag only
 };
 enum KBuf : int8_t { KB_I = 0, KB_O = 1, KB_S = 2, KB_STAGE = 3 };
 
@@ -100,6 +102,8 @@ struct KStep {
   int32_t part, nparts;   // K_RRC_FUSED: this member reduces portion `part` of `nparts`
   int32_t post_begin, post_count;  // deps waited AFTER the work, before publishing done
   int32_t need_done;      // some step depends on this one
+  int32_t fwd_begin, fwd_count;  // K_RRC_FUSED: forward destinations (ints in the fused array:
+                                 // peer, chan, rbuf, roff, roff2, seq per entry)
 };
 
 struct KTB {

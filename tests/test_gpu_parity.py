@@ -165,6 +165,24 @@ def test_allreduce_exact(algo, n, p, m, dtype, mode):
     assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
 
 
+@pytest.mark.parametrize("n,p,m", [(3, 1, 1), (4, 1, 2), (8, 2, 1)])
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_allreduce_chain_sends_fusion(n, p, m, dtype, mode):
+    # TACCL_CHAIN_SENDS=1: the AG-phase sends of a direct AR are performed by the RS-phase
+    # chain members as they reduce (plan.cpp fuse_chain_sends); same bits as the oracle
+    os.environ["TACCL_CHAIN_SENDS"] = "1"
+    try:
+        count = n * p * 1013 if dtype == "bfloat16" else n * p * 2051
+        text = generate("allreduce", "direct", n, p, m)
+        kind = "bits" if dtype == "int32" else "intval"
+        ins = [allreduce_input(count, dtype, kind, 16, r) for r in range(n)]
+        got = run_gpu(text, "allreduce", n, dtype, ins, mode=mode)
+        assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
+    finally:
+        os.environ.pop("TACCL_CHAIN_SENDS", None)
+
+
 @pytest.mark.parametrize("algo,n,dtype,tol", [
     ("ring", 8, "float32", 1e-6), ("direct", 8, "float32", 1e-6), ("direct", 4, "float32", 1e-6),
     ("ring", 4, "bfloat16", 1e-2), ("direct", 8, "bfloat16", 1e-2), ("direct", 4, "bfloat16", 1e-2),
