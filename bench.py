@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="taccl", choices=["taccl", "reference"])
     ap.add_argument("--size", type=int, default=GIB, help="S: Allgather output bytes")
-    ap.add_argument("--algo", default="direct")
+    ap.add_argument("--algo", default="auto", help="auto = the size-specialised default set (generator/tuned.py)")
     ap.add_argument("--chunks", type=int, default=1)
     ap.add_argument("--instances", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -108,6 +108,16 @@ def busbw_factor(coll, n):
     return 2.0 * (n - 1) / n if coll == "allreduce" else (n - 1) / n
 
 
+def resolve_algo(algo, n, S):
+    """the schedule the run uses: `auto` = the default set's member for this size"""
+    if n == 1:
+        return "direct"
+    if algo != "auto":
+        return algo
+    from paper_2111_04867_b200.generator.tuned import ranges
+    return next(al for al, lo, hi in ranges("allgather", n) if lo <= S < hi)
+
+
 def cpu_oracle_baseline(size_bytes, n, algo, seconds=10.0):
     """The oracle (test infrastructure) as it stands, on a bounded sample of the workload."""
     import numpy as np
@@ -146,7 +156,7 @@ def main():
     coll = "allgather"
     S = a.size
     workload = (f"allgather n=1 local copy path, {S >> 20} MiB bf16" if n == 1 else
-                f"allgather {a.algo} schedule n={n} p={a.chunks} m={a.instances}, {S >> 20} MiB output bf16")
+                f"allgather n={n}, {S >> 20} MiB output bf16, schedule {a.algo}")
     metric = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 
     if a.impl == "reference":
@@ -154,7 +164,7 @@ def main():
         if rank != 0:
             return
         steps = a.steps or 3
-        cpu = cpu_oracle_baseline(S, n, a.algo, seconds=max(2.0, 2.0 * (steps + a.warmup)))
+        cpu = cpu_oracle_baseline(S, n, resolve_algo(a.algo, n, S), seconds=max(2.0, 2.0 * (steps + a.warmup)))
         line = {"impl": "reference", "metric": metric, "value": cpu["value"], "unit": "GB/s", "n_gpus": n,
                 "steps": steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
@@ -176,7 +186,11 @@ def main():
     count = S // 2 // n  # bf16 elements per rank
     scratch = (2 * S + (64 << 20)) if not a.no_e2e else (64 << 20)
     comm = taccl.Comm(rank=rank, nranks=n, device=local_rank, scratch_bytes=scratch)
-    comm.load(generate(coll, a.algo if n > 1 else "direct", n, a.chunks, a.instances))
+    algo_used = resolve_algo(a.algo, n, S)
+    if a.algo == "auto":
+        comm.load_defaults(("allgather",))
+    else:
+        comm.load(generate(coll, algo_used, n, a.chunks, a.instances))
     g = torch.Generator(device="cuda").manual_seed(211104867 + rank)
     inp = torch.randint(-32768, 32767, (count,), dtype=torch.int16, device="cuda", generator=g).view(torch.bfloat16)
     out = torch.empty(n * count, dtype=torch.bfloat16, device="cuda")
@@ -265,7 +279,8 @@ def main():
         line = {"metric": metric, "value": round(value, 2), "unit": "GB/s", "n_gpus": n, "steps": steps,
                 "warmup": a.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": workload, "size_bytes": S, "algo": a.algo if n > 1 else "copy",
+                "config": {"workload": workload, "size_bytes": S, "algo": algo_used if n > 1 else "copy",
+                           "algo_choice": a.algo,
                            "chunks_per_rank": a.chunks, "instances": a.instances,
                            "plan": comm.plan_info("allgather", count, taccl.BFLOAT16),
                            "l2": "inputs and outputs > 126 MB L2 (no flush needed)",
@@ -276,7 +291,7 @@ def main():
             line["busbw_per_gpu"] = round(busbw, 2)
             line["busbw_frac_of_900"] = round(busbw / NVLINK_NOMINAL, 4)
         if n == 1 and not a.no_cpu:
-            line["cpu_baseline"] = cpu_oracle_baseline(S, n, "direct")
+            line["cpu_baseline"] = cpu_oracle_baseline(S, n, algo_used)
         print(json.dumps(line))
     if world > 1:
         dist.barrier()

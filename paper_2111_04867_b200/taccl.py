@@ -130,10 +130,7 @@ class Comm:
                 _check(lib().taccl_comm_set_peers(allb, HANDLE_BYTES))
 
     def _all_gather_bytes(self, b: bytes) -> bytes:
-        import torch.distributed as dist
-        out = [None] * self.nranks
-        dist.all_gather_object(out, b, group=self.group)
-        return b"".join(out)
+        return all_gather_blobs(b, self.nranks, self.group)
 
     def load(self, text: str):
         b = text.encode()
@@ -222,6 +219,18 @@ class Comm:
 
     def reduce_scatter(self, out, inp, stream=None):
         self.run(REDUCESCATTER, out, inp, stream)
+
+
+def all_gather_blobs(b: bytes, nranks: int, group=None) -> bytes:
+    """The one-time handle exchange: every rank's fixed-size blob, in rank
+    order, concatenated — the layout taccl_comm_set_peers / taccl_register_buffer expect.
+    Works on any torch.distributed backend (gloo in the CPU tests, nccl in the bench)."""
+    import torch.distributed as dist
+    if len(b) != HANDLE_BYTES:
+        raise ValueError(f"handle blobs are {HANDLE_BYTES} bytes, got {len(b)}")
+    out = [None] * nranks
+    dist.all_gather_object(out, b, group=group)
+    return b"".join(out)
 
 
 def launch_count() -> int:
