@@ -188,6 +188,8 @@ __device__ __noinline__ void cta_reduce(char* dst, char* const* fwd, int nfwd, c
   uintptr_t align = (uintptr_t)dst | (uintptr_t)src0;
   for (int s = 0; s < ns; ++s) align |= (uintptr_t)(stages[s] + soff);
   for (int f = 0; f < nfwd; ++f) align |= (uintptr_t)(fwd[f] + soff);
+  // the first forward destination in a register (rrc+send, the common case); more from smem
+  char* const f0 = nfwd > 0 ? fwd[0] + soff : nullptr;
   const int64_t nv = (align & 15) ? 0 : nelem / V;
   int64_t v = tid;
   for (; v + (int64_t)(RU - 1) * nt < nv; v += (int64_t)RU * nt) {
@@ -213,7 +215,8 @@ __device__ __noinline__ void cta_reduce(char* dst, char* const* fwd, int nfwd, c
       const int4 o = E::pack(acc[u]);
       const int64_t off = (v + (int64_t)u * nt) * 16;
       st_v4(reinterpret_cast<int4*>(dst + off), o);
-      for (int f = 0; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
+      if (f0) st_v4(reinterpret_cast<int4*>(f0 + off), o);
+      for (int f = 1; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
     }
   }
   for (; v < nv; v += nt) {
@@ -227,7 +230,8 @@ __device__ __noinline__ void cta_reduce(char* dst, char* const* fwd, int nfwd, c
     }
     const int4 o = E::pack(acc);
     st_v4(reinterpret_cast<int4*>(dst + off), o);
-    for (int f = 0; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
+    if (f0) st_v4(reinterpret_cast<int4*>(f0 + off), o);
+    for (int f = 1; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
   }
   for (int64_t e = nv * V + tid; e < nelem; e += nt) {
     const int64_t off = e * E::bytes;
@@ -545,7 +549,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
   __shared__ char* s_fwd[kMaxRanks];  // forward destinations of this step (RRCS / chain sends)
   __shared__ __align__(8) u64 s_bar[kTmaStages];
   extern __shared__ __align__(128) int4 s_dyn[];  // [TMA stages (direct kernel)] [plan]
-  int4* const s_plan = s_dyn + (LL ? 0 : kTmaBytes / 16);
+  int4* const s_plan = s_dyn + (LL || !A.tma ? 0 : kTmaBytes / 16);
   const int tid = threadIdx.x;
   u64 t_entry = 0;
   if (A.trace && tid == 0) t_entry = globaltimer();
@@ -618,12 +622,16 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kern
   // front — this rank's previous call has fully completed (stream order), so nothing of it
   // can still read the buffers the sender is about to store into; announcing per piece as
   // it starts would throttle the sender to this CTA's per-piece progress.
-  if (!LL && tb.recv >= 0 && tid == 0) {
+  if (!LL && tb.recv >= 0 && tid == 0 && !A.ready_per_piece) {
     u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
     for (int j = c0; j < nsplit; j += ct) st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
   }
   for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
+    if (!LL && tb.recv >= 0 && tid == 0 && A.ready_per_piece) {  // A/B knob: announce as each piece starts
+      u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
+      st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
+    }
     bool sender_ready = false;
 
     for (int k = 0; k < tb.nsteps; ++k) {

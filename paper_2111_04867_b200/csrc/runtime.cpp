@@ -124,7 +124,7 @@ taccl_result_t comm_common_init(int nranks, int device, size_t scratch) {
   g.device = device;
   g.arena_bytes = kOffScratch + (scratch ? scratch : env_size("TACCL_SCRATCH_BYTES", 256ull << 20));
   g.timeout_ns = (uint64_t)(env_size("TACCL_TIMEOUT_S", 20) * 1000000000ull);
-  g.staged_bytes = std::min<int64_t>((int64_t)env_size("TACCL_STAGED_REGION", 4 << 20),
+  g.staged_bytes = std::min<int64_t>((int64_t)env_size("TACCL_STAGED_REGION", 16 << 20),
                                      (int64_t)(g.arena_bytes - kOffScratch) / 8) & ~(int64_t)4095;
   std::string err;
   g.max_ctas = executor_max_ctas(device, &err);
@@ -211,8 +211,11 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   const int64_t sb = staged_region_bytes();
   const int64_t total_bytes = (int64_t)n_out * G->chunk_bytes;
   const int64_t ll_cb = 16 * ((G->chunk_bytes + 7) / 8);
-  G->staged = (int64_t)a->max_stage2_chunks * ll_cb <= sb &&
-              total_bytes <= (int64_t)env_size("TACCL_STAGED_MAX", 1 << 20) ? 1 : 0;
+  // LL up to 2 MiB of output for AG/A2A and 4 MiB for AR/RS (measured crossovers vs the
+  // direct kernel at n=2 and n=4, profiles/r01_ll_threshold.txt); TACCL_STAGED_MAX overrides
+  const int64_t ll_max = (int64_t)env_size("TACCL_STAGED_MAX", (coll == TACCL_ALLREDUCE || coll == TACCL_REDUCESCATTER)
+                                                                    ? (4 << 20) : (2 << 20));
+  G->staged = (int64_t)a->max_stage2_chunks * ll_cb <= sb && total_bytes <= ll_max ? 1 : 0;
   // bytes per CTA: LL lines are latency-bound, so LL pieces are small (4 KiB of payload per
   // CTA measured best at n=2 up to 1 MiB, profiles/r01_small_sweep_n2.txt)
   const int64_t min_piece = G->staged ? (int64_t)env_size("TACCL_LL_MIN_PIECE", 4 << 10)
@@ -356,8 +359,9 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.ncta = cta;
   A.plan_smem = smem <= kPlanSmemMax ? 1 : 0;
   A.tma = (int)env_size("TACCL_TMA", 1);
+  A.ready_per_piece = (int)env_size("TACCL_READY_PER_PIECE", 0);
   std::string err;
-  const int dyn = (A.plan_smem ? smem : 0) + (A.staged ? 0 : kTmaBytes);
+  const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
   ++g.launches;
   ++g_launches;

@@ -185,6 +185,8 @@ struct KArgs {
   unsigned long long* trace;  // optional %globaltimer stamps, kTraceSlots per CTA (taccl_trace)
   int32_t trace_ctas;         // CTAs that fit in the trace buffer
   int32_t ncta;               // grid size
+  int32_t ready_per_piece;    // A/B knob (TACCL_READY_PER_PIECE): entry handshake per piece start
+  int32_t pad3;
   uint32_t cta_map[256];      // per CTA: local rank, tb, first piece, CTAs of the tb (cta_pack)
 };
 constexpr int kMaxGrid = 256;
