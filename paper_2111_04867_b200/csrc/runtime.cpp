@@ -211,10 +211,9 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   const int64_t sb = staged_region_bytes();
   const int64_t total_bytes = (int64_t)n_out * G->chunk_bytes;
   const int64_t ll_cb = 16 * ((G->chunk_bytes + 7) / 8);
-  // LL up to 2 MiB of output for AG/A2A and 4 MiB for AR/RS (measured crossovers vs the
+  // LL up to 2 MiB of output for AG/A2A/AR and 4 MiB for RS (measured crossovers vs the
   // direct kernel at n=2 and n=4, profiles/r01_ll_threshold.txt); TACCL_STAGED_MAX overrides
-  const int64_t ll_max = (int64_t)env_size("TACCL_STAGED_MAX", (coll == TACCL_ALLREDUCE || coll == TACCL_REDUCESCATTER)
-                                                                    ? (4 << 20) : (2 << 20));
+  const int64_t ll_max = (int64_t)env_size("TACCL_STAGED_MAX", coll == TACCL_REDUCESCATTER ? (4 << 20) : (2 << 20));
   G->staged = (int64_t)a->max_stage2_chunks * ll_cb <= sb && total_bytes <= ll_max ? 1 : 0;
   // bytes per CTA: LL lines are latency-bound, so LL pieces are small (4 KiB of payload per
   // CTA measured best at n=2 up to 1 MiB, profiles/r01_small_sweep_n2.txt)

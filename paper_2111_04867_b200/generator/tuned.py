@@ -23,13 +23,20 @@ def ranges(coll: str, n: int):
         return [("direct", 0, INF)] if n == 2 else [("direct", 0, 128 * MiB), ("ring", 128 * MiB, INF)]
     if coll == "alltoall":
         return [("direct", 0, INF)]
+    # rings round every hop's bf16 partial (reading R4): at n >= 8 that reaches 1.2e-2 relative
+    # error on U[1,2) inputs, above the north star's 1e-2, so large-n sets keep the direct
+    # (one rounding per element) schedules
     if coll == "allreduce":
         if n == 2:
             return [("oneshot", 0, 16 * MiB), ("direct", 16 * MiB, INF)]
         small = MiB // 2 if n <= 4 else MiB // 4
+        if n >= 8:
+            return [("oneshot", 0, small), ("direct", small, INF)]
         return [("oneshot", 0, small), ("direct", small, 64 * MiB), ("ring", 64 * MiB, INF)]
     if coll == "reducescatter":
-        return [("direct", 0, INF)] if n == 2 else [("direct", 0, 32 * MiB), ("ring", 32 * MiB, INF)]
+        if n == 2 or n >= 8:
+            return [("direct", 0, INF)]
+        return [("direct", 0, 32 * MiB), ("ring", 32 * MiB, INF)]
     raise ValueError(coll)
 
 

@@ -308,6 +308,48 @@ def test_run_host_pipelined_single_rank(coll, count, piece):
         os.environ.pop("TACCL_HOST_PIECE_BYTES", None)
 
 
+# ---------------------------------------------------------------- device tracing
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_trace_timeline_is_consistent(mode):
+    # taccl_trace: per CTA entry <= prologue <= step start <= waits <= done <= exit, identity
+    # words name (rank, tb, piece) of every CTA of the launch
+    os.environ["TACCL_STAGED_MAX"] = MODES[mode]
+    n, count = 4, 4 * 8192
+    comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=64 << 20)
+    try:
+        text = generate("allreduce", "direct", n, 1, 1)
+        comm.load(text)
+        ins = [to_dev(allreduce_input(count, "int32", "bits", 17, r), "int32") for r in range(n)]
+        outs = [torch.empty(count, dtype=torch.int32, device="cuda") for _ in range(n)]
+        comm.run_emulated("allreduce", outs, ins)
+        buf = torch.zeros(1024 * taccl.TRACE_SLOTS, dtype=torch.int64, device="cuda")
+        comm.trace(buf)
+        comm.run_emulated("allreduce", outs, ins)
+        torch.cuda.synchronize()
+        comm.trace(None)
+        comm.check()
+        grid = comm.plan_info("allreduce", count, taccl.INT32)["ctas"] * n
+        T = buf[:grid * taccl.TRACE_SLOTS].view(grid, taccl.TRACE_SLOTS).cpu().tolist()
+        prog = oracle.parse(text)
+        seen = set()
+        for row in T:
+            ident = row[-2]
+            r, tb = ident >> 32, (ident >> 16) & 0xFFFF
+            seen.add((r, tb))
+            assert 0 < row[0] <= row[1] <= row[-1]
+            nsteps = len(prog.gpus[r].tbs[tb].steps)
+            last = row[1]
+            for k in range(nsteps):
+                s0, s1, s3 = row[2 + 4 * k], row[3 + 4 * k], row[5 + 4 * k]
+                assert last <= s0 <= s1 <= s3 <= row[-1], (r, tb, k)
+                last = s3
+        assert seen == {(r, t) for r in range(n) for t in range(len(prog.gpus[r].tbs))}
+    finally:
+        comm.destroy()
+        os.environ.pop("TACCL_STAGED_MAX", None)
+
+
 # ---------------------------------------------------------------- edge cases
 
 def test_single_rank_copy_path():

@@ -35,7 +35,11 @@ def gen(coll, al, n):
     """algorithm name -> EF text; suffix _split = sends and receives in separate threadblocks"""
     if al.endswith("_split"):
         return generate(coll, al[:-6], n, 1, 1, pair=False)
-    return generate(coll, al, n, 1, 1)
+    # name_pP_mM: chunks per rank P, instances M (PAPER.md:702-711, 785-789)
+    parts = al.split("_")
+    p = next((int(x[1:]) for x in parts[1:] if x.startswith("p")), 1)
+    m = next((int(x[1:]) for x in parts[1:] if x.startswith("m")), 1)
+    return generate(coll, parts[0], n, p, m)
 
 
 def factor(coll, n):
@@ -114,6 +118,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (no host overhead)")
+    ap.add_argument("--algos", default=None, help="comma list overriding the per-collective defaults")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -142,7 +147,7 @@ def main():
             comm.free(h)
     out_f = open(a.out or os.path.join(ROOT, "gpurun_out", f"sweep_n{n}.jsonl"), "a") if rank == 0 else None
     for coll in a.colls.split(","):
-        algos = ALGOS[coll] if n > 1 else ["direct"]
+        algos = (a.algos.split(",") if a.algos else ALGOS[coll]) if n > 1 else ["direct"]
         handles = {al: load(gen(coll, al, n)) for al in algos}
         for k in range(a.size_lo, a.size_hi + 1):
             S = 1 << k
