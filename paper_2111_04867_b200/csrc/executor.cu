@@ -542,7 +542,7 @@ __device__ void record_error(const Ctx& c, int what, int step) {
 // LL = staged (small-message) mode, a compile-time specialisation so each variant carries
 // only its own data path (register pressure: the LL variant inlines its line loop).
 template <bool LL>
-__global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, 1) taccl_exec_kernel(const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPerSM) taccl_exec_kernel(const __grid_constant__ KArgs A) {
   __shared__ int s_abort;
   __shared__ u64 s_epoch;
   __shared__ const char* s_stage[kMaxRanks + 1];

@@ -209,9 +209,13 @@ TACCL_HD inline int cta_indep(uint32_t m) { return (int)((m >> 28) & 1); }
 constexpr int kTraceSlots = TACCL_TRACE_SLOTS;
 constexpr int kTraceSteps = (kTraceSlots - 4) / 4;
 
-constexpr int kThreads = 512;    // direct (bulk) kernel
+#ifndef TACCL_DIRECT_THREADS
+#define TACCL_DIRECT_THREADS 512
+#endif
+constexpr int kThreads = TACCL_DIRECT_THREADS;  // direct (bulk) kernel; 1024/kThreads CTAs per SM
+constexpr int kDirectPerSM = 1024 / kThreads;
 constexpr int kThreadsLL = 256;  // LL (small-message) kernel: 255 registers/thread, no spills
-constexpr int kTmaStages = 4, kTmaStage = 32 << 10;
+constexpr int kTmaStages = 4, kTmaStage = (32 << 10) / kDirectPerSM;
 constexpr int kTmaBytes = kTmaStages * kTmaStage;  // dynamic smem of the direct kernel
 
 // Pieces of one threadblock = its CTAs (same rule on host and device). Dependent tbs share
@@ -227,7 +231,7 @@ TACCL_HD inline int tb_pieces(int indep, int weight, int wsum, int budget, int s
 
 // executor.cu
 int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::string* err);
-constexpr int kPlanSmemMax = 48 << 10;  // plans up to this size are staged in shared memory
+constexpr int kPlanSmemMax = (48 << 10) / kDirectPerSM;  // plans up to this size are staged in smem
 int executor_max_ctas(int device, std::string* err);  // co-resident CTA capacity
 
 }  // namespace taccl

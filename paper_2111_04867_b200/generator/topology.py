@@ -19,6 +19,12 @@ from dataclasses import dataclass, field
 NVLINK_ALPHA_US = 0.7            # Table 1
 NVLINK5_BETA_US_PER_MB = (1 << 20) / 900e9 * 1e6   # 1.165 us/MB at 900 GB/s
 IB_ALPHA_US, IB_BETA_US_PER_MB = 1.7, 106.0        # Table 1
+# Measured on this pool's B200s through this executor (tools/alphabeta.py over the graph-mode
+# sweeps, profiles/r01_alphabeta.json): one connection per GPU (ring hop) streams at 714 GB/s
+# (beta 1.468 us/MB) with ~6 us per hop of flag/fence overhead (direct kernel); n-1 concurrent
+# connections share ~690 GB/s per GPU (the paper's multi-connection effect).
+B200_NVLINK_ALPHA_US = 6.6
+B200_NVLINK_BETA_US_PER_MB = 1.468
 
 
 @dataclass(frozen=True)
@@ -45,7 +51,8 @@ class Topology:
 
 
 def nvswitch(n: int, alpha=NVLINK_ALPHA_US, beta=NVLINK5_BETA_US_PER_MB) -> Topology:
-    """One B200 NVSwitch domain: every GPU reaches every other at full bandwidth."""
+    """One B200 NVSwitch domain: every GPU reaches every other at full bandwidth. Defaults are
+    the paper's alpha with the nominal NVLink 5 beta; nvswitch_measured() uses the profile."""
     t = Topology(f"nvswitch{n}", n, [0] * n)
     for u in range(n):
         for v in range(n):
@@ -53,6 +60,11 @@ def nvswitch(n: int, alpha=NVLINK_ALPHA_US, beta=NVLINK5_BETA_US_PER_MB) -> Topo
                 t.links[(u, v)] = Link(alpha, beta, "nvlink")
     t.switches.append(list(range(n)))
     return t
+
+
+def nvswitch_measured(n: int) -> Topology:
+    """nvswitch() with the alpha-beta values profiled on B200 (B200_NVLINK_*)."""
+    return nvswitch(n, B200_NVLINK_ALPHA_US, B200_NVLINK_BETA_US_PER_MB)
 
 
 def multinode(nodes: int, per_node: int, intra=(NVLINK_ALPHA_US, NVLINK5_BETA_US_PER_MB),

@@ -16,7 +16,8 @@ INF = math.inf
 
 
 def ranges(coll: str, n: int):
-    """[(algo, min_bytes, max_bytes)] covering [0, inf) for `coll` at n ranks."""
+    """[(algo, min_bytes, max_bytes)] covering [0, inf) for `coll` at n ranks; algo may carry
+    a chunk-partitioning suffix `_pK` (K chunks per rank)."""
     if n == 1:
         return [("direct", 0, INF)]
     if coll == "allgather":
@@ -32,7 +33,9 @@ def ranges(coll: str, n: int):
         small = MiB // 2 if n <= 4 else MiB // 4
         if n >= 8:
             return [("oneshot", 0, small), ("direct", small, INF)]
-        return [("oneshot", 0, small), ("direct", small, 64 * MiB), ("ring", 64 * MiB, INF)]
+        # 2 chunks per rank pipeline the ring's 2(n-1) hops: -10..13% time at >= 128 MiB
+        # (profiles/r01_ar_variants_n4.txt)
+        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("ring_p2", 128 * MiB, INF)]
     if coll == "reducescatter":
         if n == 2 or n >= 8:
             return [("direct", 0, INF)]
@@ -43,4 +46,8 @@ def ranges(coll: str, n: int):
 def default_schedules(coll: str, n: int):
     """EF texts of the default set for (coll, n), each carrying its size range."""
     from . import generate
-    return [generate(coll, algo, n, 1, 1, min_bytes=lo, max_bytes=hi) for algo, lo, hi in ranges(coll, n)]
+    out = []
+    for algo, lo, hi in ranges(coll, n):
+        name, _, p = algo.partition("_p")
+        out.append(generate(coll, name, n, int(p) if p else 1, 1, min_bytes=lo, max_bytes=hi))
+    return out

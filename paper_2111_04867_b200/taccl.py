@@ -11,7 +11,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtaccl.so")
+LIB_PATH = os.environ.get("TACCL_LIB") or os.path.join(HERE, "libtaccl.so")  # TACCL_LIB: experiment variants
 
 ALLGATHER, ALLTOALL, ALLREDUCE, REDUCESCATTER = 0, 1, 2, 3
 INT32, FLOAT32, BFLOAT16 = 0, 1, 2

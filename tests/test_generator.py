@@ -193,6 +193,15 @@ def test_instances_double_threadblocks_and_halve_chunks():
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
 
 
+def test_measured_profile_topology_synthesizes_correct_schedules():
+    # the profiled B200 alpha-beta (tools/alphabeta.py) plugs into the greedy synthesizer
+    from paper_2111_04867_b200.generator.topology import nvswitch_measured
+    for coll in ("allgather", "alltoall"):
+        alg = synthesize(coll, 4, 2, topology=nvswitch_measured(4))
+        from paper_2111_04867_b200.generator.lowering import lower
+        assert oracle.validate(lower(alg)).ok
+
+
 @pytest.mark.parametrize("coll", ["allgather", "alltoall", "allreduce", "reducescatter"])
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
 def test_default_sets_cover_all_sizes_once(coll, n):
