@@ -128,7 +128,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     S_max = 1 << a.size_hi
-    comm = taccl.Comm(rank=rank, nranks=n, device=local, scratch_bytes=S_max + (64 << 20))
+    comm = taccl.Comm(rank=rank, nranks=n, device=local, scratch_bytes=2 * S_max + (64 << 20))
     dt = torch.bfloat16 if a.dtype == "bfloat16" else torch.float32
     es = 2 if dt == torch.bfloat16 else 4
     # buffers sized for the largest message; registered once (zero-copy)
