@@ -212,8 +212,8 @@ constexpr int kTraceSteps = (kTraceSlots - 4) / 4;
 #ifndef TACCL_DIRECT_THREADS
 #define TACCL_DIRECT_THREADS 512
 #endif
-constexpr int kThreads = TACCL_DIRECT_THREADS;  // direct (bulk) kernel; 1024/kThreads CTAs per SM
-constexpr int kDirectPerSM = 1024 / kThreads;
+constexpr int kThreads = TACCL_DIRECT_THREADS;  // direct (bulk) kernel; 512/kThreads CTAs per SM
+constexpr int kDirectPerSM = 512 / kThreads;    // (512 threads: one CTA per SM, 128 registers)
 constexpr int kThreadsLL = 256;  // LL (small-message) kernel: 255 registers/thread, no spills
 constexpr int kTmaStages = 4, kTmaStage = (32 << 10) / kDirectPerSM;
 constexpr int kTmaBytes = kTmaStages * kTmaStage;  // dynamic smem of the direct kernel

@@ -378,7 +378,7 @@ def test_trace_timeline_is_consistent(mode):
         torch.cuda.synchronize()
         comm.trace(None)
         comm.check()
-        grid = comm.plan_info("allreduce", count, taccl.INT32)["ctas"] * n
+        grid = comm.plan_info("allreduce", count, taccl.INT32)["ctas"]  # all emulated ranks' CTAs
         T = buf[:grid * taccl.TRACE_SLOTS].view(grid, taccl.TRACE_SLOTS).cpu().tolist()
         prog = oracle.parse(text)
         seen = set()
@@ -386,12 +386,12 @@ def test_trace_timeline_is_consistent(mode):
             ident = row[-2]
             r, tb = ident >> 32, (ident >> 16) & 0xFFFF
             seen.add((r, tb))
-            assert 0 < row[0] <= row[1] <= row[-1]
+            assert 0 < row[0] <= row[1] <= row[-1], row[:2] + row[-2:]
             nsteps = len(prog.gpus[r].tbs[tb].steps)
             last = row[1]
             for k in range(nsteps):
                 s0, s1, s3 = row[2 + 4 * k], row[3 + 4 * k], row[5 + 4 * k]
-                assert last <= s0 <= s1 <= s3 <= row[-1], (r, tb, k)
+                assert last <= s0 <= s1 <= s3 <= row[-1], (r, tb, k, last, s0, s1, s3, row[-1])
                 last = s3
         assert seen == {(r, t) for r in range(n) for t in range(len(prog.gpus[r].tbs))}
     finally:
