@@ -644,12 +644,12 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           const int dt = deps[2 * (st.dep_begin + d)], dk = deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
-        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS) && !sender_ready) {
+        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) && !sender_ready) {
           ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
           sender_ready = true;
         }
         // staged (LL) mode: no data flags, every line carries its own (ll_lines)
-        if (ok && !LL && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS))
+        if (ok && !LL && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RCS))
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
         if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
@@ -659,9 +659,9 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
             s_stage[f] = LL ? my_staged + (int64_t)fz[3] * ll_cb : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
           }
         }
-        if (ok && (st.op == K_RRC || st.op == K_RRCS || st.op == K_RECV))
+        if (ok && (st.op == K_RRC || st.op == K_RRCS || st.op == K_RECV || st.op == K_RCS))
           s_stage[0] = LL ? my_staged + (int64_t)st.soff2 * ll_cb : local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
-        if (ok && (st.op == K_SEND || st.op == K_RRCS))
+        if (ok && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS))
           s_fwd[0] = LL ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * ll_cb
                         : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
         if (ok && st.op == K_RRC_FUSED) {  // fused sends of the chain's result (fuse_chain_sends)
@@ -682,7 +682,8 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       __syncthreads();
       if (s_abort) return;
 
-      if (LL && (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED)) {
+      if (LL && (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED ||
+                 st.op == K_RCS)) {
         // LL path: this piece's lines of every chunk (same split on both sides)
         const int64_t nl = (cbytes + 7) / 8;
         int64_t l0 = (int64_t)((unsigned)nl * (unsigned)j / (unsigned)nsplit);  // nl*split < 2^32 (LL sizes)
@@ -692,9 +693,9 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           l0 = a0 + m * st.part / st.nparts;
           l1 = a0 + m * (st.part + 1) / st.nparts;
         }
-        const char* src = (st.op == K_RECV) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+        const char* src = (st.op == K_RECV || st.op == K_RCS) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
         char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-        const int nfwd = (st.op == K_SEND || st.op == K_RRCS) ? 1 : st.op == K_RRC_FUSED ? st.fwd_count : 0;
+        const int nfwd = (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) ? 1 : st.op == K_RRC_FUSED ? st.fwd_count : 0;
         const bool reduce = st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED;
         const int nin = st.op == K_SEND ? 0 : st.op == K_RRC_FUSED ? st.fuse_count : 1;
         const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt, l0, l1,
@@ -755,6 +756,12 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         }
         case K_RECV:  // zero-copy: the bytes are already in place
           break;
+        case K_RCS: {  // the bytes landed in dst (zero-copy); push them on to the send's peer
+          const char* src = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+          char* dst = s_fwd[0];
+          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+          break;
+        }
         default:  // K_NOP, K_SENT, K_PUB: no data work on this side
           break;
       }
@@ -771,13 +778,14 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         }
         if (!LL && st.op == K_RRC_FUSED && st.fwd_count)  // this member's peer stores, before its
           asm volatile("fence.acq_rel.sys;" ::: "memory");  // done flag (a K_PUB acquires it)
-        if (!LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_PUB)) {
+        if (!LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_PUB || st.op == K_RCS)) {
           // all threads' peer stores are ordered before this by bar.sync (causality order);
           // the system-scope acq_rel fence makes them visible before the flag (cumulativity;
           // K_PUB: the chain members' stores, ordered by their fence + our acquire of done)
           if (A.variant != 9) asm volatile("fence.acq_rel.sys;" ::: "memory");  // 9: timing probe only
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
-          st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j), E | (u64)((st.op == K_RRCS ? st.fwd_seq : st.seq) + 1));
+          st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j),
+                         E | (u64)((st.op == K_RRCS || st.op == K_RCS ? st.fwd_seq : st.seq) + 1));
         }
         if (st.need_done && ok) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
         if (tr) trace[5 + 4 * k] = globaltimer();

@@ -307,9 +307,12 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
         for (int i = 0; i + 1 < kt.nsteps; ++i) {
           KStep& a = rp.steps[kt.step_begin + i];
           KStep& b = rp.steps[kt.step_begin + i + 1];
-          if (a.op == K_RRC && b.op == K_SEND && b.srcbuf == a.dstbuf && b.srcoff == a.dstoff &&
-              b.cnt == a.cnt && b.dep_count == 0 && b.post_count == 0) {
-            a.op = K_RRCS;
+          // recv-copy-send (§8(f) row 1, relays of ring and hierarchical schedules): same shape
+          const bool rcs = a.op == K_RECV && b.op == K_SEND && b.srcbuf == a.dstbuf && b.srcoff == a.dstoff &&
+                           b.cnt == a.cnt && b.dep_count == 0 && b.post_count == 0 && a.post_count == 0;
+          if (rcs || (a.op == K_RRC && b.op == K_SEND && b.srcbuf == a.dstbuf && b.srcoff == a.dstoff &&
+                      b.cnt == a.cnt && b.dep_count == 0 && b.post_count == 0)) {
+            a.op = rcs ? K_RCS : K_RRCS;
             a.rbuf = b.rbuf;
             a.roff = b.roff;
             a.fwd_seq = b.seq;
@@ -324,7 +327,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
       long long w = 0;
       for (int i = 0; i < kt.nsteps; ++i) {
         const KStep& ks = rp.steps[kt.step_begin + i];
-        const int f = ks.op == K_SEND ? 4 : ks.op == K_CPY ? 1 : ks.op == K_RRC ? 2 : ks.op == K_RRCS ? 6 :
+        const int f = ks.op == K_SEND || ks.op == K_RCS ? 4 : ks.op == K_CPY ? 1 : ks.op == K_RRC ? 2 : ks.op == K_RRCS ? 6 :
                       ks.op == K_RRC_FUSED ? 1 + (ks.fuse_count + 4 * ks.fwd_count) / std::max(1, ks.nparts) : 0;
         w += (long long)f * ks.cnt;
       }

@@ -81,8 +81,10 @@ enum KOp : int8_t {
   K_RRCS = 6,      // rrc fused with the next step's send of its result (recv-reduce-copy-send):
                    // one pass writes dst locally and the send's destination on the peer
   K_SENT = 7,      // a send already performed (and published) by the preceding K_RRCS
-  K_PUB = 8        // a send whose bytes the fused chain it follows already stored (fuse_chain_sends):
+  K_PUB = 8,       // a send whose bytes the fused chain it follows already stored (fuse_chain_sends):
                    // publish the data flag only
+  K_RCS = 9        // recv fused with the next step's send of what it received (recv-copy-send,
+                   // relays): LL: one pass over the lines; direct: wait, then push dst onward
 };
 enum KBuf : int8_t { KB_I = 0, KB_O = 1, KB_S = 2, KB_STAGE = 3 };
 
