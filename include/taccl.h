@@ -127,7 +127,8 @@ taccl_result_t taccl_load_algo(const char* schedule_text, size_t len, taccl_algo
  * elements per peer (both buffers hold nranks*count), AR count = total elements, RS count =
  * elements per rank (sendbuf holds nranks*count, recvbuf count). sendbuf/recvbuf are
  * device pointers; recvbuf must be registered (taccl_register_buffer) unless emulated.
- * Out-of-place only (in-place -> UNSUPPORTED). Enqueues ONE kernel on `stream`
+ * In-place / overlapping buffers are accepted (the input is first copied, on `stream`, to a
+ * private arena region; INVALID_ARG if the arena is too small). Enqueues ONE kernel on `stream`
  * (a cudaStream_t; NULL = legacy default stream); returns without synchronizing. The
  * call is CUDA-graph capturable (epochs live on the device). */
 taccl_result_t taccl_run(taccl_coll_t coll, const void* sendbuf, void* recvbuf, size_t count,

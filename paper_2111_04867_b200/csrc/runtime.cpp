@@ -392,12 +392,24 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
   const int elt = elt_size(dtype), n = g.nranks;
   if (!sendbuf || !recvbuf) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
   const size_t ib = in_bytes(coll, count, elt, n), ob = out_bytes(coll, count, elt, n);
-  if ((const char*)sendbuf < (const char*)recvbuf + ob && (const char*)recvbuf < (const char*)sendbuf + ib)
-    return fail(TACCL_ERR_UNSUPPORTED, "in-place / overlapping buffers are not supported (reading G10)");
+  const bool overlapping = (const char*)sendbuf < (const char*)recvbuf + ob && (const char*)recvbuf < (const char*)sendbuf + ib;
   Algo* a = select_algo(coll, select_bytes(coll, count, elt, n));
   if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
   Geometry G;
   if ((rc = geometry(a, coll, count, elt, 1, base_off, &G))) return rc;
+  if (overlapping) {
+    // in-place / overlapping call (NCCL allows AG with sendbuf = recvbuf + rank*count and AR
+    // with sendbuf = recvbuf; reading G10): the schedules read the input while peers write
+    // the output, so the input is first copied (same stream, before the launch) to a private
+    // region past this call's symmetric arena layout — private, so it need not be symmetric
+    const int64_t priv = (G.need + 255) & ~(int64_t)255;
+    if ((size_t)(priv + (int64_t)ib) > g.arena_bytes)
+      return fail(TACCL_ERR_INVALID_ARG, "arena too small for an in-place call: need " + std::to_string(priv + ib) +
+                                             " bytes (raise scratch_bytes / TACCL_SCRATCH_BYTES)");
+    char* copy = g.arenas[0] + priv;
+    CUDA_TRY(cudaMemcpyAsync(copy, sendbuf, ib, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    sendbuf = copy;
+  }
   char* peer_out[1][kMaxRanks] = {};
   if (arena_out) {
     for (int q = 0; q < n; ++q) peer_out[0][q] = g.peer_arena[q] + ((char*)recvbuf - g.peer_arena[g.rank]);

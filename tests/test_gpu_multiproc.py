@@ -64,6 +64,17 @@ def _worker(rank, n, port, cases, q):
             os.environ.pop("TACCL_HOST_PIECE_BYTES")
             vt = {"int32": torch.int32, "float32": torch.int32, "bfloat16": torch.int16}[dtype]
             ok = ok and bool(np.array_equal(h_out.view(vt).numpy().view(want.dtype), want))
+            # NCCL's in-place forms (reading G10): AR sendbuf == recvbuf, AG sendbuf = own slot
+            if coll in ("allreduce", "allgather"):
+                buf = torch.empty(e_out, dtype=tdt[dtype], device="cuda")
+                if coll == "allreduce":
+                    buf.copy_(x)
+                    comm.run(coll, buf, buf)
+                else:
+                    buf[rank * count:(rank + 1) * count].copy_(x)
+                    comm.run(coll, buf, buf[rank * count:(rank + 1) * count])
+                torch.cuda.synchronize()
+                ok = ok and bool(np.array_equal(buf.cpu().view(vt).numpy().view(want.dtype), want))
             results.append(ok)
             comm.free(h)
         comm.destroy()

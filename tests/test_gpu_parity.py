@@ -409,6 +409,22 @@ def test_single_rank_copy_path():
         assert_bits_equal(got, ins)
 
 
+@pytest.mark.parametrize("coll", ["allgather", "allreduce"])
+def test_in_place_single_rank(coll):
+    # NCCL's in-place forms (reading G10): the input is copied to a private arena region first
+    comm = taccl.Comm(rank=0, nranks=1, device=0, scratch_bytes=8 << 20)
+    try:
+        comm.load(generate(coll, "direct", 1, 1, 1))
+        x = to_dev(allreduce_input(12345, "int32", "bits", 18, 0), "int32")
+        buf = x.clone()
+        comm.run(coll, buf, buf)
+        torch.cuda.synchronize()
+        comm.check()
+        assert torch.equal(buf, x)
+    finally:
+        comm.destroy()
+
+
 def test_count_not_divisible_is_rejected():
     comm = taccl.Comm(nranks=2, device=0, emulated=True, scratch_bytes=1 << 20)
     try:
