@@ -189,7 +189,7 @@ void fuse_chain_sends(const Program& P, RankPlan& rp, const std::vector<std::vec
   }
 }
 
-std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
+std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
   // per-step seq numbers and staging offsets
@@ -279,9 +279,10 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs) {
       }
     }
     if (fuse) fuse_chains(g, hb, flat, rp, deps, post);
-    // opt-in (TACCL_CHAIN_SENDS=1): measured +12% for direct AR at n=4 >= 256 MiB but -10%
-    // at 2-32 MiB, where the default sets use direct AR (profiles/r01_chain_sends_n4.txt)
-    if (fuse && fuse_rrcs && getenv("TACCL_CHAIN_SENDS")) fuse_chain_sends(P, rp, deps, post);
+    // chain_sends: the LL kernel's plan (-10% time for LL direct AR at n=4); the direct kernel
+    // only with TACCL_CHAIN_SENDS=1 (+12% at >= 256 MiB, -10% at 2-32 MiB;
+    // profiles/r01_chain_sends_n4.txt, r01_chain_sends_ll_n4.txt)
+    if (fuse && fuse_rrcs && chain_sends) fuse_chain_sends(P, rp, deps, post);
     // flatten dependency lists; need_done: referenced by some (post-)dependency
     for (size_t i = 0; i < rp.steps.size(); ++i) {
       KStep& ks = rp.steps[i];

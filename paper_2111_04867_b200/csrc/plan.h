@@ -19,6 +19,7 @@ struct RankPlan {
 
 // `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables);
 // `fuse_rrcs`: fuse rrc + send-of-its-result into one pass (env TACCL_NO_RRCS=1 disables).
-std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs);
+// `chain_sends`: fuse the sends of a chain's result into the chain (fuse_chain_sends).
+std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends);
 
 }  // namespace taccl

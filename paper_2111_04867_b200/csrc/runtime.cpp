@@ -57,6 +57,7 @@ struct Algo {
   uint64_t min_bytes, max_bytes;
   int max_scratch_chunks = 0, max_stage_chunks = 0, max_stage2_chunks = 0, max_steps_cnt = 1;
   std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
+  std::vector<DevPlan> plans_ll;  // the same program planned for the LL kernel (chain sends fused)
   std::vector<int> ntb;         // per rank
   std::vector<std::vector<int>> weights;  // per rank, per tb
   std::vector<std::vector<int>> indep;    // per rank, per tb
@@ -326,7 +327,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
     KRank& R = A.r[i];
-    const DevPlan& dp = a->plans[r];
+    const DevPlan& dp = G.staged ? a->plans_ll[r] : a->plans[r];
     R.plan = (const char*)dp.mem;
     R.plan_bytes = dp.bytes;
     R.steps_off = dp.steps_off;
@@ -553,6 +554,8 @@ taccl_result_t taccl_comm_destroy(void) {
   for (Algo* a : g.algos) {
     for (auto& p : a->plans)
       if (p.mem) cudaFree(p.mem);
+    for (auto& p : a->plans_ll)
+      if (p.mem) cudaFree(p.mem);
     delete a;
   }
   for (auto& kv : g.ipc_open) cudaIpcCloseMemHandle(kv.second);
@@ -618,7 +621,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
   if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
   if (!text) return fail(TACCL_ERR_INVALID_ARG, "null text");
   std::unique_ptr<Algo> a(new Algo);
-  std::vector<RankPlan> plans;
+  std::vector<RankPlan> plans, plans_ll;
   try {
     Program P = parse_ef(text, len);
     check_program(P, true);
@@ -632,7 +635,11 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
       }
     }
     if (P.instances > kMaxSplit) return fail(TACCL_ERR_UNSUPPORTED, "instances > TACCL_MAX_SPLIT");
-    plans = build_plans(P, env_size("TACCL_NO_FUSE", 0) == 0, env_size("TACCL_NO_RRCS", 0) == 0);
+    const bool fuse = env_size("TACCL_NO_FUSE", 0) == 0, rrcs = env_size("TACCL_NO_RRCS", 0) == 0;
+    // chain-send fusion pays off in the LL kernel (one step less per hop) but not in the
+    // direct kernel (profiles/r01_chain_sends_ll_n4.txt): two plans, picked per call
+    plans = build_plans(P, fuse, rrcs, env_size("TACCL_CHAIN_SENDS", 0) != 0);
+    plans_ll = build_plans(P, fuse, rrcs, env_size("TACCL_NO_CHAIN_SENDS_LL", 0) == 0);
     a->name = P.name;
     a->coll = P.coll;
     a->nranks = P.nranks;
@@ -644,6 +651,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     return fail(TACCL_ERR_INVALID_SCHEDULE, e.kind + ": " + e.msg);
   }
   a->plans.assign(a->nranks, DevPlan());
+  a->plans_ll.assign(a->nranks, DevPlan());
   a->ntb.assign(a->nranks, 0);
   for (int r = 0; r < a->nranks; ++r) {
     a->ntb[r] = (int)plans[r].tbs.size();
@@ -662,6 +670,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->fused_chains += plans[r].fused_chains;
     if (g.emulated || r == g.rank) {
       taccl_result_t rc = upload(plans[r], &a->plans[r]);
+      if (!rc) rc = upload(plans_ll[r], &a->plans_ll[r]);
       if (rc) return rc;
     }
   }
@@ -675,6 +684,8 @@ taccl_result_t taccl_free(taccl_algo_t algo) {
   auto it = std::find(g.algos.begin(), g.algos.end(), (Algo*)algo);
   if (it == g.algos.end()) return fail(TACCL_ERR_INVALID_ARG, "unknown algorithm");
   for (auto& p : (*it)->plans)
+    if (p.mem) cudaFree(p.mem);
+  for (auto& p : (*it)->plans_ll)
     if (p.mem) cudaFree(p.mem);
   delete *it;
   g.algos.erase(it);

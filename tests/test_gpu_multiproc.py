@@ -115,3 +115,52 @@ def test_multiprocess_parity(n):
     for rank, results, err in sorted(res, key=lambda x: x[0]):
         assert err is None, f"rank {rank}: {err}"
         assert all(results), f"rank {rank}: failing cases {[c for c, ok in zip(CASES, results) if not ok]}"
+
+
+def _timeout_worker(rank, n, port, q):
+    import torch.distributed as dist
+    from paper_2111_04867_b200 import taccl
+    from paper_2111_04867_b200.generator import generate
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TACCL_TIMEOUT_S="1")
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    try:
+        comm = taccl.Comm(rank=rank, nranks=n, device=rank, scratch_bytes=16 << 20)
+        comm.load(generate("allgather", "direct", n, 1, 1))
+        x = torch.ones(1 << 16, dtype=torch.int32, device="cuda")
+        out = torch.empty(n << 16, dtype=torch.int32, device="cuda")
+        comm.register(out)
+        code = None
+        if rank == 0:  # rank 1 never joins the call: rank 0's waits must time out, not hang
+            comm.run("allgather", out, x)
+            torch.cuda.synchronize()
+            try:
+                comm.check()
+            except taccl.TacclError as e:
+                code = e.code
+        dist.barrier()
+        comm.destroy()
+        q.put((rank, code, None))
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_watchdog_timeout_surfaces():
+    # a peer that never issues the call: the device watchdog (%globaltimer, TACCL_TIMEOUT_S)
+    # ends every spin and taccl_check reports TACCL_ERR_TIMEOUT (6)
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][2] is None and res[1][2] is None, res
+    assert res[0][1] == 6
