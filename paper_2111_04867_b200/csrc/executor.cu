@@ -327,25 +327,6 @@ __device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
 __device__ __forceinline__ void st_volatile_v4(void* p, uint4 v) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
-// wait until line p carries `flag` in both flag words; false on timeout
-__device__ __forceinline__ bool ll_wait(const char* p, unsigned flag, uint4* out, u64 timeout_ns) {
-  uint4 v = ld_volatile_v4(p);
-  if (v.y == flag && v.w == flag) {
-    *out = v;
-    return true;
-  }
-  const u64 t0 = globaltimer();
-  for (;;) {
-    for (int i = 0; i < 64; ++i) {
-      v = ld_volatile_v4(p);
-      if (v.y == flag && v.w == flag) {
-        *out = v;
-        return true;
-      }
-    }
-    if (globaltimer() - t0 > timeout_ns) return false;
-  }
-}
 // nb payload bytes at p (any alignment; nb <= 8) <-> one u64 (little-endian byte order)
 __device__ __forceinline__ u64 ld_bytes(const char* p, int nb) {
   if (nb == 8 && ((uintptr_t)p & 7) == 0) return __ldcg(reinterpret_cast<const unsigned long long*>(p));
@@ -391,7 +372,9 @@ constexpr int kLLU = 2;
 __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src, char* dst, const char* const* ins,
                                          int nin, char* const* fwd, int nfwd, int64_t cb, int64_t llcb, int cnt,
                                          int64_t l0, int64_t l1,
-                                         unsigned flag, u64 timeout_ns) {
+                                         unsigned flag, u64 timeout_ns, u64* ft = nullptr) {
+  // ft (TACCL_TRACE_FINE builds only): thread 0's stamps after its first batch's loads were
+  // issued, after its waits, after its stores
   const unsigned m = (unsigned)(l1 - l0), total = m * (unsigned)cnt, nt = blockDim.x;
   for (unsigned base = threadIdx.x; base < total; base += kLLU * nt) {
     int64_t pb[kLLU], lb[kLLU];
@@ -411,6 +394,9 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
       for (int i = 0; i < kMaxRanks; ++i)
         if (i < nin && vb[u]) w[u][i] = ld_volatile_v4(ins[i] + lb[u]);
     }
+#ifdef TACCL_TRACE_FINE
+    if (ft && base == threadIdx.x) ft[0] = globaltimer();
+#endif
     // wait for every line of the batch: re-poll the ones not yet valid, all in one loop
     u64 t0 = 0;
     for (int it = 0;; ++it) {
@@ -430,6 +416,9 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
         else if (now - t0 > timeout_ns) return false;
       }
     }
+#ifdef TACCL_TRACE_FINE
+    if (ft && base == threadIdx.x) ft[1] = globaltimer();
+#endif
 #pragma unroll
     for (int u = 0; u < kLLU; ++u) {
       if (!reduce) {
@@ -471,6 +460,9 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
       if (dst) st_bytes(dst + pb[u], v[u], vb[u]);
       for (int f = 0; f < nfwd; ++f) st_volatile_v4(fwd[f] + lb[u], ll_line(v[u], flag));
     }
+#ifdef TACCL_TRACE_FINE
+    if (ft && base == threadIdx.x) ft[2] = globaltimer();
+#endif
   }
   return true;
 }
@@ -638,6 +630,55 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       const KStep& st = steps[tb.step_begin + k];
       const bool tr = trace && j == c0 && k < kTraceSteps;
       if (tr) trace[2 + 4 * k] = globaltimer();
+      // LL fast path: a step with nothing to wait for needs no thread-0 pre-phase and no
+      // barrier before its data work — every thread derives its slot pointers itself
+      const bool fast = LL && st.dep_count == 0 &&
+                        (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RCS ||
+                         st.op == K_RRC_FUSED);
+      if (fast) {
+        if (tr) trace[3 + 4 * k] = trace[2 + 4 * k];  // nothing to wait for
+        const bool fz = st.op == K_RRC_FUSED;
+        const char* ins[kMaxRanks];
+        char* fws[kMaxRanks];
+        int nin = 0, nfw = 0;
+        if (fz) {  // the chain members' slots (chain order) and the fused sends' slots
+#pragma unroll
+          for (int f = 0; f < kMaxRanks; ++f)
+            if (f < st.fuse_count) ins[f] = my_staged + (int64_t)fused[4 * (st.fuse_begin + f) + 3] * ll_cb;
+#pragma unroll
+          for (int f = 0; f < kMaxRanks; ++f)
+            if (f < st.fwd_count) {
+              const int* fw = fused + st.fwd_begin + 6 * f;
+              fws[f] = R.peer_arena[fw[0]] + parity_off + (int64_t)fw[4] * ll_cb;
+            }
+          nin = st.fuse_count;
+          nfw = st.fwd_count;
+        } else {
+          ins[0] = my_staged + (int64_t)st.soff2 * ll_cb;
+          nin = st.op == K_SEND ? 0 : 1;
+          if (!(st.op == K_RECV || st.op == K_RRC)) {
+            fws[0] = R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * ll_cb;
+            nfw = 1;
+          }
+        }
+        const int64_t nl = (cbytes + 7) / 8;
+        int64_t l0 = (int64_t)((unsigned)nl * (unsigned)j / (unsigned)nsplit);
+        int64_t l1 = (int64_t)((unsigned)nl * (unsigned)(j + 1) / (unsigned)nsplit);
+        if (fz) {  // this member's portion of the piece
+          const int64_t m = l1 - l0, a0 = l0;
+          l0 = a0 + m * st.part / st.nparts;
+          l1 = a0 + m * (st.part + 1) / st.nparts;
+        }
+        const char* src = (st.op == K_RECV || st.op == K_RCS) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+        char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+        const bool ok = ll_lines(A.dtype, st.op == K_RRC || st.op == K_RRCS || fz, src, dst, ins, nin, fws, nfw, cbytes,
+                                 ll_cb, st.cnt, l0, l1, ll_flag, A.timeout_ns);
+        if (tr) trace[4 + 4 * k] = globaltimer();
+        if (__syncthreads_or(!ok)) {
+          if (tid == 0) record_error(c, st.op, k);
+          return;
+        }
+      } else {
       if (tid == 0) {
         bool ok = true;
         for (int d = 0; d < st.dep_count && ok; ++d) {
@@ -698,9 +739,15 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         const int nfwd = (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) ? 1 : st.op == K_RRC_FUSED ? st.fwd_count : 0;
         const bool reduce = st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED;
         const int nin = st.op == K_SEND ? 0 : st.op == K_RRC_FUSED ? st.fuse_count : 1;
+#ifdef TACCL_TRACE_FINE
+        // fine build: [2+4k] loads issued, [3+4k] waits done, [4+4k] stores issued (thread 0)
+        const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt, l0, l1,
+                                 ll_flag, A.timeout_ns, tr ? trace + 2 + 4 * k : nullptr);
+#else
         const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt, l0, l1,
                                  ll_flag, A.timeout_ns);
         if (tr) trace[4 + 4 * k] = globaltimer();
+#endif
         if (__syncthreads_or(!ok)) {
           if (tid == 0) record_error(c, st.op, k);
           return;
@@ -766,6 +813,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           break;
       }
       __syncthreads();
+      }  // !fast
       if (tid == 0) {
         bool ok = true;  // post-dependencies: the other members of a fused chain
         for (int d = 0; d < st.post_count && ok; ++d) {
