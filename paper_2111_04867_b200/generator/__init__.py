@@ -1,4 +1,4 @@
-"""Offline CPU schedule generator: template and greedy algorithms lowered
+"""Offline CPU schedule generator: template, greedy and MILP algorithms lowered
 to EF v1 text (docs/SCHEDULE.md). Not on the timed path."""
 from .algorithm import Algorithm, Transfer  # noqa: F401
 from .lowering import LoweringError, lower  # noqa: F401
@@ -16,6 +16,9 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
         alg = fn(nranks // 2, chunks, **kw)
     elif algo == "greedy":
         from .greedy import synthesize
+        alg = synthesize(coll, nranks, chunks, **kw)
+    elif algo == "milp":  # the paper's three-stage synthesizer (HiGHS MILPs, milp.py)
+        from .milp import synthesize
         alg = synthesize(coll, nranks, chunks, **kw)
     else:
         alg = templates.TEMPLATES[(coll, algo)](nranks, chunks)

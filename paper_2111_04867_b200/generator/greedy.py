@@ -125,8 +125,9 @@ def route(coll, lt: Topology, sk: Sketch, chunks, chunk_mb):
     return trees
 
 
-def order(lt: Topology, trees, chunk_mb, src_of):
-    """Stage 2 greedy (App. B.2) with the IB contiguity stand-in: returns scheduled transfers
+def order(lt: Topology, trees, chunk_mb, src_of, merge=True):
+    """Stage 2 greedy (App. B.2) with the IB contiguity stand-in (merge=False: one chunk per
+    transfer, the input of the Stage-3 MILP, milp.py): returns scheduled transfers
     [(start, end, chunks, u, v)]."""
     link_t = {l: 0.0 for l in lt.links}
     send_port = {u: 0.0 for u in range(lt.n)}
@@ -166,7 +167,7 @@ def order(lt: Topology, trees, chunk_mb, src_of):
         (start, *_), c, u, v = min(ready)
         link = lt.links[(u, v)]
         group = [(c, u, v)]
-        if link.kind == "ib":
+        if merge and link.kind == "ib":
             # contiguity: everything else waiting for this link that is already available
             # at u by `start` goes in the same transfer (one alpha)
             more = sorted(k for k in ready if k[2] == u and k[3] == v and k[1] != c and avail[(k[1], u)] <= start)

@@ -141,6 +141,28 @@ def test_greedy_schedules_bit_exact(coll, n, p, kw, mode):
         assert_bits_equal(got, oracle.expected_outputs(coll, ins, "bfloat16"))
 
 
+MILP = [("allgather", 8, 2, {}), ("alltoall", 8, 2, {}), ("allgather", 8, 2, {"topology": "2x4", "size": 1 << 16}),
+        ("alltoall", 8, 1, {"topology": "2x4", "size": 1 << 16}), ("allreduce", 4, 2, {}),
+        ("reducescatter", 8, 1, {"topology": "2x4", "size": 1 << 16})]
+
+
+@pytest.mark.parametrize("coll,n,p,kw", MILP)
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_milp_schedules_bit_exact(coll, n, p, kw, mode):
+    """The three-stage MILP synthesizer's schedules (generator/milp.py; chunks the Stage-3
+    MILP sends together become cnt > 1 steps) run bit-exactly."""
+    text = generate(coll, "milp", n, p, 1, **kw)
+    count = p * 997 if coll == "allgather" else n * p * 997
+    if coll in ("allreduce", "reducescatter"):
+        ins = [allreduce_input(count, "int32", "bits", 12, r) for r in range(n)]
+        got = run_gpu(text, coll, n, "int32", ins, mode=mode)
+        assert_bits_equal(got, oracle.expected_outputs(coll, ins, "int32"))
+    else:
+        ins = bits_inputs(coll, n, count, "bfloat16", 13)
+        got = run_gpu(text, coll, n, "bfloat16", ins, mode=mode)
+        assert_bits_equal(got, oracle.expected_outputs(coll, ins, "bfloat16"))
+
+
 # ---------------------------------------------------------------- AR
 
 AR = [

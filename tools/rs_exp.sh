@@ -1,0 +1,20 @@
+#!/bin/bash
+# RS large-message experiment at n GPUs (under gpurun --gpus n): paired vs split
+# threadblocks, lanes (pieces per CTA), CTA targets. usage: bash tools/rs_exp.sh N TAG
+n=$1; tag=${2:-rs}
+mkdir -p gpurun_out
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29541"
+out=gpurun_out/rs_exp_n${n}_$tag.txt; : > $out
+for env in "" "TACCL_LANES=256" "TACCL_LANES=512" "TACCL_TARGET_CTAS=148" "TACCL_TARGET_CTAS=148 TACCL_LANES=512"; do
+  echo "== env: $env" >> $out
+  rm -f gpurun_out/rs_tmp.jsonl
+  env $env timeout 300 $TR tools/sweep.py --colls ${COLLS:-reducescatter} --size-lo 24 --size-hi 30 --graph --no-nccl \
+     --algos ${ALGOS:-direct,direct_split,direct_m4_split} --out gpurun_out/rs_tmp.jsonl > gpurun_out/rs_tmp.log 2>&1 || tail -5 gpurun_out/rs_tmp.log >> $out
+  python - >> $out <<'PY'
+import json
+for l in open("gpurun_out/rs_tmp.jsonl"):
+    r = json.loads(l)
+    print(r["coll"], r["S"], " ".join(f'{k[6:-6]}={v:.0f}' for k, v in r.items() if k.startswith("taccl_") and k.endswith("_busbw")))
+PY
+done
+cat $out

@@ -32,14 +32,12 @@ def gen(coll, al, n):
     if al == "auto":  # the size-specialised default set (generator/tuned.py)
         from paper_2111_04867_b200.generator.tuned import default_schedules
         return default_schedules(coll, n)
-    """algorithm name -> EF text; suffix _split = sends and receives in separate threadblocks"""
-    if al.endswith("_split"):
-        return generate(coll, al[:-6], n, 1, 1, pair=False)
-    # name_pP_mM: chunks per rank P, instances M (PAPER.md:702-711, 785-789)
+    """algorithm name -> EF text. name[_pP][_mM][_split]: chunks per rank P, instances M
+    (PAPER.md:702-711, 785-789); _split = sends and receives in separate threadblocks"""
     parts = al.split("_")
-    p = next((int(x[1:]) for x in parts[1:] if x.startswith("p")), 1)
-    m = next((int(x[1:]) for x in parts[1:] if x.startswith("m")), 1)
-    return generate(coll, parts[0], n, p, m)
+    p = next((int(x[1:]) for x in parts[1:] if x[:1] == "p" and x[1:].isdigit()), 1)
+    m = next((int(x[1:]) for x in parts[1:] if x[:1] == "m" and x[1:].isdigit()), 1)
+    return generate(coll, parts[0], n, p, m, pair="split" not in parts[1:])
 
 
 def factor(coll, n):
