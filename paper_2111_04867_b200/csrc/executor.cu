@@ -531,6 +531,15 @@ __device__ void record_error(const Ctx& c, int what, int step) {
   }
 }
 
+__device__ __forceinline__ void st_release_sys(u64* p, u64 v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// a send the receiver loads in place (pull mode; direct kernel only): it reads this rank's
+// input and the plan marked its matched receive-reduce as reading it in place (st.poff >= 0)
+__device__ __forceinline__ bool pulled(const KArgs& A, const KStep& st) {
+  return A.pull && st.op == K_SEND && st.poff >= 0;
+}
+
 // LL = staged (small-message) mode, a compile-time specialisation so each variant carries
 // only its own data path (register pressure: the LL variant inlines its line loop).
 template <bool LL>
@@ -644,7 +653,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         if (fz) {  // the chain members' slots (chain order) and the fused sends' slots
 #pragma unroll
           for (int f = 0; f < kMaxRanks; ++f)
-            if (f < st.fuse_count) ins[f] = my_staged + (int64_t)fused[4 * (st.fuse_begin + f) + 3] * ll_cb;
+            if (f < st.fuse_count) ins[f] = my_staged + (int64_t)fused[kFuseStride * (st.fuse_begin + f) + 3] * ll_cb;
 #pragma unroll
           for (int f = 0; f < kMaxRanks; ++f)
             if (f < st.fwd_count) {
@@ -685,7 +694,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           const int dt = deps[2 * (st.dep_begin + d)], dk = deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
-        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) && !sender_ready) {
+        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) && !sender_ready && !pulled(A, st)) {
           ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
           sender_ready = true;
         }
@@ -694,14 +703,18 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
         if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
-            const int* fz = fused + 4 * (st.fuse_begin + f);
+            const int* fz = fused + kFuseStride * (st.fuse_begin + f);
             const KTB o = tbs[fz[0]];
             if (!LL) ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
-            s_stage[f] = LL ? my_staged + (int64_t)fz[3] * ll_cb : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
+            s_stage[f] = LL ? my_staged + (int64_t)fz[3] * ll_cb
+                       : (A.pull && fz[4] >= 0) ? R.peer_in[o.recv] + (int64_t)fz[4] * cbytes  // pull: in place
+                                                 : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
           }
         }
         if (ok && (st.op == K_RRC || st.op == K_RRCS || st.op == K_RECV || st.op == K_RCS))
-          s_stage[0] = LL ? my_staged + (int64_t)st.soff2 * ll_cb : local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
+          s_stage[0] = LL ? my_staged + (int64_t)st.soff2 * ll_cb
+                     : (A.pull && st.poff >= 0) ? R.peer_in[tb.recv] + (int64_t)st.poff * cbytes  // pull: in place
+                                                : local_base(c, KB_STAGE) + (int64_t)st.soff * cbytes;
         if (ok && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS))
           s_fwd[0] = LL ? R.peer_arena[tb.send] + parity_off + (int64_t)st.roff2 * ll_cb
                         : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
@@ -761,6 +774,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       } else switch (st.op) {
         case K_SEND:
         case K_CPY: {
+          if (pulled(A, st)) break;  // the receiver loads it in place (pull mode)
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = st.op == K_CPY ? local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes
                                      : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
@@ -824,6 +838,23 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           record_error(c, st.op, k);
           s_abort = 1;
         }
+        // pull mode: the reader acks the sender once its loads of the sender's input are done
+        // (bar.sync above; release orders them) — a fused chain's last member acks every input
+        // after the post-dependencies covered the other members' portions
+        if (ok && !LL && A.pull) {
+          if ((st.op == K_RRC || st.op == K_RRCS) && st.poff >= 0) {
+            u64* ack = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffAck);
+            st_release_sys(ack + flag_slot(R.rank, tb.chan, j), E | (u64)(st.seq + 1));
+          } else if (st.op == K_RRC_FUSED && st.part + 1 == st.nparts) {
+            for (int f = 0; f < st.fuse_count; ++f) {
+              const int* fz = fused + kFuseStride * (st.fuse_begin + f);
+              if (fz[4] < 0) continue;
+              const KTB o = tbs[fz[0]];
+              u64* ack = reinterpret_cast<u64*>(R.peer_arena[o.recv] + kOffAck);
+              st_release_sys(ack + flag_slot(R.rank, o.chan, j), E | (u64)(fz[1] + 1));
+            }
+          }
+        }
         if (!LL && st.op == K_RRC_FUSED && st.fwd_count)  // this member's peer stores, before its
           asm volatile("fence.acq_rel.sys;" ::: "memory");  // done flag (a K_PUB acquires it)
         if (!LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_PUB || st.op == K_RCS)) {
@@ -843,6 +874,21 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         if (s_abort) return;
       }
     }
+  }
+  // pull mode: this CTA's pulled sends are complete once their readers acked (the caller may
+  // reuse the input after the call). Waited here, after every piece, so no reader can be
+  // waiting on this CTA (its data flags were published at the sends' places).
+  if (!LL && A.pull && tid == 0 && tb.send >= 0) {
+    const u64* ack = reinterpret_cast<const u64*>(R.arena + kOffAck);
+    for (int j = c0; j < nsplit; j += ct)
+      for (int k = 0; k < tb.nsteps; ++k) {
+        const KStep& st = steps[tb.step_begin + k];
+        if (pulled(A, st) && !wait_ge<true>(ack + flag_slot(tb.send, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns)) {
+          record_error(c, st.op, k);
+          j = nsplit;
+          break;
+        }
+      }
   }
   // completion: the rank's CTA 0 advances the rank's epoch for the next call once all other
   // CTAs of the rank have arrived (read this call's epoch) — by now they normally have, so

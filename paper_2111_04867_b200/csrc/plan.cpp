@@ -94,13 +94,10 @@ void fuse_chains(const Gpu& g, const HB& hb, const std::map<std::pair<int, int>,
     const int K = (int)chain.size();
     std::vector<std::pair<int, int>> head_in = first.deps;
     if (head.second > 0) head_in.emplace_back(head.first, head.second - 1);
-    const int fb = (int32_t)rp.fused.size() / 4;
+    const int fb = (int32_t)rp.fused.size() / kFuseStride;
     for (int i = 0; i < K; ++i) {
       const KStep& x = rp.steps[flat.at(chain[i])];
-      rp.fused.push_back(chain[i].first);
-      rp.fused.push_back(x.seq);
-      rp.fused.push_back(x.soff);
-      rp.fused.push_back(x.soff2);
+      for (int v : {chain[i].first, x.seq, x.soff, x.soff2, x.poff}) rp.fused.push_back(v);
     }
     for (int i = 0; i < K; ++i) {
       const int fi = flat.at(chain[i]);
@@ -231,6 +228,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
       rp.tbs.push_back(kt);
       for (const Step& st : tb.steps) {
         KStep ks{};
+        ks.poff = -1;
         ks.srcbuf = st.srcbuf == B_NONE ? 0 : kbuf(st.srcbuf);
         ks.dstbuf = st.dstbuf == B_NONE ? 0 : kbuf(st.dstbuf);
         ks.srcoff = st.srcoff;
@@ -265,12 +263,20 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
             ks.seq = seq[{g.id, tb.id, st.s}];
             ks.soff2 = soff2[{g.id, tb.id, st.s}];
             break;
-          case ST_RRC:
+          case ST_RRC: {
             ks.op = K_RRC;
             ks.seq = seq[{g.id, tb.id, st.s}];
             ks.soff = soff[{g.id, tb.id, st.s}];
             ks.soff2 = soff2[{g.id, tb.id, st.s}];
+            // matched send: the seq-th send of the peer's tb for (send=g.id, chan); pull mode
+            // reads its source in place when it is the peer's input (read-only, valid from the
+            // peer's call entry, reading R1)
+            for (const TB& ptb : P.gpus[tb.recv].tbs)
+              if (ptb.send == g.id && ptb.chan == tb.chan)
+                for (const Step& ps : ptb.steps)
+                  if (ps.type == ST_S && seq[{tb.recv, ptb.id, ps.s}] == ks.seq && ps.srcbuf == B_I) ks.poff = ps.srcoff;
             break;
+          }
           case ST_CPY: ks.op = K_CPY; break;
           default: ks.op = K_NOP; break;
         }
@@ -279,6 +285,18 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
       }
     }
     if (fuse) fuse_chains(g, hb, flat, rp, deps, post);
+    // pull mode acks are "read up to message seq" per connection, so they must be written in
+    // message order: a chain's inputs are acked by its last member, which may run after a later
+    // receive of a member's own threadblock acked — such chains keep the push path
+    for (const KTB& kt : rp.tbs)
+      for (int k = 0; k < kt.nsteps; ++k) {
+        const KStep& x = rp.steps[kt.step_begin + k];
+        if (x.op != K_RRC_FUSED) continue;
+        bool later = false;
+        for (int k2 = k + 1; k2 < kt.nsteps; ++k2) later = later || rp.steps[kt.step_begin + k2].poff >= 0;
+        if (later)
+          for (int f = 0; f < x.fuse_count; ++f) rp.fused[kFuseStride * (x.fuse_begin + f) + 4] = -1;
+      }
     // chain_sends: the LL kernel's plan (-10% time for LL direct AR at n=4); the direct kernel
     // only with TACCL_CHAIN_SENDS=1 (+12% at >= 256 MiB, -10% at 2-32 MiB;
     // profiles/r01_chain_sends_n4.txt, r01_chain_sends_ll_n4.txt)
@@ -343,6 +361,28 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
     rp.fused_chains = (int)std::count_if(rp.steps.begin(), rp.steps.end(),
                                          [](const KStep& k) { return k.op == K_RRC_FUSED && k.part == 0; });
   }
+  // a send is pulled (pull mode: no push, the receiver loads it in place) exactly when its
+  // matched receive's final plan reads it in place; both sides must agree
+  for (int r = 0; r < n; ++r)
+    for (const KTB& kt : plans[r].tbs)
+      for (int k = 0; k < kt.nsteps; ++k) {
+        KStep& x = plans[r].steps[kt.step_begin + k];
+        if (x.op != K_SEND) continue;
+        x.poff = -1;
+        const RankPlan& pp = plans[kt.send];
+        for (const KTB& pt : pp.tbs) {
+          if (pt.recv != r || pt.chan != kt.chan) continue;
+          for (int q = 0; q < pt.nsteps; ++q) {
+            const KStep& y = pp.steps[pt.step_begin + q];
+            if (y.seq != x.seq) continue;
+            if (y.op == K_RRC || y.op == K_RRCS) x.poff = y.poff;
+            else if (y.op == K_RRC_FUSED) x.poff = pp.fused[kFuseStride * (y.fuse_begin + y.part) + 4];
+            else if (y.op == K_RECV || y.op == K_RCS) x.poff = -1;
+            else continue;
+            break;
+          }
+        }
+      }
   return plans;
 }
 

@@ -304,7 +304,8 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
 
 taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int elt,
                       const std::vector<int>& ranks, const void* const* sends, void* const* recvs,
-                      char* const (*peer_out)[kMaxRanks], void* stream) {
+                      char* const (*peer_out)[kMaxRanks], void* stream,
+                      const char* const (*peer_in)[kMaxRanks] = nullptr) {
   KArgs A;
   memset(&A, 0, sizeof(A));
   A.nlocal = (int)ranks.size();
@@ -340,6 +341,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     for (int q = 0; q < g.nranks; ++q) {
       R.peer_out[q] = peer_out[i][q];
       R.peer_arena[q] = g.peer_arena[q];
+      R.peer_in[q] = peer_in ? peer_in[i][q] : nullptr;
     }
     R.rank = r;
     R.ntb = dp.ntb;
@@ -360,6 +362,15 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.plan_smem = smem <= kPlanSmemMax ? 1 : 0;
   A.tma = (int)env_size("TACCL_TMA", 1);
   A.ready_per_piece = (int)env_size("TACCL_READY_PER_PIECE", 0);
+  // pull mode needs every peer's input mapped (registered, or in the symmetric arena) and
+  // the direct kernel; TACCL_PULL=0 disables it
+  // Default: ReduceScatter only — measured at n=2 (profiles/r01_pull_n2.txt), pull takes RS
+  // from 497 to 642 GB/s busbw at 1 GiB (one pass instead of push + staged reduce) but costs
+  // AR 689 -> 663 (its push path already fuses the reduce with the next push, and peer loads
+  // stream slower than peer stores: 668 vs 705 GB/s, profiles/r01_p2p_probe.txt)
+  const size_t pull_env = env_size("TACCL_PULL", 2);  // 0 off, 1 on, 2 default
+  const bool pull_want = pull_env == 2 ? a->coll == C_RS : pull_env != 0;
+  A.pull = (peer_in && !G.staged && g.nranks > 1 && pull_want) ? 1 : 0;
   std::string err;
   const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -424,10 +435,28 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
   } else {
     peer_out[0][0] = (char*)recvbuf;
   }
+  // pull mode: peers' inputs, when the input is inside a registered buffer or the arena
+  // (host runs); an in-place call's private input copy is not symmetric -> no pull
+  const char* peer_in[1][kMaxRanks] = {};
+  bool have_in = false;
+  if (n > 1 && !overlapping) {
+    const char* sb = (const char*)sendbuf;
+    if (sb >= g.peer_arena[g.rank] && sb + ib <= g.peer_arena[g.rank] + g.arena_bytes) {
+      for (int q = 0; q < n; ++q) peer_in[0][q] = g.peer_arena[q] + (sb - g.peer_arena[g.rank]);
+      have_in = true;
+    } else {
+      for (const Reg& rg : g.regs)
+        if ((uintptr_t)sb >= rg.lo && (uintptr_t)sb + ib <= rg.hi) {
+          for (int q = 0; q < n; ++q) peer_in[0][q] = rg.peer_base[q] + ((uintptr_t)sb - rg.lo);
+          have_in = true;
+          break;
+        }
+    }
+  }
   std::vector<int> ranks{g.rank};
   const void* s[1] = {sendbuf};
   void* r[1] = {recvbuf};
-  return launch(a, G, dtype, elt, ranks, s, r, peer_out, stream);
+  return launch(a, G, dtype, elt, ranks, s, r, peer_out, stream, have_in ? peer_in : nullptr);
 }
 
 taccl_result_t upload(const RankPlan& rp, DevPlan* dp) {
@@ -711,12 +740,16 @@ taccl_result_t taccl_run_emulated(taccl_coll_t coll, const void* const* sendbufs
   if ((rc = geometry(a, coll, count, elt, n, 0, &G))) return rc;
   std::vector<int> ranks(n);
   char* peer_out[kMaxRanks][kMaxRanks] = {};
+  const char* peer_in[kMaxRanks][kMaxRanks] = {};
   for (int r = 0; r < n; ++r) {
     ranks[r] = r;
     if (!sendbufs[r] || !recvbufs[r]) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
-    for (int q = 0; q < n; ++q) peer_out[r][q] = (char*)recvbufs[q];
+    for (int q = 0; q < n; ++q) {
+      peer_out[r][q] = (char*)recvbufs[q];
+      peer_in[r][q] = (const char*)sendbufs[q];
+    }
   }
-  return launch(a, G, dtype, elt, ranks, sendbufs, recvbufs, peer_out, stream);
+  return launch(a, G, dtype, elt, ranks, sendbufs, recvbufs, peer_out, stream, peer_in);
 }
 
 taccl_result_t taccl_run_host(taccl_coll_t coll, const void* host_send, void* host_recv, size_t count,

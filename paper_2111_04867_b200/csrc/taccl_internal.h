@@ -106,7 +106,12 @@ struct KStep {
   int32_t need_done;      // some step depends on this one
   int32_t fwd_begin, fwd_count;  // K_RRC_FUSED: forward destinations (ints in the fused array:
                                  // peer, chan, rbuf, roff, roff2, seq per entry)
+  int32_t poff;           // receive-reduces whose matched send reads the sender's input: that
+                          // send's input offset (chunk units), else -1 (pull mode reads it in
+                          // place); K_SEND: >= 0 iff its matched receive reads it in place
 };
+// K_RRC_FUSED member entries in the fused array: tb, seq, soff, soff2, poff
+constexpr int kFuseStride = 5;
 
 struct KTB {
   int32_t send, recv, chan;
@@ -125,7 +130,9 @@ constexpr size_t kFlagSlots = (size_t)kMaxRanks * kMaxChan * kMaxSplit;
 constexpr size_t kOffData = 0;                                   // u64[kFlagSlots], written by senders
 constexpr size_t kOffReady = kOffData + kFlagSlots * 8;          // u64[kFlagSlots], written by receivers
 constexpr size_t kOffDone = kOffReady + kFlagSlots * 8;          // u64[kMaxTB*kMaxSplit], local
-constexpr size_t kOffCtrl = kOffDone + (size_t)kMaxTB * kMaxSplit * 8;
+constexpr size_t kOffAck = kOffDone + (size_t)kMaxTB * kMaxSplit * 8;  // u64[kFlagSlots], pull mode:
+                                                                  // written by readers of our input
+constexpr size_t kOffCtrl = kOffAck + kFlagSlots * 8;
 constexpr size_t kCtrlBytes = 256;   // epoch (u64), finished (u32), error (u32), err detail
 constexpr size_t kOffScratch = (kOffCtrl + kCtrlBytes + 4095) & ~(size_t)4095;
 
@@ -160,6 +167,7 @@ struct KRank {
   char* arena;
   char* peer_out[kMaxRanks];    // peer's output buffer (this call's recvbuf on the peer)
   char* peer_arena[kMaxRanks];  // peer's arena (flags, scratch, staging)
+  const char* peer_in[kMaxRanks];  // pull mode: peer's input buffer (this call's sendbuf on the peer)
   int32_t rank, ntb, ncta;  // ncta: CTAs of this rank in the launch
   int32_t budget;          // CTAs of this rank: tb t gets tb_ctas(weight_t, wsum, ...)
   int32_t wsum, pad;
@@ -188,7 +196,10 @@ struct KArgs {
   int32_t trace_ctas;         // CTAs that fit in the trace buffer
   int32_t ncta;               // grid size
   int32_t ready_per_piece;    // A/B knob (TACCL_READY_PER_PIECE): entry handshake per piece start
-  int32_t pad3;
+  int32_t pull;               // pull mode (direct kernel): a receive-reduce whose matched send
+                              // reads the sender's input loads it from the peer (no push, no
+                              // staging); the reader acks, the sender's CTAs wait for the acks
+                              // before they exit (its input may be reused after the call)
   uint32_t cta_map[256];      // per CTA: local rank, tb, first piece, CTAs of the tb (cta_pack)
 };
 constexpr int kMaxGrid = 256;

@@ -148,7 +148,8 @@ class Comm:
         _check(lib().taccl_free(h))
 
     def register(self, t):
-        """Collective: make tensor `t`'s storage a zero-copy receive target on every rank."""
+        """Collective: map tensor `t`'s storage on every rank — a zero-copy receive target
+        (outputs) or an in-place pull source (inputs, pull mode)."""
         if self.emulated or self.nranks == 1:
             return
         key = (t.untyped_storage().data_ptr(), t.untyped_storage().nbytes())
@@ -168,6 +169,7 @@ class Comm:
         n = self.nranks
         count = inp.numel() // n if c in (ALLTOALL, REDUCESCATTER) else inp.numel()
         self.register(out)
+        self.register(inp)
         _check(lib().taccl_run(c, ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                count, dtype_code(inp, c), _stream(stream)))
 

@@ -95,6 +95,9 @@ CASES = [
     ("allgather", "direct", 1, 1, "bfloat16", 3, None),
     ("reducescatter", "direct", 1, 1, "float32", 1 << 17, "intval"),
     ("reducescatter", "ring", 2, 2, "int32", 2 * 3001, "bits"),
+    # above the LL threshold: the direct kernel in pull mode (inputs registered by comm.run)
+    ("reducescatter", "direct", 1, 1, "bfloat16", 3 << 20, "intval"),
+    ("reducescatter", "direct", 2, 2, "int32", 2 * 600007, "bits"),
 ]
 
 
@@ -130,6 +133,7 @@ def _timeout_worker(rank, n, port, q):
         x = torch.ones(1 << 16, dtype=torch.int32, device="cuda")
         out = torch.empty(n << 16, dtype=torch.int32, device="cuda")
         comm.register(out)
+        comm.register(x)  # registration is collective (comm.run registers inputs too)
         code = None
         if rank == 0:  # rank 1 never joins the call: rank 0's waits must time out, not hang
             comm.run("allgather", out, x)

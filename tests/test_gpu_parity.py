@@ -38,7 +38,9 @@ def to_host(t, dtype, like):
 MODES = {"direct": "0", "staged": str(1 << 40)}  # TACCL_STAGED_MAX: zero-copy vs staged mode
 
 
-def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20, mode=None):
+def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20, mode=None, pull=None):
+    if pull is not None:  # pull mode (default on): receive-reduces load peers' inputs in place
+        os.environ["TACCL_PULL"] = str(int(pull))
     if lanes:
         os.environ["TACCL_LANES"] = str(lanes)
     if mode:
@@ -59,6 +61,7 @@ def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20, mode=None):
         comm.destroy()
         os.environ.pop("TACCL_LANES", None)
         os.environ.pop("TACCL_STAGED_MAX", None)
+        os.environ.pop("TACCL_PULL", None)
 
 
 def bits_inputs(coll, n, count, dtype, cfg):
@@ -174,13 +177,15 @@ AR = [
 
 @pytest.mark.parametrize("algo,n,p,m", AR)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["direct", "staged"])
+@pytest.mark.parametrize("mode", ["direct", "staged", "push"])
 def test_allreduce_exact(algo, n, p, m, dtype, mode):
+    # direct = zero-copy kernel (pull mode on: rrcs fed by a peer's input load it in place);
+    # push = the same kernel with pull off (sends push into the receiver's rrc staging)
     count = n * p * 1013 if dtype == "bfloat16" else n * p * 2051
     text = generate("allreduce", algo, n, p, m)
     kind = "bits" if dtype == "int32" else "intval"
     ins = [allreduce_input(count, dtype, kind, 4, r) for r in range(n)]
-    got = run_gpu(text, "allreduce", n, dtype, ins, mode=mode)
+    got = run_gpu(text, "allreduce", n, dtype, ins, mode="direct" if mode == "push" else mode, pull=mode != "push")
     if dtype == "int32":
         assert_bits_equal(got, oracle.expected_outputs("allreduce", ins, "int32"))
     # integer-valued floats: every order is exact, so the oracle's schedule result is the answer
@@ -251,14 +256,14 @@ RS = [("ring", 2, 1, 1), ("ring", 4, 2, 2), ("ring", 8, 1, 4), ("direct", 2, 1, 
 
 @pytest.mark.parametrize("algo,n,p,m", RS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["direct", "staged"])
+@pytest.mark.parametrize("mode", ["direct", "staged", "push"])
 def test_reducescatter_exact(algo, n, p, m, dtype, mode):
     # ReduceScatter as the inverse of an Allgather; count = elements per rank
     count = p * 1013 if dtype == "bfloat16" else p * 2051
     text = generate("reducescatter", algo, n, p, m)
     kind = "bits" if dtype == "int32" else "intval"
     ins = [allreduce_input(n * count, dtype, kind, 12, r) for r in range(n)]
-    got = run_gpu(text, "reducescatter", n, dtype, ins, mode=mode)
+    got = run_gpu(text, "reducescatter", n, dtype, ins, mode="direct" if mode == "push" else mode, pull=mode != "push")
     if dtype == "int32":
         assert_bits_equal(got, oracle.expected_outputs("reducescatter", ins, "int32"))
     assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))

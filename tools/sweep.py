@@ -133,6 +133,7 @@ def main():
     big_in = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
     big_out = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
     comm.register(big_out)
+    comm.register(big_in)  # pull mode (receive-reduce reads peers' inputs in place)
     stream = torch.cuda.Stream() if a.graph else torch.cuda.current_stream()
     torch.cuda.set_stream(stream)
     tf = (lambda f, st, w: timeit_graph(f, st, w)) if a.graph else timeit
