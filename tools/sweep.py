@@ -139,6 +139,10 @@ def main():
     tf = (lambda f, st, w: timeit_graph(f, st, w)) if a.graph else timeit
 
     def load(t):  # one EF text or a list of them (a size-ranged set)
+        if world > 1:  # every rank runs rank 0's text (a solver need not be bit-deterministic)
+            obj = [t]
+            dist.broadcast_object_list(obj, src=0)
+            t = obj[0]
         return [comm.load(x) for x in t] if isinstance(t, list) else [comm.load(t)]
 
     def free(hs):
