@@ -186,7 +186,7 @@ void fuse_chain_sends(const Program& P, RankPlan& rp, const std::vector<std::vec
   }
 }
 
-std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends) {
+std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends, int pull_kinds) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
   // per-step seq numbers and staging offsets
@@ -341,6 +341,19 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
         }
       }
     }
+    // pull kinds: by default only plain rrcs read in place — measured on B200
+    // (profiles/r01_pull_n2.txt, r01_pull_n4.txt): a plain rrc (RS n=2) goes from push +
+    // serialised reduce to one pass (497 -> 642 GB/s busbw); an rrc fused with its send (AR
+    // n=2) already overlaps its reduce with the forward push and loses (689 -> 663, peer loads
+    // stream slower than stores); fused chains with n-1 remote inputs (RS n=4) lose too
+    for (KStep& x : rp.steps) {
+      const bool keep = (x.op == K_RRC && (pull_kinds & 1)) || (x.op == K_RRCS && (pull_kinds & 2));
+      if (!keep && x.op != K_SEND) x.poff = -1;
+    }
+    if (!(pull_kinds & 4))
+      for (const KStep& x : rp.steps)
+        if (x.op == K_RRC_FUSED)
+          for (int f = 0; f < x.fuse_count; ++f) rp.fused[kFuseStride * (x.fuse_begin + f) + 4] = -1;
     // tb weights: data each tb moves (remote pushes dominate)
     for (KTB& kt : rp.tbs) {
       long long w = 0;

@@ -20,6 +20,8 @@ struct RankPlan {
 // `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables);
 // `fuse_rrcs`: fuse rrc + send-of-its-result into one pass (env TACCL_NO_RRCS=1 disables).
 // `chain_sends`: fuse the sends of a chain's result into the chain (fuse_chain_sends).
-std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends);
+// pull_kinds (pull mode): which receive-reduces may read their input in place —
+// 1 plain rrc, 2 rrc fused with its send (K_RRCS), 4 fused chains
+std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends, int pull_kinds = 1);
 
 }  // namespace taccl

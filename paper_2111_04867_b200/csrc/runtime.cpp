@@ -364,13 +364,9 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.ready_per_piece = (int)env_size("TACCL_READY_PER_PIECE", 0);
   // pull mode needs every peer's input mapped (registered, or in the symmetric arena) and
   // the direct kernel; TACCL_PULL=0 disables it
-  // Default: ReduceScatter only — measured at n=2 (profiles/r01_pull_n2.txt), pull takes RS
-  // from 497 to 642 GB/s busbw at 1 GiB (one pass instead of push + staged reduce) but costs
-  // AR 689 -> 663 (its push path already fuses the reduce with the next push, and peer loads
-  // stream slower than peer stores: 668 vs 705 GB/s, profiles/r01_p2p_probe.txt)
-  const size_t pull_env = env_size("TACCL_PULL", 2);  // 0 off, 1 on, 2 default
-  const bool pull_want = pull_env == 2 ? a->coll == C_RS : pull_env != 0;
-  A.pull = (peer_in && !G.staged && g.nranks > 1 && pull_want) ? 1 : 0;
+  // which receive-reduces pull is decided per step by the plan (TACCL_PULL_KINDS at load,
+  // default plain rrcs only: plan.cpp); TACCL_PULL=0 turns the mode off
+  A.pull = (peer_in && !G.staged && g.nranks > 1 && env_size("TACCL_PULL", 1) != 0) ? 1 : 0;
   std::string err;
   const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -667,7 +663,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     const bool fuse = env_size("TACCL_NO_FUSE", 0) == 0, rrcs = env_size("TACCL_NO_RRCS", 0) == 0;
     // chain-send fusion pays off in the LL kernel (one step less per hop) but not in the
     // direct kernel (profiles/r01_chain_sends_ll_n4.txt): two plans, picked per call
-    plans = build_plans(P, fuse, rrcs, env_size("TACCL_CHAIN_SENDS", 0) != 0);
+    plans = build_plans(P, fuse, rrcs, env_size("TACCL_CHAIN_SENDS", 0) != 0, (int)env_size("TACCL_PULL_KINDS", 1));
     plans_ll = build_plans(P, fuse, rrcs, env_size("TACCL_NO_CHAIN_SENDS_LL", 0) == 0);
     a->name = P.name;
     a->coll = P.coll;

@@ -39,8 +39,9 @@ MODES = {"direct": "0", "staged": str(1 << 40)}  # TACCL_STAGED_MAX: zero-copy v
 
 
 def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20, mode=None, pull=None):
-    if pull is not None:  # pull mode (default on): receive-reduces load peers' inputs in place
-        os.environ["TACCL_PULL"] = str(int(pull))
+    if pull is not None:  # pull mode: receive-reduces load peers' inputs in place; the tests
+        os.environ["TACCL_PULL"] = str(int(pull))  # pull every kind (plain rrc, rrc+send, chains)
+        os.environ["TACCL_PULL_KINDS"] = "7"
     if lanes:
         os.environ["TACCL_LANES"] = str(lanes)
     if mode:
@@ -62,6 +63,7 @@ def run_gpu(text, coll, n, dtype, ins, lanes=None, scratch=64 << 20, mode=None, 
         os.environ.pop("TACCL_LANES", None)
         os.environ.pop("TACCL_STAGED_MAX", None)
         os.environ.pop("TACCL_PULL", None)
+        os.environ.pop("TACCL_PULL_KINDS", None)
 
 
 def bits_inputs(coll, n, count, dtype, cfg):
