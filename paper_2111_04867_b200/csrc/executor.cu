@@ -242,11 +242,91 @@ __device__ __noinline__ void cta_reduce(char* dst, char* const* fwd, int nfwd, c
   }
 }
 
+// NS (1..3) inputs besides src0, known at compile time: every input's loads of an iteration
+// are issued before the first one is consumed, so a thread keeps (NS+1) x RU vectors in flight
+// instead of RU (the generic loop above waits for each input before loading the next). This
+// matters when inputs are peer memory (pull mode: ~us load latency over NVLink). Same
+// association order (src0 + in_0 + in_1 + ...) as the generic loop: identical results.
+template <int DT, int NS>
+__device__ __noinline__ void cta_reduce_n(char* dst, char* const* fwd, int nfwd, const char* src0,
+                                          const char* const* stages, int64_t soff, int64_t nelem) {
+  using E = Elt<DT>;
+  constexpr int V = E::V, RU = NS == 1 ? 4 : 2;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const char* in[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) in[s] = stages[s] + soff;
+  uintptr_t align = (uintptr_t)dst | (uintptr_t)src0;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) align |= (uintptr_t)in[s];
+  for (int f = 0; f < nfwd; ++f) align |= (uintptr_t)(fwd[f] + soff);
+  char* const f0 = nfwd > 0 ? fwd[0] + soff : nullptr;
+  const int64_t nv = (align & 15) ? 0 : nelem / V;
+  int64_t v = tid;
+  for (; v + (int64_t)(RU - 1) * nt < nv; v += (int64_t)RU * nt) {
+    int4 raw[NS + 1][RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) raw[0][u] = ld_cg(reinterpret_cast<const int4*>(src0 + (v + (int64_t)u * nt) * 16));
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int u = 0; u < RU; ++u) raw[s + 1][u] = ld_cg(reinterpret_cast<const int4*>(in[s] + (v + (int64_t)u * nt) * 16));
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      typename E::acc acc[V], x[V];
+      E::unpack(raw[0][u], acc);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        E::unpack(raw[s + 1][u], x);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = E::add(acc[e], x[e]);
+      }
+      const int4 o = E::pack(acc);
+      const int64_t off = (v + (int64_t)u * nt) * 16;
+      st_v4(reinterpret_cast<int4*>(dst + off), o);
+      if (f0) st_v4(reinterpret_cast<int4*>(f0 + off), o);
+      for (int f = 1; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
+    }
+  }
+  // remaining whole vectors (per thread), then the scalar tail — as the generic loop
+  for (; v < nv; v += nt) {
+    const int64_t off = v * 16;
+    typename E::acc acc[V], x[V];
+    E::unpack(ld_cg(reinterpret_cast<const int4*>(src0 + off)), acc);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      E::unpack(ld_cg(reinterpret_cast<const int4*>(in[s] + off)), x);
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] = E::add(acc[e], x[e]);
+    }
+    const int4 o = E::pack(acc);
+    st_v4(reinterpret_cast<int4*>(dst + off), o);
+    if (f0) st_v4(reinterpret_cast<int4*>(f0 + off), o);
+    for (int f = 1; f < nfwd; ++f) st_v4(reinterpret_cast<int4*>(fwd[f] + soff + off), o);
+  }
+  for (int64_t e = nv * V + tid; e < nelem; e += nt) {
+    const int64_t off = e * E::bytes;
+    typename E::acc acc = E::load(src0 + off);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc = E::add(acc, E::load(in[s] + off));
+    E::store(dst + off, acc);
+    for (int f = 0; f < nfwd; ++f) E::store(fwd[f] + soff + off, acc);
+  }
+}
+
 __device__ void reduce_dispatch(int dtype, char* dst, char* const* fwd, int nfwd, const char* src0,
                                 const char* const* stages, int ns, int64_t soff, int64_t nelem) {
-  if (dtype == TACCL_INT32) cta_reduce<TACCL_INT32>(dst, fwd, nfwd, src0, stages, ns, soff, nelem);
-  else if (dtype == TACCL_FLOAT32) cta_reduce<TACCL_FLOAT32>(dst, fwd, nfwd, src0, stages, ns, soff, nelem);
-  else cta_reduce<TACCL_BFLOAT16>(dst, fwd, nfwd, src0, stages, ns, soff, nelem);
+#define TACCL_RED(DT)                                                                   \
+  switch (ns) {                                                                         \
+    case 1: cta_reduce_n<DT, 1>(dst, fwd, nfwd, src0, stages, soff, nelem); break;      \
+    case 2: cta_reduce_n<DT, 2>(dst, fwd, nfwd, src0, stages, soff, nelem); break;      \
+    case 3: cta_reduce_n<DT, 3>(dst, fwd, nfwd, src0, stages, soff, nelem); break;      \
+    default: cta_reduce<DT>(dst, fwd, nfwd, src0, stages, ns, soff, nelem); break;      \
+  }
+  if (dtype == TACCL_INT32) { TACCL_RED(TACCL_INT32) }
+  else if (dtype == TACCL_FLOAT32) { TACCL_RED(TACCL_FLOAT32) }
+  else { TACCL_RED(TACCL_BFLOAT16) }
+#undef TACCL_RED
 }
 
 // ---------------------------------------------------------------- TMA bulk-copy pipeline
