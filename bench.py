@@ -25,6 +25,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import nvlink_counters  # noqa: E402  (NVML only; no GPU work)
 
 GIB = 1 << 30
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -216,6 +218,11 @@ def main():
 
     launches0 = taccl.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phys = local_rank  # NVML index of this rank's GPU
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    if vis and all(x.strip().isdigit() for x in vis.split(",")):
+        phys = int(vis.split(",")[local_rank])
+    nvl0 = nvlink_counters.read(phys) if n > 1 else None
     with Clocks(local_rank) as clk:
         barrier()
         e0.record(stream)
@@ -223,6 +230,7 @@ def main():
             comm.all_gather(out, inp)
         e1.record(stream)
         torch.cuda.synchronize()
+    nvl1 = nvlink_counters.read(phys) if n > 1 else None
     launches = taccl.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     if world > 1:
@@ -249,8 +257,18 @@ def main():
                                "MEASURED_PEAKS.json has no NVLink figure); nominal 900 for context"}
     roof["traffic"] = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path):
+    if n == 1 and os.path.exists(tr_path):  # ncu DRAM bytes per launch (tools/ncu_round.sh)
         roof["traffic"] = json.load(open(tr_path)).get(f"n{n}_{S}")
+    if n > 1 and nvl0 and nvl1:
+        # NVLink payload bytes this GPU transmitted per launch (NVML counters around the timed
+        # region; the ncu recipe cannot capture a multi-rank kernel), max over ranks
+        tx = torch.tensor([(nvl1["tx"] - nvl0["tx"]) / steps, (nvl1["rx"] - nvl0["rx"]) / steps],
+                          dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tx, op=dist.ReduceOp.MAX)
+        roof["traffic"] = round(float(tx[0]))
+        roof["traffic_rx"] = round(float(tx[1]))
+        roof["traffic_source"] = f"NVML NVLink {nvl0['field']} tx/rx bytes per launch, max over ranks (algorithmic {int(S * (n - 1) / n)})"
     roof["kernel"] = "taccl_exec_kernel"
 
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region

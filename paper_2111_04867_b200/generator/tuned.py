@@ -34,9 +34,10 @@ def ranges(coll: str, n: int):
         if n >= 8:
             return [("oneshot", 0, small), ("direct", small, INF)]
         # 2 chunks per rank pipeline the ring's 2(n-1) hops: -10..13% time at >= 128 MiB
-        # (profiles/r01_ar_variants_n4.txt)
-        return [("oneshot", 0, small), ("direct", small, 64 * MiB), ("ring", 64 * MiB, 128 * MiB),
-                ("ring_p2", 128 * MiB, INF)]
+        # (profiles/r01_ar_variants_n4.txt); below 128 MiB the direct schedule (multi-input
+        # reduce with every load in flight) is ahead of the ring (r01_sweep_n4_graph.jsonl:
+        # 64 MiB 183.8 vs 192.6 us)
+        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("ring_p2", 128 * MiB, INF)]
     if coll == "reducescatter":
         if n == 2 or n >= 8:
             return [("direct", 0, INF)]
