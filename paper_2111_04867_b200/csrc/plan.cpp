@@ -92,8 +92,35 @@ void fuse_chains(const Gpu& g, const HB& hb, const std::map<std::pair<int, int>,
     if (!ok) continue;
     // rewrite the members
     const int K = (int)chain.size();
-    std::vector<std::pair<int, int>> head_in = first.deps;
-    if (head.second > 0) head_in.emplace_back(head.first, head.second - 1);
+    // what every member must wait for: the steps that happened before X_1 and conflict with
+    // the chain (write its source or destination, or read its destination), not all of X_1's
+    // incoming edges — a member waiting on X_1's threadblock predecessor (e.g. the send before
+    // an all-pairs reduce-scatter's first rrc) would add a cross-CTA wait that orders nothing
+    // the chain touches. Kept minimal: a conflicting step ordered before another one is implied.
+    std::vector<std::pair<int, int>> head_in;
+    if (getenv("TACCL_CHAIN_OLDDEPS") && atoi(getenv("TACCL_CHAIN_OLDDEPS"))) {  // A/B knob: every incoming edge
+      head_in = first.deps;
+      if (head.second > 0) head_in.emplace_back(head.first, head.second - 1);
+    } else {
+      const int r = g.id;
+      std::vector<std::pair<int, int>> q;
+      for (const TB& tb : g.tbs)
+        for (const Step& st : tb.steps) {
+          if (std::find(chain.begin(), chain.end(), std::make_pair(tb.id, st.s)) != chain.end()) continue;
+          const bool writes_src_or_dst = st.dstbuf != B_NONE &&
+              (overlap(st.dstbuf, st.dstoff, st.cnt, first.srcbuf, first.srcoff, first.cnt) ||
+               overlap(st.dstbuf, st.dstoff, st.cnt, lastst.dstbuf, lastst.dstoff, lastst.cnt));
+          const bool reads_dst = st.srcbuf != B_NONE && overlap(st.srcbuf, st.srcoff, st.cnt, lastst.dstbuf, lastst.dstoff, lastst.cnt);
+          if ((writes_src_or_dst || reads_dst) && hb.before(r, tb.id, st.s, r, head.first, head.second))
+            q.emplace_back(tb.id, st.s);
+        }
+      for (auto a : q) {
+        bool implied = false;
+        for (auto b : q)
+          if (a != b && hb.before(r, a.first, a.second, r, b.first, b.second)) implied = true;
+        if (!implied) head_in.push_back(a);
+      }
+    }
     const int fb = (int32_t)rp.fused.size() / kFuseStride;
     for (int i = 0; i < K; ++i) {
       const KStep& x = rp.steps[flat.at(chain[i])];
@@ -285,6 +312,20 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
       }
     }
     if (fuse) fuse_chains(g, hb, flat, rp, deps, post);
+    // a chain's last member waits for the other members' portions (post-dependencies) only so
+    // that its done flag means "whole result written"; when no step depends on it, the wait is
+    // pure latency (one cross-CTA poll at the end of every small Allreduce/ReduceScatter)
+    {
+      std::vector<char> wanted(rp.steps.size(), 0);
+      for (size_t i = 0; i < rp.steps.size(); ++i)
+        for (auto e : deps[i]) wanted[flat.at(e)] = 1;
+      for (const KTB& kt : rp.tbs)  // a threadblock successor relies on it too (program order)
+        for (int k = 0; k + 1 < kt.nsteps; ++k) wanted[kt.step_begin + k] = 1;
+      for (size_t i = 0; i < rp.steps.size(); ++i)
+        if (!post[i].empty() && !wanted[i] && rp.steps[i].fwd_count == 0 &&
+            !(getenv("TACCL_CHAIN_OLDDEPS") && atoi(getenv("TACCL_CHAIN_OLDDEPS"))))
+          post[i].clear();
+    }
     // pull mode acks are "read up to message seq" per connection, so they must be written in
     // message order: a chain's inputs are acked by its last member, which may run after a later
     // receive of a member's own threadblock acked — such chains keep the push path

@@ -10,13 +10,14 @@ for envc in $ENVS; do
   env=$(echo $envc | tr ',' ' '); [ "$env" = base ] && env=""
   echo "== env: $env" >> $out
   rm -f gpurun_out/rs_tmp.jsonl
-  env $env timeout 300 $TR tools/sweep.py --colls ${COLLS:-reducescatter} --size-lo 24 --size-hi 30 --graph --no-nccl \
+  env $env timeout 300 $TR tools/sweep.py --colls ${COLLS:-reducescatter} --size-lo ${SIZE_LO:-24} --size-hi ${SIZE_HI:-30} --graph --no-nccl \
      --algos ${ALGOS:-direct,direct_split} --out gpurun_out/rs_tmp.jsonl > gpurun_out/rs_tmp.log 2>&1 || tail -5 gpurun_out/rs_tmp.log >> $out
   python - >> $out <<'PY'
 import json
 for l in open("gpurun_out/rs_tmp.jsonl"):
     r = json.loads(l)
-    print(r["coll"], r["S"], " ".join(f'{k[6:-6]}={v:.0f}' for k, v in r.items() if k.startswith("taccl_") and k.endswith("_busbw")))
+    print(r["coll"], r["S"], " ".join(f'{k[6:-6]}={v:.0f}' for k, v in r.items() if k.startswith("taccl_") and k.endswith("_busbw")),
+          "us:", " ".join(f'{k[6:-3]}={v:.1f}' for k, v in r.items() if k.startswith("taccl_") and k.endswith("_us") and "best" not in k))
 PY
 done
 cat $out
