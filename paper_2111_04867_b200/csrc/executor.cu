@@ -586,17 +586,27 @@ __device__ __forceinline__ char* remote_base(const Ctx& c, int peer, int buf) {
 // piece the step is one contiguous range; otherwise every chunk is cut into stripes of
 // A.stripe bytes and piece j owns stripes j, j + split, ... of each chunk, so at any moment
 // all CTAs of a threadblock stream through one window of memory.
+// `stripe` is A.stripe for dependent threadblocks (piece j must cover the same bytes on the
+// sender and the receiver); an independent threadblock (own piece count) halves it until every
+// one of its pieces owns a stripe of each chunk (else CTAs beyond the stripe count idle —
+// measured: the n=1 copy at 64 KiB ran on 1 of 16 CTAs, 5.7 vs 2.6 us).
+__device__ __forceinline__ int64_t piece_stripe(const KArgs& a, bool indep, int split, int64_t cbytes) {
+  int64_t st = a.stripe;
+  if (indep)
+    while (st > 512 && st * split > cbytes) st >>= 1;
+  return st;
+}
 template <typename F>
-__device__ __forceinline__ void for_piece(const KArgs& a, int j, int split, int cnt, int64_t cbytes, F&& f) {
+__device__ __forceinline__ void for_piece(int64_t stripe, int j, int split, int cnt, int64_t cbytes, F&& f) {
   if (split == 1) {
     f((int64_t)0, (int64_t)cnt * cbytes);
     return;
   }
-  const int64_t nb = (cbytes + a.stripe - 1) / a.stripe;
+  const int64_t nb = (cbytes + stripe - 1) / stripe;
   for (int q = 0; q < cnt; ++q)
     for (int64_t b = j; b < nb; b += split) {
-      const int64_t off = b * a.stripe;
-      f((int64_t)q * cbytes + off, min(a.stripe, cbytes - off));
+      const int64_t off = b * stripe;
+      f((int64_t)q * cbytes + off, min(stripe, cbytes - off));
     }
 }
 
@@ -677,6 +687,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   // before the next (every CTA visits pieces in increasing order, so a wait on piece j only
   // ever depends on piece-j work of CTAs that have finished all their pieces < j).
   const int nsplit = cta_indep(me) ? ct : A.split;  // this tb's piece count
+  const int64_t stripe = piece_stripe(A, cta_indep(me), nsplit, A.chunk_elems * A.elt);
   Ctx c{&A, &R, t, 0, 0};
   c.epoch = s_epoch;
   const u64 E = c.epoch << 24;
@@ -849,7 +860,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         if (st.op == K_CPY) {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { ll_copy(dst + off, src + off, len); });
+          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { ll_copy(dst + off, src + off, len); });
         }
       } else switch (st.op) {
         case K_SEND:
@@ -861,15 +872,15 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           // TMA bulk path (A.tma: 1 = local copies, 2 = also pushes to peers) for 16-byte
           // aligned ranges; one elected thread drives it, the CTA waits at the next barrier
           const bool tma = !LL && (A.tma == 2 || (A.tma == 1 && st.op == K_CPY)) &&
-                           ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)cbytes | (uintptr_t)A.stripe) & 15) == 0);
+                           ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)cbytes | (uintptr_t)stripe) & 15) == 0);
           if (tma) {
             if (tid == 0) {
               asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
-              for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { tma_push(tp, dst + off, src + off, len); });
+              for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { tma_push(tp, dst + off, src + off, len); });
               tma_finish(tp);
             }
           } else {
-            for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+            for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           }
           break;
         }
@@ -878,7 +889,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           const int nfwd = st.op == K_RRCS ? 1 : 0;
-          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             reduce_dispatch(A.dtype, dst + off, s_fwd, nfwd, src + off, s_stage, 1, off, len / elt);
           });
           break;
@@ -887,7 +898,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           const int64_t unit = (cbytes % 16 == 0) ? 16 : elt;
-          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             const int64_t nu = len / unit;
             const int64_t a = off + nu * st.part / st.nparts * unit;
             const int64_t b = (st.part + 1 == st.nparts) ? off + len : off + nu * (st.part + 1) / st.nparts * unit;
@@ -900,7 +911,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         case K_RCS: {  // the bytes landed in dst (zero-copy); push them on to the send's peer
           const char* src = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           char* dst = s_fwd[0];
-          for_piece(A, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
+          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           break;
         }
         default:  // K_NOP, K_SENT, K_PUB: no data work on this side
