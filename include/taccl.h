@@ -109,7 +109,10 @@ taccl_result_t taccl_comm_destroy(void);
  * same role in the same order. Step 1: export a blob for [ptr, ptr+bytes) (any pointer
  * inside a cudaMalloc'd allocation). Step 2: pass all ranks' blobs (rank order) to
  * taccl_register_buffer. Afterwards a taccl_run whose recvbuf lies inside [ptr, ptr+bytes)
- * stores into the peers' registered buffers at the same offset. */
+ * stores into the peers' registered buffers at the same offset, and one whose sendbuf lies
+ * inside a registered buffer runs in pull mode (receive-reduces fed by a peer's input load it
+ * in place over NVLink; the call then completes only after every reader is done with this
+ * rank's sendbuf). An unregistered sendbuf is pushed (no pull mode). */
 taccl_result_t taccl_buffer_export(const void* ptr, size_t bytes, void* out, size_t* len);
 taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* all_blobs,
                                      size_t len_each);
@@ -126,7 +129,8 @@ taccl_result_t taccl_load_algo(const char* schedule_text, size_t len, taccl_algo
  * count convention: AG count = elements per rank (recvbuf holds nranks*count), A2A count =
  * elements per peer (both buffers hold nranks*count), AR count = total elements, RS count =
  * elements per rank (sendbuf holds nranks*count, recvbuf count). sendbuf/recvbuf are
- * device pointers; recvbuf must be registered (taccl_register_buffer) unless emulated.
+ * device pointers; recvbuf must be registered (taccl_register_buffer) unless emulated;
+ * a registered sendbuf enables pull mode (TACCL_PULL=0 disables it).
  * In-place / overlapping buffers are accepted (the input is first copied, on `stream`, to a
  * private arena region; INVALID_ARG if the arena is too small). Enqueues ONE kernel on `stream`
  * (a cudaStream_t; NULL = legacy default stream); returns without synchronizing. The
