@@ -112,7 +112,9 @@ taccl_result_t taccl_comm_destroy(void);
  * stores into the peers' registered buffers at the same offset, and one whose sendbuf lies
  * inside a registered buffer runs in pull mode (receive-reduces fed by a peer's input load it
  * in place over NVLink; the call then completes only after every reader is done with this
- * rank's sendbuf). An unregistered sendbuf is pushed (no pull mode). */
+ * rank's sendbuf). An unregistered sendbuf is pushed (no pull mode). All ranks
+ * of a call must agree: either every rank's sendbuf lies in a registered buffer or none does
+ * (a mismatch ends in TACCL_ERR_TIMEOUT from the watchdog, reported by taccl_check). */
 taccl_result_t taccl_buffer_export(const void* ptr, size_t bytes, void* out, size_t* len);
 taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* all_blobs,
                                      size_t len_each);
