@@ -17,6 +17,7 @@
 // sender's arena; a sender's first store of the call waits for it.
 // Epochs live in device memory (incremented by the rank's last CTA), so launches are
 // CUDA-graph capturable. Every spin wait has a %globaltimer watchdog.
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -1002,7 +1003,51 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   }
 }
 
+// Lean copy for single-step local-copy plans (n=1 schedules are one `cpy`): no plan, flags or
+// epochs are involved, so the interpreter's prologue/epilogue is skipped. 16-byte vectors,
+// 8 in flight per thread, grid-stride; evict-first stores (the copy is not re-read).
+__global__ void __launch_bounds__(256) taccl_copy_kernel(char* __restrict__ dst, const char* __restrict__ src, int64_t n) {
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const int64_t nv = n >> 4;
+    const int4* s = reinterpret_cast<const int4*>(src);
+    int4* d = reinterpret_cast<int4*>(dst);
+    constexpr int U = 8;
+    int64_t i = tid;
+    for (; i + (int64_t)(U - 1) * nt < nv; i += (int64_t)U * nt) {
+      int4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_cg(s + i + (int64_t)u * nt);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st_v4_cs(d + i + (int64_t)u * nt, v[u]);
+    }
+    for (; i < nv; i += nt) st_v4(d + i, ld_cg(s + i));
+    for (int64_t b = (nv << 4) + tid; b < n; b += nt) dst[b] = src[b];
+  } else {
+    for (int64_t b = tid; b < n; b += nt) dst[b] = src[b];
+  }
+}
+
 }  // namespace
+
+int copy_grid(int64_t bytes) {
+  static int sms = 0;
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
+  const int64_t per_cta = 256LL * 16 * 8;  // one unrolled pass of a CTA
+  const int64_t want = (bytes + per_cta - 1) / per_cta;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+}
+
+int launch_copy(char* dst, const char* src, int64_t bytes, void* stream, std::string* err) {
+  taccl_copy_kernel<<<copy_grid(bytes), 256, 0, (cudaStream_t)stream>>>(dst, src, bytes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("copy launch: ") + cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
 
 int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::string* err) {
   if (a.staged) taccl_exec_kernel<true><<<grid, kThreadsLL, smem, (cudaStream_t)stream>>>(a);

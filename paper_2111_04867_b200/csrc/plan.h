@@ -10,7 +10,7 @@ struct RankPlan {
   std::vector<KTB> tbs;
   std::vector<KStep> steps;
   std::vector<int32_t> deps;   // pairs (tb, step)
-  std::vector<int32_t> fused;  // quadruples (tb, seq, soff, soff2)
+  std::vector<int32_t> fused;  // chain entries (tb, seq, soff, soff2, poff), then forward entries
   int stage_chunks = 0;        // rrc staging this rank needs (chunk units)
   int stage2_chunks = 0;       // staged mode: every receive's slot (chunk units)
   int scratch_chunks = 0;      // EF scratch buffer (chunk units)

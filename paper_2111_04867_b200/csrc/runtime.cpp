@@ -56,6 +56,9 @@ struct Algo {
   int nranks, p, instances;
   uint64_t min_bytes, max_bytes;
   int max_scratch_chunks = 0, max_stage_chunks = 0, max_stage2_chunks = 0, max_steps_cnt = 1;
+  // n = 1 plan that is one input -> output `cpy` (no deps): runs as the lean copy kernel
+  bool lean_copy = false;
+  int lean_srcoff = 0, lean_dstoff = 0, lean_cnt = 0;
   std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
   std::vector<DevPlan> plans_ll;  // the same program planned for the LL kernel (chain sends fused)
   std::vector<int> ntb;         // per rank
@@ -302,10 +305,27 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   return TACCL_SUCCESS;
 }
 
+// the lean copy kernel below 256 MiB: the interpreter's TMA bulk pipeline streams large copies
+// faster (1 GiB: 6300 vs 6090 GB/s r+w), the lean kernel wins below (1 KB: 1.3 vs 3.2 us;
+// 64 MiB: 22.3 vs 23.5 us; profiles/r01_lean_copy_n1.txt)
+bool lean(const Algo* a, const Geometry& G) {
+  return a->lean_copy && (int64_t)a->lean_cnt * G.chunk_bytes < (int64_t)env_size("TACCL_LEAN_MAX", 256ull << 20);
+}
+
 taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int elt,
                       const std::vector<int>& ranks, const void* const* sends, void* const* recvs,
                       char* const (*peer_out)[kMaxRanks], void* stream,
                       const char* const (*peer_in)[kMaxRanks] = nullptr) {
+  if (lean(a, G)) {  // n = 1, one input -> output copy
+    std::string err;
+    const int64_t cb = G.chunk_bytes;
+    if (launch_copy((char*)recvs[0] + a->lean_dstoff * cb, (const char*)sends[0] + a->lean_srcoff * cb,
+                    a->lean_cnt * cb, stream, &err))
+      return fail(TACCL_ERR_CUDA, err);
+    ++g.launches;
+    ++g_launches;
+    return TACCL_SUCCESS;
+  }
   KArgs A;
   memset(&A, 0, sizeof(A));
   A.nlocal = (int)ranks.size();
@@ -693,6 +713,16 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->max_stage_chunks = std::max(a->max_stage_chunks, plans[r].stage_chunks);
     a->max_stage2_chunks = std::max(a->max_stage2_chunks, plans[r].stage2_chunks);
     a->fused_chains += plans[r].fused_chains;
+    if (a->nranks == 1 && plans[r].steps.size() == 1) {
+      const KStep& k = plans[r].steps[0];
+      if (k.op == K_CPY && k.srcbuf == KB_I && k.dstbuf == KB_O && k.dep_count == 0 &&
+          env_size("TACCL_NO_LEAN_COPY", 0) == 0) {
+        a->lean_copy = true;
+        a->lean_srcoff = k.srcoff;
+        a->lean_dstoff = k.dstoff;
+        a->lean_cnt = k.cnt;
+      }
+    }
     if (g.emulated || r == g.rank) {
       taccl_result_t rc = upload(plans[r], &a->plans[r]);
       if (!rc) rc = upload(plans_ll[r], &a->plans_ll[r]);
@@ -826,6 +856,12 @@ taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dt
   if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
   Geometry G;
   if ((rc = geometry(a, coll, count, elt, 1, 0, &G))) return rc;
+  if (lean(a, G)) {  // n = 1 single-copy plan: the lean copy kernel
+    if (ctas) *ctas = copy_grid((int64_t)a->lean_cnt * G.chunk_bytes);
+    if (split) *split = 1;
+    if (threads) *threads = 256;
+    return TACCL_SUCCESS;
+  }
   if (ctas) *ctas = G.grid;
   if (split) *split = G.split;
   if (threads) *threads = G.staged ? kThreadsLL : kThreads;

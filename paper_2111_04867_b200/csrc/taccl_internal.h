@@ -244,6 +244,9 @@ TACCL_HD inline int tb_pieces(int indep, int weight, int wsum, int budget, int s
 
 // executor.cu
 int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::string* err);
+// single-step local-copy plans (n = 1): dst[0, bytes) = src[0, bytes) in one lean kernel
+int launch_copy(char* dst, const char* src, int64_t bytes, void* stream, std::string* err);
+int copy_grid(int64_t bytes);  // its grid size
 constexpr int kPlanSmemMax = (48 << 10) / kDirectPerSM;  // plans up to this size are staged in smem
 int executor_max_ctas(int device, std::string* err);  // co-resident CTA capacity
 

@@ -9,7 +9,7 @@ AR="python tools/emu_time.py --coll allreduce --algo direct --n 4 --bytes 268435
 LL="python tools/emu_time.py --coll allgather --algo direct --n 2 --bytes 65536 --iters 20"
 $B > gpurun_out/plain_b_$tag.log 2>&1 &&
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_$tag.csv $B > /dev/null 2>&1 &&
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:taccl_exec -s 5 -c 1 -o gpurun_out/prof_copy_$tag $B > gpurun_out/ncu_copy_$tag.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:taccl_ -s 5 -c 1 -o gpurun_out/prof_copy_$tag $B > gpurun_out/ncu_copy_$tag.log 2>&1
 echo "copy rc=$?"
 $AR > gpurun_out/plain_ar_$tag.log 2>&1 &&
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:taccl_exec -s 3 -c 1 -o gpurun_out/prof_ar_$tag $AR > gpurun_out/ncu_ar_$tag.log 2>&1
