@@ -81,6 +81,18 @@ taccl_result_t taccl_check(void);
  * Returns SUCCESS or INVALID_SCHEDULE; last_error is "<class>: <message>". */
 taccl_result_t taccl_validate(const char* text, size_t len, int direct_store);
 
+/* Host-only, no communicator or GPU: check `text` (direct-store mode) and write rank `rank`'s
+ * executable plan as text into out[0, cap) (NUL-terminated, truncated if cap is too small;
+ * *needed = full length + 1). ll = 0: the direct kernel's plan, 1: the LL kernel's. One line
+ * per threadblock ("tb <t> send=<p> recv=<p> chan=<c> indep=<0|1>") followed by one line per
+ * step: "  <k> <OP> src=<buf>:<off> dst=<buf>:<off> cnt=<n> seq=<s> poff=<o> deps=<t:k,...>
+ * post=<t:k,...> part=<i>/<n> fuse=<count> fwd=<count>". For tests and inspection of the
+ * plan transformations (chain fusion, rrc+send fusion, pull-mode marking).
+ * Env knobs that shape plans at load (TACCL_NO_FUSE, TACCL_PULL_KINDS, ...) apply.
+ * Errors: INVALID_ARG (null pointers, rank out of range), INVALID_SCHEDULE. */
+taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, char* out, size_t cap,
+                               size_t* needed);
+
 /* ---- communicator (one per process) ---------------------------------------------------- */
 
 /* One rank per process on `cuda_device`. Allocates the rank's arena in device memory:

@@ -529,6 +529,54 @@ taccl_result_t taccl_validate(const char* text, size_t len, int direct_store) {
   return TACCL_SUCCESS;
 }
 
+taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, char* out, size_t cap,
+                               size_t* needed) {
+  if (!text || !needed) return fail(TACCL_ERR_INVALID_ARG, "null pointer");
+  std::string d;
+  try {
+    Program P = parse_ef(text, len);
+    check_program(P, true);
+    if (rank < 0 || rank >= P.nranks) return fail(TACCL_ERR_INVALID_ARG, "rank out of range");
+    const bool fuse = env_size("TACCL_NO_FUSE", 0) == 0, rrcs = env_size("TACCL_NO_RRCS", 0) == 0;
+    std::vector<RankPlan> plans =
+        ll ? build_plans(P, fuse, rrcs, env_size("TACCL_NO_CHAIN_SENDS_LL", 0) == 0)
+           : build_plans(P, fuse, rrcs, env_size("TACCL_CHAIN_SENDS", 0) != 0, (int)env_size("TACCL_PULL_KINDS", 1));
+    const RankPlan& rp = plans[rank];
+    static const char* ops[] = {"SEND", "RECV", "RRC", "CPY", "NOP", "RRC_FUSED", "RRCS", "SENT", "PUB", "RCS"};
+    static const char* bufs[] = {"i", "o", "s", "stage"};
+    auto pairs = [&](int b, int c) {
+      std::string x;
+      for (int q = 0; q < c; ++q)
+        x += (q ? "," : "") + std::to_string(rp.deps[2 * (b + q)]) + ":" + std::to_string(rp.deps[2 * (b + q) + 1]);
+      return x;
+    };
+    for (size_t t = 0; t < rp.tbs.size(); ++t) {
+      const KTB& kt = rp.tbs[t];
+      d += "tb " + std::to_string(t) + " send=" + std::to_string(kt.send) + " recv=" + std::to_string(kt.recv) +
+           " chan=" + std::to_string(kt.chan) + " indep=" + std::to_string(kt.indep) + "\n";
+      for (int k = 0; k < kt.nsteps; ++k) {
+        const KStep& x = rp.steps[kt.step_begin + k];
+        d += "  " + std::to_string(k) + " " + ops[(int)x.op] + " src=" + bufs[(int)x.srcbuf] + ":" +
+             std::to_string(x.srcoff) + " dst=" + bufs[(int)x.dstbuf] + ":" + std::to_string(x.dstoff) +
+             " cnt=" + std::to_string(x.cnt) + " seq=" + std::to_string(x.seq) + " poff=" + std::to_string(x.poff) +
+             " deps=" + pairs(x.dep_begin, x.dep_count) + " post=" + pairs(x.post_begin, x.post_count) +
+             " part=" + std::to_string(x.part) + "/" + std::to_string(x.nparts) +
+             " fuse=" + std::to_string(x.op == K_RRC_FUSED ? x.fuse_count : 0) + " fwd=" + std::to_string(x.fwd_count) + "\n";
+      }
+    }
+  } catch (const SchedError& e) {
+    return fail(TACCL_ERR_INVALID_SCHEDULE, e.kind + ": " + e.msg);
+  }
+  *needed = d.size() + 1;
+  if (out && cap) {
+    const size_t m = std::min(cap - 1, d.size());
+    memcpy(out, d.data(), m);
+    out[m] = 0;
+  }
+  g_err.clear();
+  return TACCL_SUCCESS;
+}
+
 taccl_result_t taccl_comm_init(int rank, int nranks, int cuda_device, size_t scratch_bytes) {
   if (rank < 0 || rank >= nranks) return fail(TACCL_ERR_INVALID_ARG, "rank out of range");
   taccl_result_t rc = comm_common_init(nranks, cuda_device, scratch_bytes);

@@ -44,6 +44,7 @@ def lib():
             "taccl_last_error": ([], c_cp),
             "taccl_check": ([], c_int),
             "taccl_validate": ([c_cp, c_size, c_int], c_int),
+            "taccl_plan_dump": ([c_cp, c_size, c_int, c_int, c_vp, c_size, ctypes.POINTER(c_size)], c_int),
             "taccl_comm_init": ([c_int, c_int, c_int, c_size], c_int),
             "taccl_comm_init_emulated": ([c_int, c_int, c_size], c_int),
             "taccl_comm_export_handle": ([c_vp, ctypes.POINTER(c_size)], c_int),
@@ -76,6 +77,16 @@ def _check(rc):
 
 def last_error() -> str:
     return lib().taccl_last_error().decode()
+
+
+def plan_dump(text: str, rank: int, ll: bool = False) -> str:
+    """Rank `rank`'s executable plan as text (host only; include/taccl.h taccl_plan_dump)."""
+    b = text.encode()
+    need = ctypes.c_size_t(0)
+    _check(lib().taccl_plan_dump(b, len(b), rank, int(ll), None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().taccl_plan_dump(b, len(b), rank, int(ll), buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
 
 
 def validate(text: str, direct: bool = True):

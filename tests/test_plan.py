@@ -1,0 +1,102 @@
+"""CPU tests of the plan builder (csrc/plan.cpp) through the host-only taccl_plan_dump: the
+transformations the executor relies on — rrc chain fusion, rrc+send fusion, pull-mode marking
+(both sides of a connection must agree), minimal chain dependencies and post-dependency
+elision. The GPU parity tests prove the results; these pin the shapes."""
+import re
+
+import pytest
+
+from paper_2111_04867_b200 import taccl
+from paper_2111_04867_b200.generator import generate
+
+STEP = re.compile(r"\s+(\d+) (\w+) src=(\w+):(\d+) dst=(\w+):(\d+) cnt=(\d+) seq=(\d+) poff=(-?\d+) "
+                  r"deps=([\d:,]*) post=([\d:,]*) part=(\d+)/(\d+) fuse=(\d+) fwd=(\d+)")
+TB = re.compile(r"tb (\d+) send=(-?\d+) recv=(-?\d+) chan=(\d+) indep=(\d)")
+
+
+def plan(text, rank, ll=False):
+    tbs = []
+    for line in taccl.plan_dump(text, rank, ll).splitlines():
+        m = TB.match(line)
+        if m:
+            tbs.append({"send": int(m[2]), "recv": int(m[3]), "chan": int(m[4]), "steps": []})
+            continue
+        m = STEP.match(line)
+        assert m, line
+        tbs[-1]["steps"].append({"op": m[2], "src": (m[3], int(m[4])), "dst": (m[5], int(m[6])), "cnt": int(m[7]),
+                                 "seq": int(m[8]), "poff": int(m[9]), "deps": [d for d in m[10].split(",") if d],
+                                 "post": [d for d in m[11].split(",") if d], "part": int(m[12]), "nparts": int(m[13]),
+                                 "fuse": int(m[14])})
+    return tbs
+
+
+def test_rs_n2_plain_rrc_is_pulled_on_both_sides():
+    text = generate("reducescatter", "direct", 2, 1, 1)
+    for r in range(2):
+        (tb,) = plan(text, r)
+        send, rrc = tb["steps"]
+        assert send["op"] == "SEND" and rrc["op"] == "RRC"
+        # the receiver reads the peer's input chunk r in place; the sender marks the same send
+        assert rrc["poff"] == r and send["poff"] == 1 - r
+
+
+def test_ar_n2_rrc_fused_with_its_send_and_not_pulled_by_default():
+    text = generate("allreduce", "direct", 2, 1, 1)
+    (tb,) = plan(text, 0)
+    assert [s["op"] for s in tb["steps"]] == ["SEND", "RRCS", "SENT", "RECV"]
+    assert all(s["poff"] == -1 for s in tb["steps"])
+
+
+def test_pull_kinds_env_marks_rrcs_and_chains(monkeypatch):
+    monkeypatch.setenv("TACCL_PULL_KINDS", "7")
+    (tb,) = plan(generate("allreduce", "direct", 2, 1, 1), 1)
+    assert tb["steps"][1]["op"] == "RRCS" and tb["steps"][1]["poff"] == 1 and tb["steps"][0]["poff"] == 0
+    tbs = plan(generate("reducescatter", "direct", 4, 1, 1), 2)
+    assert all(t["steps"][0]["poff"] >= 0 for t in tbs)   # every chain input pulled -> sends marked
+
+
+@pytest.mark.parametrize("n", [3, 4, 8])
+def test_rs_chain_members_have_no_dependencies_and_no_post_wait(n):
+    # all-pairs RS: rank r's n-1 rrcs into o[0] form one chain; nothing conflicting precedes
+    # it and nothing follows it, so no member waits on another CTA at all
+    tbs = plan(generate("reducescatter", "direct", n, 1, 1), 0)
+    members = [t["steps"][1] for t in tbs if len(t["steps"]) > 1]
+    assert len(members) == n - 1
+    assert all(m["op"] == "RRC_FUSED" and m["fuse"] == n - 1 and m["nparts"] == n - 1 for m in members)
+    assert sorted(m["part"] for m in members) == list(range(n - 1))
+    assert all(m["deps"] == [] and m["post"] == [] for m in members)
+
+
+def test_ar_chain_keeps_post_wait_when_a_send_follows():
+    # direct AR: the chain's last member is followed by the AG-phase send of the reduced chunk,
+    # so it must still wait for the other members' portions before that send may read o[r]
+    tbs = plan(generate("allreduce", "direct", 4, 1, 1), 0)
+    members = [(i, t["steps"][1]) for i, t in enumerate(tbs) if t["steps"][1]["op"] == "RRC_FUSED"]
+    last = max(members, key=lambda x: x[1]["part"])
+    others = sorted(f"{i}:1" for i, _ in members if i != last[0])
+    assert sorted(last[1]["post"]) == others
+    assert all(m["deps"] == [] for _, m in members)
+
+
+def test_chain_members_inherit_conflicting_predecessors(monkeypatch):
+    # A/B knob TACCL_CHAIN_OLDDEPS=1 restores "every incoming edge of X_1": the members then
+    # wait on X_1's threadblock predecessor (the send) — the edge the trimming removes
+    monkeypatch.setenv("TACCL_CHAIN_OLDDEPS", "1")
+    tbs = plan(generate("reducescatter", "direct", 4, 1, 1), 0)
+    members = [t["steps"][1] for t in tbs]
+    assert sum(1 for m in members if m["deps"]) == 2   # the two non-head members
+    assert any(m["post"] for m in members)
+
+
+def test_ring_relays_fuse_recv_copy_send():
+    # ring AG at n=4: the relays' receive + forward of the same chunk become one RCS step
+    tbs = plan(generate("allgather", "ring", 4, 1, 1), 0)
+    ops = [s["op"] for t in tbs for s in t["steps"]]
+    assert "RCS" in ops and "SENT" in ops
+
+
+def test_plan_dump_errors():
+    with pytest.raises(taccl.TacclError):
+        taccl.plan_dump("<algo", 0)
+    with pytest.raises(taccl.TacclError):
+        taccl.plan_dump(generate("allgather", "ring", 2, 1, 1), 5)
