@@ -78,7 +78,7 @@ def test_ar_chain_keeps_post_wait_when_a_send_follows():
     assert all(m["deps"] == [] for _, m in members)
 
 
-def test_chain_members_inherit_conflicting_predecessors(monkeypatch):
+def test_old_deps_knob_restores_every_incoming_edge(monkeypatch):
     # A/B knob TACCL_CHAIN_OLDDEPS=1 restores "every incoming edge of X_1": the members then
     # wait on X_1's threadblock predecessor (the send) — the edge the trimming removes
     monkeypatch.setenv("TACCL_CHAIN_OLDDEPS", "1")
