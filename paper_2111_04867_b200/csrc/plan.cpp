@@ -321,10 +321,17 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
         for (auto e : deps[i]) wanted[flat.at(e)] = 1;
       for (const KTB& kt : rp.tbs)  // a threadblock successor relies on it too (program order)
         for (int k = 0; k + 1 < kt.nsteps; ++k) wanted[kt.step_begin + k] = 1;
-      for (size_t i = 0; i < rp.steps.size(); ++i)
-        if (!post[i].empty() && !wanted[i] && rp.steps[i].fwd_count == 0 &&
+      for (size_t i = 0; i < rp.steps.size(); ++i) {
+        // a chain whose inputs are pulled keeps the wait: its last member acks the senders for
+        // every member's reads, so the acks must follow all portions (pull mode, executor.cu)
+        bool pulled = false;
+        const KStep& x = rp.steps[i];
+        if ((pull_kinds & 4) && x.op == K_RRC_FUSED)
+          for (int f = 0; f < x.fuse_count; ++f) pulled = pulled || rp.fused[kFuseStride * (x.fuse_begin + f) + 4] >= 0;
+        if (!post[i].empty() && !wanted[i] && x.fwd_count == 0 && !pulled &&
             !(getenv("TACCL_CHAIN_OLDDEPS") && atoi(getenv("TACCL_CHAIN_OLDDEPS"))))
           post[i].clear();
+      }
     }
     // pull mode acks are "read up to message seq" per connection, so they must be written in
     // message order: a chain's inputs are acked by its last member, which may run after a later

@@ -67,6 +67,16 @@ def test_rs_chain_members_have_no_dependencies_and_no_post_wait(n):
     assert all(m["deps"] == [] and m["post"] == [] for m in members)
 
 
+def test_pulled_chain_keeps_post_wait(monkeypatch):
+    # with pulled chains (TACCL_PULL_KINDS=7) the last member acks every input for all
+    # members, so it must wait for their portions even when nothing follows the chain
+    monkeypatch.setenv("TACCL_PULL_KINDS", "7")
+    tbs = plan(generate("reducescatter", "direct", 4, 1, 1), 0)
+    members = [t["steps"][1] for t in tbs]
+    last = max(members, key=lambda m: m["part"])
+    assert len(last["post"]) == 2 and all(m["deps"] == [] for m in members)
+
+
 def test_ar_chain_keeps_post_wait_when_a_send_follows():
     # direct AR: the chain's last member is followed by the AG-phase send of the reduced chunk,
     # so it must still wait for the other members' portions before that send may read o[r]
