@@ -430,12 +430,30 @@ def test_trace_timeline_is_consistent(mode):
 
 # ---------------------------------------------------------------- edge cases
 
-def test_single_rank_copy_path():
+@pytest.mark.parametrize("lean_max", [None, "0"])
+def test_single_rank_copy_path(lean_max):
+    # n = 1 schedules are one input -> output copy: the lean copy kernel below TACCL_LEAN_MAX
+    # (default 256 MiB), the interpreter above; "0" forces the interpreter at every size
     text = generate("allgather", "direct", 1, 1, 1)
-    for count in (1, 7, 4096, (1 << 20) + 3):
-        ins = bits_inputs("allgather", 1, count, "bfloat16", 8)
-        got = run_gpu(text, "allgather", 1, "bfloat16", ins)
-        assert_bits_equal(got, ins)
+    if lean_max is not None:
+        os.environ["TACCL_LEAN_MAX"] = lean_max
+    try:
+        for count in (1, 7, 4096, (1 << 20) + 3, (3 << 20) + 1):
+            ins = bits_inputs("allgather", 1, count, "bfloat16", 8)
+            got = run_gpu(text, "allgather", 1, "bfloat16", ins)
+            assert_bits_equal(got, ins)
+    finally:
+        os.environ.pop("TACCL_LEAN_MAX", None)
+
+
+def test_lean_copy_geometry():
+    comm = taccl.Comm(rank=0, nranks=1, device=0, scratch_bytes=8 << 20)
+    try:
+        comm.load(generate("allgather", "direct", 1, 1, 1))
+        assert comm.plan_info("allgather", 1 << 20, taccl.BFLOAT16)["threads"] == 256      # lean kernel
+        assert comm.plan_info("allgather", 1 << 28, taccl.BFLOAT16)["threads"] == 512      # 512 MiB: interpreter
+    finally:
+        comm.destroy()
 
 
 @pytest.mark.parametrize("coll", ["allgather", "allreduce"])
