@@ -449,7 +449,9 @@ __device__ __forceinline__ float ll_elt_f(u64 v, int e, int dtype) {
 // Returns false if a wait timed out. One generic instance (dtype at run time): the LL kernel
 // is latency-bound and its instruction footprint matters more than its ALU work (ncu:
 // "no instruction" stalls were the second stall reason before this was slimmed).
+// MAXIN: compile-time bound on nin (1 for single-input receive-reduces: fewer live registers).
 constexpr int kLLU = 2;
+template <int MAXIN>
 __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src, char* dst, const char* const* ins,
                                          int nin, char* const* fwd, int nfwd, int64_t cb, int64_t llcb, int cnt,
                                          int64_t l0, int64_t l1,
@@ -461,7 +463,7 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
     int64_t pb[kLLU], lb[kLLU];
     int vb[kLLU];
     u64 v[kLLU];
-    uint4 w[kLLU][kMaxRanks];
+    uint4 w[kLLU][MAXIN];
 #pragma unroll
     for (int u = 0; u < kLLU; ++u) {
       const unsigned idx = base + u * nt;
@@ -472,7 +474,7 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
       vb[u] = idx < total ? (int)min((int64_t)8, cb - 8 * ll) : 0;  // valid payload bytes
       v[u] = (src && vb[u]) ? ld_bytes(src + pb[u], vb[u]) : 0;
 #pragma unroll
-      for (int i = 0; i < kMaxRanks; ++i)
+      for (int i = 0; i < MAXIN; ++i)
         if (i < nin && vb[u]) w[u][i] = ld_volatile_v4(ins[i] + lb[u]);
     }
 #ifdef TACCL_TRACE_FINE
@@ -485,7 +487,7 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
 #pragma unroll
       for (int u = 0; u < kLLU; ++u)
 #pragma unroll
-        for (int i = 0; i < kMaxRanks; ++i)
+        for (int i = 0; i < MAXIN; ++i)
           if (i < nin && vb[u] && (w[u][i].y != flag || w[u][i].w != flag)) {
             if (it) w[u][i] = ld_volatile_v4(ins[i] + lb[u]);
             all = false;
@@ -507,7 +509,7 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
       } else if (dtype == TACCL_INT32) {  // wraps mod 2^32 (G13)
         unsigned a0 = (unsigned)v[u], a1 = (unsigned)(v[u] >> 32);
 #pragma unroll
-        for (int i = 0; i < kMaxRanks; ++i)
+        for (int i = 0; i < MAXIN; ++i)
           if (i < nin) {
             a0 += w[u][i].x;
             a1 += w[u][i].z;
@@ -519,7 +521,7 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[e] = e < ne ? ll_elt_f(v[u], e, dtype) : 0.f;
 #pragma unroll
-        for (int i = 0; i < kMaxRanks; ++i) {
+        for (int i = 0; i < MAXIN; ++i) {
           if (i >= nin) break;
           const u64 y = (u64)w[u][i].x | ((u64)w[u][i].z << 32);
 #pragma unroll
@@ -544,6 +546,59 @@ __device__ __forceinline__ bool ll_lines(int dtype, bool reduce, const char* src
 #ifdef TACCL_TRACE_FINE
     if (ft && base == threadIdx.x) ft[2] = globaltimer();
 #endif
+  }
+  return true;
+}
+
+// The common LL step without a reduction (send, recv, recv+send): one input — local payload
+// `src` or the LL slot `in` — to the local payload `dst` and/or the peer slot `fwd`. Same line
+// geometry and batching as ll_lines, without its per-rank input arrays and dtype paths, so a
+// send/recv runs a short instruction sequence with few live registers.
+__device__ __forceinline__ bool ll_move(const char* src, char* dst, const char* in, char* fwd, int64_t cb, int64_t llcb,
+                                        int cnt, int64_t l0, int64_t l1, unsigned flag, u64 timeout_ns) {
+  const unsigned m = (unsigned)(l1 - l0), total = m * (unsigned)cnt, nt = blockDim.x;
+  for (unsigned base = threadIdx.x; base < total; base += kLLU * nt) {
+    int64_t pb[kLLU], lb[kLLU];
+    int vb[kLLU];
+    u64 v[kLLU];
+    uint4 w[kLLU];
+#pragma unroll
+    for (int u = 0; u < kLLU; ++u) {
+      const unsigned idx = base + u * nt;
+      const unsigned q = idx / m;
+      const int64_t ll = l0 + (idx - q * m);
+      pb[u] = (int64_t)q * cb + 8 * ll;
+      lb[u] = (int64_t)q * llcb + 16 * ll;
+      vb[u] = idx < total ? (int)min((int64_t)8, cb - 8 * ll) : 0;
+      if (in) w[u] = vb[u] ? ld_volatile_v4(in + lb[u]) : make_uint4(0, flag, 0, flag);
+      else v[u] = vb[u] ? ld_bytes(src + pb[u], vb[u]) : 0;
+    }
+    if (in) {
+      u64 t0 = 0;
+      for (int it = 0;; ++it) {
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < kLLU; ++u)
+          if (w[u].y != flag || w[u].w != flag) {
+            if (it) w[u] = ld_volatile_v4(in + lb[u]);
+            all = false;
+          }
+        if (all) break;
+        if ((it & 63) == 1) {
+          const u64 now = globaltimer();
+          if (!t0) t0 = now;
+          else if (now - t0 > timeout_ns) return false;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kLLU; ++u) v[u] = (u64)w[u].x | ((u64)w[u].z << 32);
+    }
+#pragma unroll
+    for (int u = 0; u < kLLU; ++u) {
+      if (!vb[u]) continue;
+      if (dst) st_bytes(dst + pb[u], v[u], vb[u]);
+      if (fwd) st_volatile_v4(fwd + lb[u], ll_line(v[u], flag));
+    }
   }
   return true;
 }
@@ -704,6 +759,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   char* const my_staged = R.arena + parity_off;
   const int64_t ll_cb = 16 * ((cbytes + 7) / 8);  // LL bytes per chunk slot
   const unsigned ll_flag = (unsigned)c.epoch;
+  if (LL && A.variant == 20) return;  // timing probe only: launch + prologue
   u64* const trace = (A.trace && tid == 0 && blockIdx.x < A.trace_ctas) ? A.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   if (trace) {
     trace[0] = t_entry;
@@ -719,6 +775,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
     u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
     for (int j = c0; j < nsplit; j += ct) st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
   }
+  unsigned fin_early = 0;
   for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
     if (!LL && tb.recv >= 0 && tid == 0 && A.ready_per_piece) {  // A/B knob: announce as each piece starts
@@ -729,6 +786,10 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
 
     for (int k = 0; k < tb.nsteps; ++k) {
       const KStep& st = steps[tb.step_begin + k];
+      // the rank's CTA 0: load the arrival counter as its last step starts, so the exit check
+      // below normally finds every CTA arrived without another L2 round trip on its path
+      if (tid == 0 && c0 == 0 && t == 0 && k + 1 == tb.nsteps && j + ct >= nsplit)
+        fin_early = *reinterpret_cast<volatile unsigned*>(&ctrl->finished);
       const bool tr = trace && j == c0 && k < kTraceSteps;
       if (tr) trace[2 + 4 * k] = globaltimer();
       // LL fast path: a step with nothing to wait for needs no thread-0 pre-phase and no
@@ -772,8 +833,13 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         }
         const char* src = (st.op == K_RECV || st.op == K_RCS) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
         char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-        const bool ok = ll_lines(A.dtype, st.op == K_RRC || st.op == K_RRCS || fz, src, dst, ins, nin, fws, nfw, cbytes,
-                                 ll_cb, st.cnt, l0, l1, ll_flag, A.timeout_ns);
+        const bool red = st.op == K_RRC || st.op == K_RRCS || fz;
+        const bool ok = !red ? ll_move(src, dst, nin ? ins[0] : nullptr, nfw ? fws[0] : nullptr, cbytes, ll_cb, st.cnt, l0,
+                                       l1, ll_flag, A.timeout_ns)
+                      : nin <= 1 ? ll_lines<1>(A.dtype, true, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt, l0, l1,
+                                               ll_flag, A.timeout_ns)
+                                 : ll_lines<kMaxRanks>(A.dtype, true, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt,
+                                                       l0, l1, ll_flag, A.timeout_ns);
         if (tr) trace[4 + 4 * k] = globaltimer();
         if (__syncthreads_or(!ok)) {
           if (tid == 0) record_error(c, st.op, k);
@@ -846,11 +912,15 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         const int nin = st.op == K_SEND ? 0 : st.op == K_RRC_FUSED ? st.fuse_count : 1;
 #ifdef TACCL_TRACE_FINE
         // fine build: [2+4k] loads issued, [3+4k] waits done, [4+4k] stores issued (thread 0)
-        const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt, l0, l1,
-                                 ll_flag, A.timeout_ns, tr ? trace + 2 + 4 * k : nullptr);
+        const bool ok = ll_lines<kMaxRanks>(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt,
+                                            l0, l1, ll_flag, A.timeout_ns, tr ? trace + 2 + 4 * k : nullptr);
 #else
-        const bool ok = ll_lines(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt, l0, l1,
-                                 ll_flag, A.timeout_ns);
+        const bool ok = !reduce ? ll_move(src, dst, nin ? s_stage[0] : nullptr, nfwd ? s_fwd[0] : nullptr, cbytes, ll_cb,
+                                          st.cnt, l0, l1, ll_flag, A.timeout_ns)
+                        : nin <= 1 ? ll_lines<1>(A.dtype, true, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt,
+                                                 l0, l1, ll_flag, A.timeout_ns)
+                                   : ll_lines<kMaxRanks>(A.dtype, true, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb,
+                                                         st.cnt, l0, l1, ll_flag, A.timeout_ns);
         if (tr) trace[4 + 4 * k] = globaltimer();
 #endif
         if (__syncthreads_or(!ok)) {
@@ -991,7 +1061,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       const unsigned want = (unsigned)R.ncta - 1;
       volatile unsigned* fin = &ctrl->finished;
       const u64 t0 = globaltimer();
-      while (*fin < want)
+      while (fin_early < want && A.variant != 21 && *fin < want)  // 21: timing probe only (no arrival wait)
         if (globaltimer() - t0 > A.timeout_ns) {
           record_error(c, K_NOP, -1);
           break;
