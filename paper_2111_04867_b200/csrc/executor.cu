@@ -792,13 +792,28 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         fin_early = *reinterpret_cast<volatile unsigned*>(&ctrl->finished);
       const bool tr = trace && j == c0 && k < kTraceSteps;
       if (tr) trace[2 + 4 * k] = globaltimer();
-      // LL fast path: a step with nothing to wait for needs no thread-0 pre-phase and no
-      // barrier before its data work — every thread derives its slot pointers itself
-      const bool fast = LL && st.dep_count == 0 &&
-                        (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RCS ||
-                         st.op == K_RRC_FUSED);
+      // LL data steps (one copy of their code, so the kernel's executed footprint stays small):
+      // thread 0 waits for the step's dependencies, if any (LL lines carry their own flags, so
+      // there is nothing else to wait for); then every thread derives its slot pointers itself
+      const bool fast = LL && (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS ||
+                               st.op == K_RCS || st.op == K_RRC_FUSED);
       if (fast) {
-        if (tr) trace[3 + 4 * k] = trace[2 + 4 * k];  // nothing to wait for
+        if (st.dep_count) {
+          if (tid == 0) {
+            bool ok = true;
+            for (int d = 0; d < st.dep_count && ok; ++d) {
+              const int dt = deps[2 * (st.dep_begin + d)], dk = deps[2 * (st.dep_begin + d) + 1];
+              ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
+            }
+            if (!ok) {
+              record_error(c, st.op, k);
+              s_abort = 1;
+            }
+          }
+          __syncthreads();
+          if (s_abort) return;
+        }
+        if (tr) trace[3 + 4 * k] = globaltimer();
         const bool fz = st.op == K_RRC_FUSED;
         const char* ins[kMaxRanks];
         char* fws[kMaxRanks];
@@ -834,6 +849,11 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         const char* src = (st.op == K_RECV || st.op == K_RCS) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
         char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
         const bool red = st.op == K_RRC || st.op == K_RRCS || fz;
+#ifdef TACCL_TRACE_FINE
+        // fine build: [2+4k] loads issued, [3+4k] waits done, [4+4k] stores issued (thread 0)
+        const bool ok = ll_lines<kMaxRanks>(A.dtype, red, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt, l0, l1,
+                                            ll_flag, A.timeout_ns, tr ? trace + 2 + 4 * k : nullptr);
+#else
         const bool ok = !red ? ll_move(src, dst, nin ? ins[0] : nullptr, nfw ? fws[0] : nullptr, cbytes, ll_cb, st.cnt, l0,
                                        l1, ll_flag, A.timeout_ns)
                       : nin <= 1 ? ll_lines<1>(A.dtype, true, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt, l0, l1,
@@ -841,6 +861,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
                                  : ll_lines<kMaxRanks>(A.dtype, true, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt,
                                                        l0, l1, ll_flag, A.timeout_ns);
         if (tr) trace[4 + 4 * k] = globaltimer();
+#endif
         if (__syncthreads_or(!ok)) {
           if (tid == 0) record_error(c, st.op, k);
           return;
@@ -894,40 +915,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       __syncthreads();
       if (s_abort) return;
 
-      if (LL && (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED ||
-                 st.op == K_RCS)) {
-        // LL path: this piece's lines of every chunk (same split on both sides)
-        const int64_t nl = (cbytes + 7) / 8;
-        int64_t l0 = (int64_t)((unsigned)nl * (unsigned)j / (unsigned)nsplit);  // nl*split < 2^32 (LL sizes)
-        int64_t l1 = (int64_t)((unsigned)nl * (unsigned)(j + 1) / (unsigned)nsplit);
-        if (st.op == K_RRC_FUSED) {  // this member's portion of the piece
-          const int64_t m = l1 - l0, a0 = l0;
-          l0 = a0 + m * st.part / st.nparts;
-          l1 = a0 + m * (st.part + 1) / st.nparts;
-        }
-        const char* src = (st.op == K_RECV || st.op == K_RCS) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
-        char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-        const int nfwd = (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) ? 1 : st.op == K_RRC_FUSED ? st.fwd_count : 0;
-        const bool reduce = st.op == K_RRC || st.op == K_RRCS || st.op == K_RRC_FUSED;
-        const int nin = st.op == K_SEND ? 0 : st.op == K_RRC_FUSED ? st.fuse_count : 1;
-#ifdef TACCL_TRACE_FINE
-        // fine build: [2+4k] loads issued, [3+4k] waits done, [4+4k] stores issued (thread 0)
-        const bool ok = ll_lines<kMaxRanks>(A.dtype, reduce, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt,
-                                            l0, l1, ll_flag, A.timeout_ns, tr ? trace + 2 + 4 * k : nullptr);
-#else
-        const bool ok = !reduce ? ll_move(src, dst, nin ? s_stage[0] : nullptr, nfwd ? s_fwd[0] : nullptr, cbytes, ll_cb,
-                                          st.cnt, l0, l1, ll_flag, A.timeout_ns)
-                        : nin <= 1 ? ll_lines<1>(A.dtype, true, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb, st.cnt,
-                                                 l0, l1, ll_flag, A.timeout_ns)
-                                   : ll_lines<kMaxRanks>(A.dtype, true, src, dst, s_stage, nin, s_fwd, nfwd, cbytes, ll_cb,
-                                                         st.cnt, l0, l1, ll_flag, A.timeout_ns);
-        if (tr) trace[4 + 4 * k] = globaltimer();
-#endif
-        if (__syncthreads_or(!ok)) {
-          if (tid == 0) record_error(c, st.op, k);
-          return;
-        }
-      } else if constexpr (LL) {
+      if constexpr (LL) {
         if (st.op == K_CPY) {
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
