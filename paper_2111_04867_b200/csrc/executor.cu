@@ -66,6 +66,7 @@ __device__ bool wait_ge(const u64* p, u64 target, u64 timeout_ns) {
   if ((SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= target) return true;
   const u64 t0 = globaltimer();
   for (;;) {
+#pragma unroll 1  // each poll depends on the previous one: unrolling only grows the code (i-cache)
     for (int i = 0; i < 256; ++i)
       if ((SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= target) return true;
     if (globaltimer() - t0 > timeout_ns) return false;
@@ -408,9 +409,10 @@ __device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
 __device__ __forceinline__ void st_volatile_v4(void* p, uint4 v) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
-// nb payload bytes at p (any alignment; nb <= 8) <-> one u64 (little-endian byte order)
-__device__ __forceinline__ u64 ld_bytes(const char* p, int nb) {
-  if (nb == 8 && ((uintptr_t)p & 7) == 0) return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+// nb payload bytes at p (any alignment; nb <= 8) <-> one u64 (little-endian byte order).
+// The partial / unaligned forms are out of line: they only run for ragged tails and odd
+// offsets, and inlined at every call site they were a fifth of the LL kernel's code.
+__device__ __noinline__ u64 ld_bytes_slow(const char* p, int nb) {
   u64 v = 0;
   if (((uintptr_t)p & 1) == 0 && (nb & 1) == 0) {
     for (int b = 0; b < nb; b += 2) v |= (u64)__ldcg(reinterpret_cast<const unsigned short*>(p + b)) << (8 * b);
@@ -419,14 +421,20 @@ __device__ __forceinline__ u64 ld_bytes(const char* p, int nb) {
   }
   return v;
 }
-__device__ __forceinline__ void st_bytes(char* p, u64 v, int nb) {
-  if (nb == 8 && ((uintptr_t)p & 7) == 0) {
-    *reinterpret_cast<u64*>(p) = v;
-  } else if (((uintptr_t)p & 1) == 0 && (nb & 1) == 0) {
+__device__ __forceinline__ u64 ld_bytes(const char* p, int nb) {
+  if (nb == 8 && ((uintptr_t)p & 7) == 0) return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+  return ld_bytes_slow(p, nb);
+}
+__device__ __noinline__ void st_bytes_slow(char* p, u64 v, int nb) {
+  if (((uintptr_t)p & 1) == 0 && (nb & 1) == 0) {
     for (int b = 0; b < nb; b += 2) *reinterpret_cast<unsigned short*>(p + b) = (unsigned short)(v >> (8 * b));
   } else {
     for (int b = 0; b < nb; ++b) p[b] = (char)(v >> (8 * b));
   }
+}
+__device__ __forceinline__ void st_bytes(char* p, u64 v, int nb) {
+  if (nb == 8 && ((uintptr_t)p & 7) == 0) *reinterpret_cast<u64*>(p) = v;
+  else st_bytes_slow(p, v, nb);
 }
 __device__ __forceinline__ uint4 ll_line(u64 v, unsigned flag) {
   return make_uint4((unsigned)v, flag, (unsigned)(v >> 32), flag);
