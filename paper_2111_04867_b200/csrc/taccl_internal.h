@@ -177,7 +177,9 @@ struct KArgs {
   KRank r[kMaxRanks];
   int32_t nlocal;          // local ranks in this launch
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
-  int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT)
+  int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT); timing probes
+                           // only, results invalid: 9 = no fence before data flags, 20 = LL
+                           // kernel returns after its prologue, 21 = no arrival wait at exit
   int32_t dep_ctas;        // CTAs per dependent tb (<= split; CTA c runs pieces c, c+dep_ctas, ...)
   int32_t plan_smem;       // copy the rank's plan blob into shared memory at kernel start
   int32_t indep_cap;       // max pieces of an independent tb (bytes / min piece)
