@@ -33,11 +33,13 @@ def ranges(coll: str, n: int):
         small = MiB // 2 if n <= 4 else MiB // 4
         if n >= 8:
             return [("oneshot", 0, small), ("direct", small, INF)]
-        # 2 chunks per rank pipeline the ring's 2(n-1) hops: -10..13% time at >= 128 MiB
-        # (profiles/r01_ar_variants_n4.txt); below 128 MiB the direct schedule (multi-input
-        # reduce with every load in flight) is ahead of the ring (r01_sweep_n4_graph.jsonl:
-        # 64 MiB 183.8 vs 192.6 us)
-        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("ring_p2", 128 * MiB, INF)]
+        # below 128 MiB the direct schedule (multi-input reduce with every load in flight) is
+        # ahead of the ring (r01_sweep_n4_graph.jsonl: 64 MiB 185 vs 203 us); at 128-256 MiB
+        # the plain ring is (two boxes: 128 MiB 342-344 vs ring_p2 354-369 us, 256 MiB 633-641
+        # vs 649-672); from 512 MiB 2 chunks per rank pipeline the ring's 2(n-1) hops better
+        # (512 MiB 1226 vs 1237-1259 us; profiles/r01_ar_variants_n4.txt)
+        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("ring", 128 * MiB, 512 * MiB),
+                ("ring_p2", 512 * MiB, INF)]
     if coll == "reducescatter":
         if n == 2 or n >= 8:
             return [("direct", 0, INF)]
