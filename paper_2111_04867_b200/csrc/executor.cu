@@ -579,7 +579,7 @@ __device__ __forceinline__ bool ll_move(const char* src, char* dst, const char* 
       lb[u] = (int64_t)q * llcb + 16 * ll;
       vb[u] = idx < total ? (int)min((int64_t)8, cb - 8 * ll) : 0;
       if (in) w[u] = vb[u] ? ld_volatile_v4(in + lb[u]) : make_uint4(0, flag, 0, flag);
-      else v[u] = vb[u] ? ld_bytes(src + pb[u], vb[u]) : 0;
+      else v[u] = (vb[u] && src) ? ld_bytes(src + pb[u], vb[u]) : 0;
     }
     if (in) {
       u64 t0 = 0;
@@ -803,9 +803,9 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       // LL data steps (one copy of their code, so the kernel's executed footprint stays small):
       // thread 0 waits for the step's dependencies, if any (LL lines carry their own flags, so
       // there is nothing else to wait for); then every thread derives its slot pointers itself
-      const bool fast = LL && (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS ||
+      const bool ll_data = LL && (st.op == K_SEND || st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS ||
                                st.op == K_RCS || st.op == K_RRC_FUSED);
-      if (fast) {
+      if (ll_data) {
         if (st.dep_count) {
           if (tid == 0) {
             bool ok = true;
@@ -857,6 +857,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         const char* src = (st.op == K_RECV || st.op == K_RCS) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
         char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
         const bool red = st.op == K_RRC || st.op == K_RRCS || fz;
+        if (A.variant == 22 && st.op == K_SEND) src = nullptr;  // timing probe only: no source load
 #ifdef TACCL_TRACE_FINE
         // fine build: [2+4k] loads issued, [3+4k] waits done, [4+4k] stores issued (thread 0)
         const bool ok = ll_lines<kMaxRanks>(A.dtype, red, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt, l0, l1,
@@ -985,7 +986,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           break;
       }
       __syncthreads();
-      }  // !fast
+      }  // !ll_data
       if (tid == 0) {
         bool ok = true;  // post-dependencies: the other members of a fused chain
         for (int d = 0; d < st.post_count && ok; ++d) {

@@ -179,7 +179,8 @@ struct KArgs {
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
   int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT); timing probes
                            // only, results invalid: 9 = no fence before data flags, 20 = LL
-                           // kernel returns after its prologue, 21 = no arrival wait at exit
+                           // kernel returns after its prologue, 21 = no arrival wait at exit,
+                           // 22 = LL sends skip their source load (send zeros)
   int32_t dep_ctas;        // CTAs per dependent tb (<= split; CTA c runs pieces c, c+dep_ctas, ...)
   int32_t plan_smem;       // copy the rank's plan blob into shared memory at kernel start
   int32_t indep_cap;       // max pieces of an independent tb (bytes / min piece)
