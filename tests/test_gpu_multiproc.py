@@ -168,3 +168,96 @@ def test_watchdog_timeout_surfaces():
         p.join(timeout=60)
     assert res[0][2] is None and res[1][2] is None, res
     assert res[0][1] == 6
+
+
+# ---------------------------------------------------------------- full sizes, real peers, sampled
+
+FULL_CASES = [  # (coll, dtype, total bytes, input kind); bench.py's workload is the first
+    ("allgather", "bfloat16", 1 << 30, "bits"),
+    ("alltoall", "bfloat16", 1 << 30, "bits"),
+    ("allreduce", "int32", 1 << 28, "bits"),
+    ("allreduce", "bfloat16", 1 << 28, "uniform"),
+    ("reducescatter", "int32", 1 << 30, "bits"),
+]
+
+
+def _full_worker(rank, n, port, q):
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2111_04867_b200 import taccl
+    from paper_2111_04867_b200.generator import default_schedules
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    try:
+        comm = taccl.Comm(rank=rank, nranks=n, device=rank, scratch_bytes=2 * (1 << 30) + (64 << 20))
+        results = []
+        for coll, dtype, total, kind in FULL_CASES:
+            hs = [comm.load(t) for t in default_schedules(coll, n)]
+            tdt = {"int32": torch.int32, "bfloat16": torch.bfloat16}[dtype]
+            es = 4 if dtype == "int32" else 2
+            count = total // es if coll == "allreduce" else total // es // n
+            rows_in = n if coll in ("alltoall", "reducescatter") else 1
+            rows_out = n if coll in ("allgather", "alltoall") else 1
+            g = torch.Generator(device="cuda").manual_seed(211104867 + 1000 * 3 + rank)
+            if kind == "uniform":  # U[1,2) rounded to bf16
+                x = (torch.rand(rows_in * count, device="cuda", generator=g) + 1.0).to(tdt)
+            elif dtype == "int32":
+                x = torch.randint(-2**31, 2**31 - 1, (rows_in * count,), dtype=torch.int32, device="cuda", generator=g)
+            else:
+                x = torch.randint(-2**15, 2**15, (rows_in * count,), dtype=torch.int16, device="cuda",
+                                  generator=g).view(tdt)
+            out = torch.empty(rows_out * count, dtype=tdt, device="cuda")
+            out.view(torch.uint8).fill_(0xA5)
+            comm.run(coll, out, x)  # the bench's call: registered user buffers, size-selected schedule
+            torch.cuda.synchronize()
+            comm.check()
+            # the sampled problem (every collective acts element-wise along count): each rank's
+            # input rows at the sampled columns, exchanged over gloo, fed to the oracle
+            idx = torch.from_numpy(np.sort(np.random.default_rng(11).choice(count, 4096, replace=False))).cuda()
+            iv = torch.int32 if dtype == "int32" else torch.int16
+            xv, ov = x.view(iv), out.view(iv)
+            sub = torch.cat([xv[r * count:(r + 1) * count][idx] for r in range(rows_in)]).cpu().numpy()
+            subs = [None] * n
+            dist.all_gather_object(subs, sub)
+            got = torch.cat([ov[qq * count:(qq + 1) * count][idx] for qq in range(rows_out)]).cpu().numpy()
+            if kind == "uniform":  # north star: bf16 AR within 1e-2 relative of the fp64 sum
+                want = oracle.expected_allreduce_f64([s.view(np.uint16) for s in subs], "bfloat16")
+                rel = np.abs(oracle.collectives.bf16_to_f64(got.view(np.uint16)) - want) / np.abs(want)
+                ok = bool(rel.max() <= 1e-2)
+            else:
+                want = oracle.expected_outputs(coll, subs, "int32")[rank]
+                ok = bool(np.array_equal(got, want))
+            results.append(ok)
+            for h in hs:
+                comm.free(h)
+            del x, out
+        comm.destroy()
+        q.put((rank, results, None))
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_full_size_multiprocess_sampled(n):
+    # BASELINE.json's 1 GiB sizes through the real multi-process path (CUDA IPC peers, the
+    # default size-specialised sets, the launch configuration bench.py times), outputs checked
+    # at sampled elements against the oracle on the sampled slices of every rank's input
+    if NGPU < n:
+        pytest.skip(f"needs {n} GPUs, have {NGPU}")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_full_worker, args=(r, n, port, q)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(n)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, results, err in sorted(res, key=lambda x: x[0]):
+        assert err is None, f"rank {rank}: {err}"
+        assert all(results), f"rank {rank}: failing cases {[c for c, ok in zip(FULL_CASES, results) if not ok]}"
