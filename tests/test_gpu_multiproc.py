@@ -178,7 +178,10 @@ FULL_CASES = [  # (coll, dtype, total bytes, input kind); bench.py's workload is
     ("allreduce", "int32", 1 << 28, "bits"),
     ("allreduce", "bfloat16", 1 << 28, "uniform"),
     ("reducescatter", "int32", 1 << 30, "bits"),
+    ("allreduce", "float32", 1 << 28, "uniform"),
+    ("reducescatter", "bfloat16", 1 << 30, "uniform"),
 ]
+FULL_TOL = {"float32": 1e-6, "bfloat16": 1e-2}  # north star: relative to the fp64 sum
 
 
 def _full_worker(rank, n, port, q):
@@ -195,13 +198,13 @@ def _full_worker(rank, n, port, q):
         results = []
         for coll, dtype, total, kind in FULL_CASES:
             hs = [comm.load(t) for t in default_schedules(coll, n)]
-            tdt = {"int32": torch.int32, "bfloat16": torch.bfloat16}[dtype]
-            es = 4 if dtype == "int32" else 2
+            tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}[dtype]
+            es = 2 if dtype == "bfloat16" else 4
             count = total // es if coll == "allreduce" else total // es // n
             rows_in = n if coll in ("alltoall", "reducescatter") else 1
             rows_out = n if coll in ("allgather", "alltoall") else 1
             g = torch.Generator(device="cuda").manual_seed(211104867 + 1000 * 3 + rank)
-            if kind == "uniform":  # U[1,2) rounded to bf16
+            if kind == "uniform":  # U[1,2) (bf16: rounded)
                 x = (torch.rand(rows_in * count, device="cuda", generator=g) + 1.0).to(tdt)
             elif dtype == "int32":
                 x = torch.randint(-2**31, 2**31 - 1, (rows_in * count,), dtype=torch.int32, device="cuda", generator=g)
@@ -216,16 +219,19 @@ def _full_worker(rank, n, port, q):
             # the sampled problem (every collective acts element-wise along count): each rank's
             # input rows at the sampled columns, exchanged over gloo, fed to the oracle
             idx = torch.from_numpy(np.sort(np.random.default_rng(11).choice(count, 4096, replace=False))).cuda()
-            iv = torch.int32 if dtype == "int32" else torch.int16
+            iv = torch.int16 if dtype == "bfloat16" else torch.int32
             xv, ov = x.view(iv), out.view(iv)
             sub = torch.cat([xv[r * count:(r + 1) * count][idx] for r in range(rows_in)]).cpu().numpy()
             subs = [None] * n
             dist.all_gather_object(subs, sub)
             got = torch.cat([ov[qq * count:(qq + 1) * count][idx] for qq in range(rows_out)]).cpu().numpy()
-            if kind == "uniform":  # north star: bf16 AR within 1e-2 relative of the fp64 sum
-                want = oracle.expected_allreduce_f64([s.view(np.uint16) for s in subs], "bfloat16")
-                rel = np.abs(oracle.collectives.bf16_to_f64(got.view(np.uint16)) - want) / np.abs(want)
-                ok = bool(rel.max() <= 1e-2)
+            if kind == "uniform":  # north star: float AR/RS within FULL_TOL of the fp64 sum
+                fv = np.uint16 if dtype == "bfloat16" else np.float32
+                fs = [s.view(fv) for s in subs]
+                want = oracle.expected_allreduce_f64(fs, dtype) if coll == "allreduce" else \
+                    oracle.expected_reducescatter_f64(fs, dtype)[rank]
+                rel = np.abs(oracle.collectives.to_f64(got.view(fv), dtype) - want) / np.abs(want)
+                ok = bool(rel.max() <= FULL_TOL[dtype])
             else:
                 want = oracle.expected_outputs(coll, subs, "int32")[rank]
                 ok = bool(np.array_equal(got, want))
