@@ -27,6 +27,18 @@ __global__ void __launch_bounds__(512) ar_mc(float* mc, size_t n4_begin, size_t 
   }
 }
 
+__global__ void __launch_bounds__(512) ar_mc_bf16(float* mc, size_t n4_begin, size_t n4_end) {
+  for (size_t i = n4_begin + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4_end;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float* p = mc + 4 * i;
+    unsigned a, b, c, d;  // 8 bf16 per 16 B, fp32 accumulation in the switch
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p) : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+  }
+}
+
 __global__ void fill(float* p, size_t n, float v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -36,6 +48,11 @@ int main(int argc, char** argv) {
   int n = 0;
   RK(cudaGetDeviceCount(&n));
   if (argc > 1) n = atoi(argv[1]);
+  const bool bf16 = argc > 2 && argv[2][0] == 'b';
+  auto launch = [&](int g, int t, cudaStream_t s, float* p, size_t b, size_t e) {
+    if (bf16) ar_mc_bf16<<<g, t, 0, s>>>(p, b, e);
+    else ar_mc<<<g, t, 0, s>>>(p, b, e);
+  };
   const size_t max_bytes = (size_t)1 << 30;
   int mc_ok = 0;
   CUdevice d0;
@@ -94,15 +111,19 @@ int main(int argc, char** argv) {
   // correctness at 64 MiB: rank i holds i+1 everywhere; after one AR every element = n(n+1)/2
   {
     const size_t S = 64u << 20, nf = S / 4, n4 = nf / 4;
-    for (int i = 0; i < n; ++i) { RK(cudaSetDevice(i)); fill<<<grid, threads, 0, st[i]>>>((float*)uc[i], nf, (float)(i + 1)); }
+    for (int i = 0; i < n; ++i) { RK(cudaSetDevice(i));
+      float v = (float)(i + 1);
+      if (bf16) { unsigned u = *(unsigned*)&v >> 16; u |= u << 16; v = *(float*)&u; }
+      fill<<<grid, threads, 0, st[i]>>>((float*)uc[i], nf, v); }
     sync_all();
     for (int i = 0; i < n; ++i) {
       RK(cudaSetDevice(i));
-      ar_mc<<<grid, threads, 0, st[i]>>>((float*)mcp[i], n4 * i / n, n4 * (i + 1) / n);
+      launch(grid, threads, st[i], (float*)mcp[i], n4 * i / n, n4 * (i + 1) / n);
       RK(cudaGetLastError());
     }
     sync_all();
-    const float want = n * (n + 1) / 2.0f;
+    float want = n * (n + 1) / 2.0f;
+    if (bf16) { unsigned u = *(unsigned*)&want >> 16; u |= u << 16; want = *(float*)&u; }
     size_t bad = 0;
     std::vector<float> h(nf);
     for (int i = 0; i < n; ++i) {
@@ -110,7 +131,7 @@ int main(int argc, char** argv) {
       RK(cudaMemcpy(h.data(), (void*)uc[i], S, cudaMemcpyDeviceToHost));
       for (size_t k = 0; k < nf; ++k) bad += h[k] != want;
     }
-    printf("correctness 64 MiB fp32 n=%d: %s (%zu bad of %zu)\n", n, bad ? "FAIL" : "ok", bad, nf * n);
+    printf("correctness 64 MiB %s n=%d: %s (%zu bad of %zu words)\n", bf16 ? "bf16" : "fp32", n, bad ? "FAIL" : "ok", bad, nf * n);
   }
   // timing: K back-to-back calls per GPU (no cross-GPU barrier between calls: a bandwidth probe),
   // time = max over GPUs of the per-call event time
@@ -122,7 +143,7 @@ int main(int argc, char** argv) {
       for (int k = 0; k < K; ++k)
         for (int i = 0; i < n; ++i) {
           RK(cudaSetDevice(i));
-          ar_mc<<<grid, threads, 0, st[i]>>>((float*)mcp[i], n4 * i / n, n4 * (i + 1) / n);
+          launch(grid, threads, st[i], (float*)mcp[i], n4 * i / n, n4 * (i + 1) / n);
         }
       for (int i = 0; i < n; ++i) { RK(cudaSetDevice(i)); RK(cudaEventRecord(e1[i], st[i])); }
       sync_all();
@@ -131,7 +152,7 @@ int main(int argc, char** argv) {
     for (int i = 0; i < n; ++i) { float ms; RK(cudaEventElapsedTime(&ms, e0[i], e1[i])); worst = ms > worst ? ms : worst; }
     const double us = worst * 1e3 / K;
     const double busbw = (double)S / (us * 1e-6) * 2.0 * (n - 1) / n / 1e9;
-    printf("nvls allreduce fp32 n=%d S=%10zu  %9.1f us  busbw %6.1f GB/s\n", n, S, us, busbw);
+    printf("nvls allreduce %s n=%d S=%10zu  %9.1f us  busbw %6.1f GB/s\n", bf16 ? "bf16" : "fp32", n, S, us, busbw);
   }
   return 0;
 }
