@@ -197,6 +197,7 @@ def main():
     inp = torch.randint(-32768, 32767, (count,), dtype=torch.int16, device="cuda", generator=g).view(torch.bfloat16)
     out = torch.empty(n * count, dtype=torch.bfloat16, device="cuda")
     comm.register(out)
+    comm.register(inp)
     stream = torch.cuda.current_stream()
     steps = a.steps or (6000 if n == 1 else 2500)  # timed region >= ~2 s for the clock samples
 
@@ -209,12 +210,14 @@ def main():
         comm.all_gather(out, inp)
     barrier()
     comm.check()
-    # correctness of what we time (sampled): own chunk and one peer chunk
-    ref = torch.randint(-32768, 32767, (count,), dtype=torch.int16, device="cuda",
-                        generator=torch.Generator(device="cuda").manual_seed(211104867 + (rank + 1) % n)).view(torch.bfloat16)
+    # correctness of what we time, every element: out chunk s must be rank s's input (the
+    # Allgather definition), regenerated here from rank s's seed
     ob = out.view(torch.int16)  # compare raw bits (random patterns include NaNs)
-    assert torch.equal(ob[rank * count:(rank + 1) * count], inp.view(torch.int16))
-    assert torch.equal(ob[((rank + 1) % n) * count:((rank + 1) % n + 1) * count], ref.view(torch.int16))
+    for src in range(n):
+        ref = torch.randint(-32768, 32767, (count,), dtype=torch.int16, device="cuda",
+                            generator=torch.Generator(device="cuda").manual_seed(211104867 + src))
+        assert torch.equal(ob[src * count:(src + 1) * count], ref), f"rank {rank}: chunk {src} differs"
+        del ref
 
     launches0 = taccl.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -94,61 +94,100 @@ taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, c
                                size_t* needed);
 
 /* ---- communicator (one per process) ---------------------------------------------------- */
+/* The paper's runtime reuses NCCL's communicator and transports (§6); this
+ * build replaces them with one arena per rank that peers map over NVLink (CUDA IPC), so the
+ * "connections" between threadblocks of different GPUs are plain loads and
+ * stores into peer HBM plus flag words. The library owns the arena: the paper's runtime
+ * "allocates ... scratch buffers" while the user preallocates input/output. */
 
 /* One rank per process on `cuda_device`. Allocates the rank's arena in device memory:
  * flags plus `scratch_bytes` of scratch/staging (0 = default 256 MiB, env
- * TACCL_SCRATCH_BYTES overrides). Peers are unusable until taccl_comm_set_peers. */
+ * TACCL_SCRATCH_BYTES overrides). Peers are unusable until taccl_comm_set_peers.
+ * Errors: INVALID_ARG (rank out of range, already initialized), UNSUPPORTED (nranks outside
+ * [1, TACCL_MAX_RANKS]), CUDA (allocation). */
 taccl_result_t taccl_comm_init(int rank, int nranks, int cuda_device, size_t scratch_bytes);
 
 /* All `nranks` ranks emulated in this process on one device (tests and single-GPU runs of
  * multi-rank schedules): one launch runs every rank's threadblocks, peers are the other
- * ranks' arenas in the same HBM. Use taccl_run_emulated. */
+ * ranks' arenas in the same HBM. Use taccl_run_emulated. Errors as taccl_comm_init. */
 taccl_result_t taccl_comm_init_emulated(int nranks, int cuda_device, size_t scratch_bytes);
 
-/* Writes this rank's arena IPC handle blob (TACCL_HANDLE_BYTES) to `out`; *len = size. */
+/* Writes this rank's arena IPC handle blob (TACCL_HANDLE_BYTES) to `out`; *len = size.
+ * Errors: NOT_INITIALIZED (no multi-process communicator), INVALID_ARG (null). */
 taccl_result_t taccl_comm_export_handle(void* out, size_t* len);
 
 /* `all_handles` = nranks blobs of `len_each` bytes in rank order (from an all-gather of
- * taccl_comm_export_handle). Opens the peers' arenas. */
+ * taccl_comm_export_handle). Opens the peers' arenas. Errors: INVALID_ARG (a blob is not
+ * rank q's arena, arena sizes differ), CUDA (IPC open). */
 taccl_result_t taccl_comm_set_peers(const void* all_handles, size_t len_each);
 
-/* Frees algorithms, buffers registrations, peer mappings and the arena. */
+/* Frees algorithms, buffers registrations, peer mappings and the arena (synchronizes the
+ * device first). */
 taccl_result_t taccl_comm_destroy(void);
 
 /* ---- user buffer registration (zero-copy direct stores) -------------------------------- */
 
-/* Collective, like NCCL window registration: every rank registers its own buffer of the
+/* The user preallocates the input and output buffers; a send stores
+ * straight into the matched receive's destination on the peer, so the
+ * peer's output must be mapped here first.
+ * Collective, like NCCL window registration: every rank registers its own buffer of the
  * same role in the same order. Step 1: export a blob for [ptr, ptr+bytes) (any pointer
  * inside a cudaMalloc'd allocation). Step 2: pass all ranks' blobs (rank order) to
  * taccl_register_buffer. Afterwards a taccl_run whose recvbuf lies inside [ptr, ptr+bytes)
  * stores into the peers' registered buffers at the same offset, and one whose sendbuf lies
  * inside a registered buffer runs in pull mode (receive-reduces fed by a peer's input load it
  * in place over NVLink; the call then completes only after every reader is done with this
- * rank's sendbuf). An unregistered sendbuf is pushed (no pull mode). All ranks
- * of a call must agree: either every rank's sendbuf lies in a registered buffer or none does
- * (a mismatch ends in TACCL_ERR_TIMEOUT from the watchdog, reported by taccl_check). */
+ * rank's sendbuf). An unregistered sendbuf is pushed (no pull mode).
+ * Registering the same range again replaces the earlier mapping; lookups use the latest
+ * registration covering a pointer. All ranks of a call must agree on pull mode: either every
+ * rank's sendbuf lies in a registered buffer (and no rank runs in place) or none does. A
+ * disagreement is detected by the entry handshake before any data moves: the sender aborts
+ * and taccl_check returns INVALID_ARG naming it (its receiver then surfaces TIMEOUT).
+ * Errors: NOT_INITIALIZED, INVALID_ARG (not device memory, range beyond its allocation,
+ * blob mismatch, sizes differ across ranks), CUDA (IPC). */
 taccl_result_t taccl_buffer_export(const void* ptr, size_t bytes, void* out, size_t* len);
 taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* all_blobs,
                                      size_t len_each);
+/* Local: drop the registration that starts at `ptr` (before the buffer is freed).
+ * Errors: NOT_INITIALIZED, NOT_REGISTERED (no registration starts at ptr). */
+taccl_result_t taccl_unregister_buffer(const void* ptr);
 
 /* ---- north-star calls ------------------------------------------------------------------ */
 
-/* Parse, check (direct-store mode) and upload a schedule. The algorithm is registered
- * under (coll, nranks, [minBytes, maxBytes)) for selection by taccl_run; `*out` may be
- * NULL. The text is copied. Requires an initialized communicator with matching nranks. */
+/* taccl_load_algo: the paper's lowered TACCL-EF program (§6.1: buffers,
+ * threadblocks with one send and one receive peer, steps with dependencies) arrives as
+ * text (EF v1, docs/SCHEDULE.md). It is parsed, checked in direct-store mode (structure,
+ * matching, acyclicity, races, and the collective's postcondition "each chunk reaches its
+ * destination GPUs as specified by the collective"; App. B
+ * PAPER.md:1324-1330) and planned for the device. The algorithm is registered under
+ * (coll, nranks, [minBytes, maxBytes)) for selection by taccl_run — the paper keeps
+ * size-specialised algorithms per collective. `*out` may be NULL.
+ * Ownership: the text is copied (not retained); the library owns the device plan until
+ * taccl_free or taccl_comm_destroy. Requires an initialized communicator whose nranks
+ * matches. Errors: INVALID_SCHEDULE ("<class>: <message>", first failing check),
+ * INVALID_ARG (nranks mismatch, null), UNSUPPORTED (limits above), CUDA. */
 taccl_result_t taccl_load_algo(const char* schedule_text, size_t len, taccl_algo_t* out);
 
-/* Run the collective with the loaded algorithm selected by (coll, nranks, S) where S =
+/* taccl_run: one collective call with NCCL-compatible semantics ("the
+ * same API as NCCL"), executed "in a single kernel launch" with the loaded
+ * algorithm selected by (coll, nranks, S) where S =
  * output bytes (AG), per-rank send bytes (A2A), buffer bytes (AR), send bytes (RS). NCCL
  * count convention: AG count = elements per rank (recvbuf holds nranks*count), A2A count =
  * elements per peer (both buffers hold nranks*count), AR count = total elements, RS count =
- * elements per rank (sendbuf holds nranks*count, recvbuf count). sendbuf/recvbuf are
- * device pointers; recvbuf must be registered (taccl_register_buffer) unless emulated;
- * a registered sendbuf enables pull mode (TACCL_PULL=0 disables it).
+ * elements per rank (sendbuf holds nranks*count, recvbuf count). Chunks are equal-sized
+ * (PAPER.md:742-744): the input splits into N_in chunks of c_e = E_in / N_in elements.
+ * sendbuf/recvbuf are user-owned device pointers; recvbuf must be
+ * registered (taccl_register_buffer) unless emulated or nranks == 1; a registered sendbuf
+ * enables pull mode (TACCL_PULL=0 disables it). sendbuf is read-only for the call; recvbuf
+ * is valid once `stream` passes the call.
  * In-place / overlapping buffers are accepted (the input is first copied, on `stream`, to a
  * private arena region; INVALID_ARG if the arena is too small). Enqueues ONE kernel on `stream`
  * (a cudaStream_t; NULL = legacy default stream); returns without synchronizing. The
- * call is CUDA-graph capturable (epochs live on the device). */
+ * call is CUDA-graph capturable (epochs live on the device).
+ * Errors: NOT_INITIALIZED, INVALID_ARG (null buffer, count not divisible into N_in chunks
+ * (reading G2), arena too small), NO_ALGO (no loaded algorithm for (coll, nranks, S)),
+ * NOT_REGISTERED (recvbuf), UNSUPPORTED (launch needs more co-resident CTAs than the device
+ * holds), CUDA (launch). Device-side failures surface later through taccl_check. */
 taccl_result_t taccl_run(taccl_coll_t coll, const void* sendbuf, void* recvbuf, size_t count,
                          taccl_dtype_t dtype, void* stream);
 
@@ -160,10 +199,12 @@ taccl_result_t taccl_run_emulated(taccl_coll_t coll, const void* const* sendbufs
 /* Same as taccl_run with HOST buffers: copies sendbuf H2D, runs, copies recvbuf D2H on
  * `stream` through library-owned device buffers, and synchronizes the stream. For
  * end-to-end measurements; pinned host memory gives full PCIe bandwidth. */
-taccl_result_t taccl_run_host(taccl_coll_t coll, const void* host_sendbuf, void* host_recvbuf,
+taccl_result_t taccl_run_host(taccl_coll_t coll, const void* host_send, void* host_recv,
                               size_t count, taccl_dtype_t dtype, void* stream);
 
-/* Unregister and free an algorithm (invalid while a run using it is in flight). */
+/* taccl_free: release an algorithm and its device plan (the runtime-owned half of the
+ * paper's buffer split). Invalid while a run using it is in flight
+ * (synchronize the stream first). Errors: INVALID_ARG (unknown or already freed handle). */
 taccl_result_t taccl_free(taccl_algo_t algo);
 
 /* ---- introspection (tests, bench) ----------------------------------------------------- */

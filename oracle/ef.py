@@ -73,6 +73,9 @@ class Program:
     max_bytes: float
     inplace: int
     gpus: list = field(default_factory=list)
+    # set by instances.expand_instances: chunk k' of the expanded program is subchunk k' % m of
+    # the original chunk k' // m (reading G3's floor split); 1 = ordinary equal chunks
+    subchunks: int = 1
 
 
 def _int(el, key, lo=None):

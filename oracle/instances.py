@@ -4,9 +4,11 @@ PAPER.md:785–789 (§6.2, "Instances"): "subdividing each chunk into n subchunk
 the same path as the parent chunk. All groups of instructions and their threadblocks are
 duplicated n times and executed in parallel."
 
-Reading G3: subchunk j of chunk k becomes chunk k*m + j of the expanded buffer (so the
-expanded program is again a program over equal chunks, with chunks_per_rank p*m, and the
-collective's chunk-id layout is preserved); a `cnt=q` step becomes q single-chunk steps
+Reading G3: subchunk j of chunk k is the element range [floor(j*c_e/m), floor((j+1)*c_e/m))
+of chunk k (c_e need not be a multiple of m: the subchunks then differ by one element) and
+becomes chunk k*m + j of the expanded program (chunks_per_rank p*m, so the collective's
+chunk-id layout is preserved; `Program.subchunks = m` tells `simulate.run` that chunk k' names
+that element range of the original chunk k' // m rather than an equal m-th); a `cnt=q` step becomes q single-chunk steps
 (instance j of its q chunks are strided, so one contiguous range cannot name them);
 instance j of tb t is tb t*m + j on channel chan*m + j, and a dependency on step k of tb t
 becomes a dependency on the last expanded step of k in the same instance.
@@ -24,7 +26,9 @@ def expand_instances(prog: Program) -> Program:
     if m == 1:
         return copy.deepcopy(prog)
     out = Program(prog.name + f"_x{m}", prog.coll, prog.nranks, prog.chunks_per_rank * m, 1,
-                  prog.min_bytes, prog.max_bytes, prog.inplace)
+                  prog.min_bytes, prog.max_bytes, prog.inplace, subchunks=prog.subchunks * m)
+    if prog.subchunks != 1:
+        raise ValueError("expand_instances: the program is already expanded")
     for g in prog.gpus:
         ng = Gpu(g.id, g.i_chunks * m, g.o_chunks * m, g.s_chunks * m)
         # last expanded index of every original step

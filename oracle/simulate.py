@@ -160,25 +160,40 @@ def run(prog: Program, inputs, dtype: str, graph=None, order=None):
     """Numeric execution. inputs: one 1-D array per rank (dtype storage per DTYPES, bf16 as
     uint16 bits). Returns the per-rank output arrays."""
     graph, order = _prepare(prog, graph, order)
-    n, p = prog.nranks, prog.chunks_per_rank
+    n, p, m = prog.nranks, prog.chunks_per_rank, prog.subchunks
     np_dt, _ = DTYPES[dtype]
     e_in = inputs[0].size
     count = e_in // n if prog.coll in ("alltoall", "reducescatter") else e_in
-    ce = chunk_elems(prog.coll, n, p, count)
+    # chunk q of an instance-expanded program (m > 1) is subchunk q % m of the original chunk
+    # q // m: elements [floor(j*c_e/m), floor((j+1)*c_e/m)) of it (reading G3, PAPER.md:785-789)
+    ce = chunk_elems(prog.coll, n, p // m, count)
+
+    def span(q):
+        k, j = divmod(q, m)
+        return k * ce + (j * ce) // m, k * ce + ((j + 1) * ce) // m
     bufs = []
     for g in prog.gpus:
         x = np.ascontiguousarray(inputs[g.id], dtype=np_dt)
-        if x.size != g.i_chunks * ce:
-            raise ValueError(f"rank {g.id}: input has {x.size} elements, want {g.i_chunks * ce}")
-        o = np.full(g.o_chunks * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
-        s = np.full(g.s_chunks * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
+        if x.size != g.i_chunks // m * ce:
+            raise ValueError(f"rank {g.id}: input has {x.size} elements, want {g.i_chunks // m * ce}")
+        o = np.full(g.o_chunks // m * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
+        s = np.full(g.s_chunks // m * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
         bufs.append({"i": x, "o": o, "s": s})
 
     def read(buf, off, cnt, where):
-        return buf[off * ce:(off + cnt) * ce].copy()
+        if m == 1:
+            return buf[off * ce:(off + cnt) * ce].copy()
+        return np.concatenate([buf[slice(*span(q))] for q in range(off, off + cnt)])
 
     def write(buf, off, cnt, vals):
-        buf[off * ce:(off + cnt) * ce] = vals
+        if m == 1:
+            buf[off * ce:(off + cnt) * ce] = vals
+            return
+        at = 0
+        for q in range(off, off + cnt):
+            a, b = span(q)
+            buf[a:b] = vals[at:at + b - a]
+            at += b - a
 
     def reduce(mine, got, where):
         return add(mine, got, dtype)

@@ -28,6 +28,16 @@ namespace {
 
 using u64 = unsigned long long;
 
+// Timing probes (KArgs.variant 9 / 20 / 21 / 22) knowingly break the protocol (no release fence,
+// early return, no arrival wait, zero payload). They exist only in builds with -DTACCL_PROBES
+// (python -m paper_2111_04867_b200.build -DTACCL_PROBES --out=...); in the default library
+// PROBE(v) is constant false, so no environment variable can reach them.
+#ifdef TACCL_PROBES
+#define PROBE(v) (A.variant == (v))
+#else
+#define PROBE(v) false
+#endif
+
 __device__ __forceinline__ u64 ld_acquire_sys(const u64* p) {
   u64 v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -617,6 +627,10 @@ __device__ __forceinline__ void ll_copy(char* dst, const char* src, int64_t n) {
   if ((((uintptr_t)dst | (uintptr_t)src | (uintptr_t)n) & 15) == 0) {
     for (int64_t i = tid; i < n / 16; i += nt)
       st_v4(reinterpret_cast<int4*>(dst) + i, ld_cg(reinterpret_cast<const int4*>(src) + i));
+  } else if ((((uintptr_t)dst | (uintptr_t)src) & 7) == 0) {  // line-aligned ranges (8-byte cuts)
+    for (int64_t i = tid; i < n / 8; i += nt)
+      reinterpret_cast<u64*>(dst)[i] = __ldcg(reinterpret_cast<const u64*>(src) + i);
+    for (int64_t b = (n & ~(int64_t)7) + tid; b < n; b += nt) dst[b] = src[b];
   } else {
     for (int64_t b = tid; b < n; b += nt) dst[b] = src[b];
   }
@@ -687,6 +701,15 @@ __device__ void record_error(const Ctx& c, int what, int step) {
 
 __device__ __forceinline__ void st_release_sys(u64* p, u64 v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Sender side of the entry handshake: wait until the receiver entered this call (its ready
+// word carries epoch << 1 | its pull mode). 0 = ready, 1 = timeout, 2 = the receiver's pull
+// mode differs from ours (ranks disagree on sendbuf registration / in-place: a pulled receive
+// would read an input nobody keeps valid, a pushed one a staging slot nobody fills).
+__device__ __forceinline__ int wait_ready(const u64* p, u64 epoch, int pull, u64 timeout_ns) {
+  if (!wait_ge<true>(p, epoch << 1, timeout_ns)) return 1;
+  const u64 v = ld_acquire_sys(p);
+  return ((v >> 1) == epoch && (int)(v & 1) != (pull & 1)) ? 2 : 0;
 }
 // a send the receiver loads in place (pull mode; direct kernel only): it reads this rank's
 // input and the plan marked its matched receive-reduce as reading it in place (st.poff >= 0)
@@ -767,7 +790,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   char* const my_staged = R.arena + parity_off;
   const int64_t ll_cb = 16 * ((cbytes + 7) / 8);  // LL bytes per chunk slot
   const unsigned ll_flag = (unsigned)c.epoch;
-  if (LL && A.variant == 20) return;  // timing probe only: launch + prologue
+  if (LL && PROBE(20)) return;  // timing probe only: launch + prologue
   u64* const trace = (A.trace && tid == 0 && blockIdx.x < A.trace_ctas) ? A.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   if (trace) {
     trace[0] = t_entry;
@@ -775,20 +798,23 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
     trace[kTraceSlots - 2] = ((u64)R.rank << 32) | ((u64)c.t << 16) | (u64)c0;
   }
 
+  // entry word: this call's epoch and whether this rank runs in pull mode; a sender whose own
+  // mode differs aborts with kErrPullMismatch (taccl_check) before it moves any data
+  const u64 ready_word = (c.epoch << 1) | (u64)(A.pull & 1);
   // entry handshake: tell our sender we are in this call, for every piece this CTA owns, up
   // front — this rank's previous call has fully completed (stream order), so nothing of it
   // can still read the buffers the sender is about to store into; announcing per piece as
   // it starts would throttle the sender to this CTA's per-piece progress.
   if (!LL && tb.recv >= 0 && tid == 0 && !A.ready_per_piece) {
     u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
-    for (int j = c0; j < nsplit; j += ct) st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
+    for (int j = c0; j < nsplit; j += ct) st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), ready_word);
   }
   unsigned fin_early = 0;
   for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
     if (!LL && tb.recv >= 0 && tid == 0 && A.ready_per_piece) {  // A/B knob: announce as each piece starts
       u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
-      st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), c.epoch);
+      st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), ready_word);
     }
     bool sender_ready = false;
 
@@ -857,7 +883,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         const char* src = (st.op == K_RECV || st.op == K_RCS) ? nullptr : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
         char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
         const bool red = st.op == K_RRC || st.op == K_RRCS || fz;
-        if (A.variant == 22 && st.op == K_SEND) src = nullptr;  // timing probe only: no source load
+        if (PROBE(22) && st.op == K_SEND) src = nullptr;  // timing probe only: no source load
 #ifdef TACCL_TRACE_FINE
         // fine build: [2+4k] loads issued, [3+4k] waits done, [4+4k] stores issued (thread 0)
         const bool ok = ll_lines<kMaxRanks>(A.dtype, red, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt, l0, l1,
@@ -878,12 +904,15 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       } else {
       if (tid == 0) {
         bool ok = true;
+        int what = st.op;  // error detail: the step's op, or kErrPullMismatch
         for (int d = 0; d < st.dep_count && ok; ++d) {
           const int dt = deps[2 * (st.dep_begin + d)], dk = deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
-        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) && !sender_ready && !pulled(A, st)) {
-          ok = wait_ge<true>(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.timeout_ns);
+        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) && !sender_ready) {
+          const int w = wait_ready(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.pull, A.timeout_ns);
+          ok = w == 0;
+          what = w == 2 ? kErrPullMismatch : st.op;
           sender_ready = true;
         }
         // staged (LL) mode: no data flags, every line carries its own (ll_lines)
@@ -910,13 +939,17 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           for (int f = 0; f < st.fwd_count && ok; ++f) {
             const int* fw = fused + st.fwd_begin + 6 * f;  // peer, chan, rbuf, roff, roff2, seq
             // entry handshake of that send's connection: its receiver is in this call
-            if (!LL) ok = wait_ge<true>(my_ready + flag_slot(fw[0], fw[1], j), c.epoch, A.timeout_ns);
+            if (!LL) {
+              const int w = wait_ready(my_ready + flag_slot(fw[0], fw[1], j), c.epoch, A.pull, A.timeout_ns);
+              ok = w == 0;
+              what = w == 2 ? kErrPullMismatch : st.op;
+            }
             s_fwd[f] = LL ? R.peer_arena[fw[0]] + parity_off + (int64_t)fw[4] * ll_cb
                           : remote_base(c, fw[0], fw[2]) + (int64_t)fw[3] * cbytes;
           }
         }
         if (!ok) {
-          record_error(c, st.op, k);
+          record_error(c, what, k);
           s_abort = 1;
         }
         if (tr) trace[3 + 4 * k] = globaltimer();
@@ -925,10 +958,15 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       if (s_abort) return;
 
       if constexpr (LL) {
-        if (st.op == K_CPY) {
+        if (st.op == K_CPY) {  // piece j = the same line range of every chunk as the LL data
+          // steps use (a dependency on piece j of a receive or send then covers exactly these bytes)
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
-          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { ll_copy(dst + off, src + off, len); });
+          const int64_t nl = (cbytes + 7) / 8;
+          const int64_t b0 = 8 * (int64_t)((unsigned)nl * (unsigned)j / (unsigned)nsplit);
+          const int64_t b1 = min(cbytes, 8 * (int64_t)((unsigned)nl * (unsigned)(j + 1) / (unsigned)nsplit));
+          if (b1 > b0)
+            for (int q = 0; q < st.cnt; ++q) ll_copy(dst + q * cbytes + b0, src + q * cbytes + b0, b1 - b0);
         }
       } else switch (st.op) {
         case K_SEND:
@@ -1020,7 +1058,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           // all threads' peer stores are ordered before this by bar.sync (causality order);
           // the system-scope acq_rel fence makes them visible before the flag (cumulativity;
           // K_PUB: the chain members' stores, ordered by their fence + our acquire of done)
-          if (A.variant != 9) asm volatile("fence.acq_rel.sys;" ::: "memory");  // 9: timing probe only
+          if (!PROBE(9)) asm volatile("fence.acq_rel.sys;" ::: "memory");  // 9: timing probe only
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j),
                          E | (u64)((st.op == K_RRCS || st.op == K_RCS ? st.fwd_seq : st.seq) + 1));
@@ -1058,7 +1096,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
       const unsigned want = (unsigned)R.ncta - 1;
       volatile unsigned* fin = &ctrl->finished;
       const u64 t0 = globaltimer();
-      while (fin_early < want && A.variant != 21 && *fin < want)  // 21: timing probe only (no arrival wait)
+      while (fin_early < want && !PROBE(21) && *fin < want)  // 21: timing probe only (no arrival wait)
         if (globaltimer() - t0 > A.timeout_ns) {
           record_error(c, K_NOP, -1);
           break;

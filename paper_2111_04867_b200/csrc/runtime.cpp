@@ -66,6 +66,7 @@ struct Algo {
   std::vector<std::vector<int>> indep;    // per rank, per tb
   std::vector<int> wsum;        // per rank
   int fused_chains = 0;
+  bool has_pull = false;  // some send of the direct plan is read in place (pull mode applies)
 };
 
 struct Reg {
@@ -386,7 +387,9 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   // the direct kernel; TACCL_PULL=0 disables it
   // which receive-reduces pull is decided per step by the plan (TACCL_PULL_KINDS at load,
   // default plain rrcs only: plan.cpp); TACCL_PULL=0 turns the mode off
-  A.pull = (peer_in && !G.staged && g.nranks > 1 && env_size("TACCL_PULL", 1) != 0) ? 1 : 0;
+  // (only for plans with pulled steps: for the others the mode changes nothing, and a rank
+  // running in place next to one that does not is legal)
+  A.pull = (peer_in && a->has_pull && !G.staged && g.nranks > 1 && env_size("TACCL_PULL", 1) != 0) ? 1 : 0;
   std::string err;
   const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -461,8 +464,8 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
       for (int q = 0; q < n; ++q) peer_in[0][q] = g.peer_arena[q] + (sb - g.peer_arena[g.rank]);
       have_in = true;
     } else {
-      for (const Reg& rg : g.regs)
-        if ((uintptr_t)sb >= rg.lo && (uintptr_t)sb + ib <= rg.hi) {
+      for (auto it = g.regs.rbegin(); it != g.regs.rend(); ++it)
+        if (const Reg& rg = *it; (uintptr_t)sb >= rg.lo && (uintptr_t)sb + ib <= rg.hi) {
           for (int q = 0; q < n; ++q) peer_in[0][q] = rg.peer_base[q] + ((uintptr_t)sb - rg.lo);
           have_in = true;
           break;
@@ -509,6 +512,10 @@ taccl_result_t taccl_check(void) {
   for (size_t i = 0; i < g.arenas.size(); ++i) {
     Ctrl c;
     CUDA_TRY(cudaMemcpy(&c, g.arenas[i] + kOffCtrl, sizeof(c), cudaMemcpyDeviceToHost));
+    if (c.error && c.err_what == kErrPullMismatch)
+      return fail(TACCL_ERR_INVALID_ARG, "rank " + std::to_string(c.err_rank) + " tb " + std::to_string(c.err_tb) +
+                                             ": its receiver runs in the other pull mode (every rank's sendbuf must be"
+                                             " registered, or none; in-place calls on all ranks or none)");
     if (c.error)
       return fail(TACCL_ERR_TIMEOUT, "device watchdog: rank " + std::to_string(c.err_rank) + " tb " +
                                          std::to_string(c.err_tb) + " step " + std::to_string(c.err_step) +
@@ -706,7 +713,20 @@ taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* 
     if (rc) return rc;
     rg.peer_base[q] = base + b.offset;
   }
+  // the same range registered again (a freed buffer's address came back) replaces the old
+  // mapping; lookups take the latest registration that covers a pointer
+  g.regs.erase(std::remove_if(g.regs.begin(), g.regs.end(), [&](const Reg& o) { return o.lo == rg.lo && o.hi == rg.hi; }),
+               g.regs.end());
   g.regs.push_back(rg);
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_unregister_buffer(const void* ptr) {
+  if (!g.up || g.emulated) return fail(TACCL_ERR_NOT_INITIALIZED, "no multi-process communicator");
+  const size_t before = g.regs.size();
+  g.regs.erase(std::remove_if(g.regs.begin(), g.regs.end(), [&](const Reg& o) { return o.lo == (uintptr_t)ptr; }),
+               g.regs.end());
+  if (g.regs.size() == before) return fail(TACCL_ERR_NOT_REGISTERED, "no registration starts at this pointer");
   return TACCL_SUCCESS;
 }
 
@@ -761,6 +781,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->max_stage_chunks = std::max(a->max_stage_chunks, plans[r].stage_chunks);
     a->max_stage2_chunks = std::max(a->max_stage2_chunks, plans[r].stage2_chunks);
     a->fused_chains += plans[r].fused_chains;
+    for (const KStep& k : plans[r].steps) a->has_pull = a->has_pull || (k.op == K_SEND && k.poff >= 0);
     if (a->nranks == 1 && plans[r].steps.size() == 1) {
       const KStep& k = plans[r].steps[0];
       if (k.op == K_CPY && k.srcbuf == KB_I && k.dstbuf == KB_O && k.dep_count == 0 &&

@@ -146,6 +146,8 @@ TACCL_HD inline size_t flag_slot(int peer, int chan, int j) {
   return ((size_t)peer * kMaxChan + chan) * kMaxSplit + j;
 }
 
+constexpr int kErrPullMismatch = 100;  // Ctrl.err_what: ranks disagree on pull mode
+
 struct Ctrl {
   unsigned long long epoch;
   unsigned int finished;

@@ -52,6 +52,7 @@ def lib():
             "taccl_comm_destroy": ([], c_int),
             "taccl_buffer_export": ([c_vp, c_size, c_vp, ctypes.POINTER(c_size)], c_int),
             "taccl_register_buffer": ([c_vp, c_size, c_vp, c_size], c_int),
+            "taccl_unregister_buffer": ([c_vp], c_int),
             "taccl_load_algo": ([c_cp, c_size, ctypes.POINTER(c_vp)], c_int),
             "taccl_run": ([c_int, c_vp, c_vp, c_size, c_int, c_vp], c_int),
             "taccl_run_emulated": ([c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_size, c_int, c_vp], c_int),
@@ -128,7 +129,6 @@ class Comm:
     def __init__(self, rank=0, nranks=1, device=0, scratch_bytes=0, emulated=False, group=None):
         self.rank, self.nranks, self.device, self.emulated = rank, nranks, device, emulated
         self.group = group
-        self._registered = {}
         if emulated:
             _check(lib().taccl_comm_init_emulated(nranks, device, scratch_bytes))
         else:
@@ -159,28 +159,34 @@ class Comm:
         _check(lib().taccl_free(h))
 
     def register(self, t):
-        """Collective: map tensor `t`'s storage on every rank — a zero-copy receive target
-        (outputs) or an in-place pull source (inputs, pull mode)."""
+        """Collective (every rank, same role, same order — like NCCL window registration): map
+        tensor `t`'s storage on every rank, as a zero-copy receive target (outputs) or an
+        in-place pull source (inputs, pull mode). Explicit: run() never registers, so no rank
+        can enter the exchange while another skips it. Registering a storage range again
+        replaces the earlier mapping (a freed tensor's address may come back with different
+        peer addresses)."""
         if self.emulated or self.nranks == 1:
             return
-        key = (t.untyped_storage().data_ptr(), t.untyped_storage().nbytes())
-        if key in self._registered:
-            return
-        ptr, nbytes = key
+        ptr, nbytes = t.untyped_storage().data_ptr(), t.untyped_storage().nbytes()
         blob = ctypes.create_string_buffer(HANDLE_BYTES)
         n = ctypes.c_size_t(0)
         _check(lib().taccl_buffer_export(ctypes.c_void_p(ptr), nbytes, blob, ctypes.byref(n)))
         allb = self._all_gather_bytes(blob.raw[:n.value])
         _check(lib().taccl_register_buffer(ctypes.c_void_p(ptr), nbytes, allb, HANDLE_BYTES))
-        self._registered[key] = True
+
+    def unregister(self, t):
+        """Local: forget the mapping of `t`'s storage (call before the tensor is freed)."""
+        if self.emulated or self.nranks == 1:
+            return
+        _check(lib().taccl_unregister_buffer(ctypes.c_void_p(t.untyped_storage().data_ptr())))
 
     def run(self, coll, out, inp, stream=None):
-        """One collective call; `coll` in COLLS. Tensors are contiguous CUDA tensors."""
+        """One collective call; `coll` in COLLS. Tensors are contiguous CUDA tensors. With
+        nranks > 1, `out` must lie in a registered storage (register(); NOT_REGISTERED
+        otherwise); a registered `inp` enables pull mode (every rank's, or none)."""
         c = COLLS[coll] if isinstance(coll, str) else coll
         n = self.nranks
         count = inp.numel() // n if c in (ALLTOALL, REDUCESCATTER) else inp.numel()
-        self.register(out)
-        self.register(inp)
         _check(lib().taccl_run(c, ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                count, dtype_code(inp, c), _stream(stream)))
 

@@ -34,6 +34,15 @@ def test_no_compute_calls_needed_for_validation():
     assert ok, msg
 
 
+@pytest.mark.parametrize("f", ["c1_ag_ring_n2_p2.xml", "ar_rsag_n2_p1.xml", "ag_relay_cpy_n2.xml"])
+def test_golden_programs_pass_both_validators(f):
+    text = golden(f)
+    assert oracle.validate(oracle.parse(text)).ok
+    for direct in (True, False):
+        ok, kind, msg = taccl.validate(text, direct)
+        assert ok, (f, direct, kind, msg)
+
+
 MUTS = mutate.load_mutations(golden("mutations.txt"))
 
 

@@ -48,6 +48,8 @@ def _worker(rank, n, port, cases, q):
             x = torch.from_numpy(ins[rank].view(view[dtype])).view(tdt[dtype]).cuda()
             e_out = count if coll in ("allreduce", "reducescatter") else n * count
             out = torch.empty(e_out, dtype=tdt[dtype], device="cuda")
+            comm.register(out)  # collective, explicit (run() never registers)
+            comm.register(x)    # pull mode for receive-reduces fed by a peer's input
             for _ in range(3):  # repeated calls exercise epochs / entry handshakes
                 out.view(torch.uint8).fill_(0xA5)
                 comm.run(coll, out, x)
@@ -67,6 +69,7 @@ def _worker(rank, n, port, cases, q):
             # NCCL's in-place forms (reading G10): AR sendbuf == recvbuf, AG sendbuf = own slot
             if coll in ("allreduce", "allgather"):
                 buf = torch.empty(e_out, dtype=tdt[dtype], device="cuda")
+                comm.register(buf)
                 if coll == "allreduce":
                     buf.copy_(x)
                     comm.run(coll, buf, buf)
@@ -75,7 +78,10 @@ def _worker(rank, n, port, cases, q):
                     comm.run(coll, buf, buf[rank * count:(rank + 1) * count])
                 torch.cuda.synchronize()
                 ok = ok and bool(np.array_equal(buf.cpu().view(vt).numpy().view(want.dtype), want))
+                comm.unregister(buf)
             results.append(ok)
+            comm.unregister(out)
+            comm.unregister(x)
             comm.free(h)
         comm.destroy()
         q.put((rank, results, None))
@@ -133,7 +139,7 @@ def _timeout_worker(rank, n, port, q):
         x = torch.ones(1 << 16, dtype=torch.int32, device="cuda")
         out = torch.empty(n << 16, dtype=torch.int32, device="cuda")
         comm.register(out)
-        comm.register(x)  # registration is collective (comm.run registers inputs too)
+        comm.register(x)  # registration is collective and explicit
         code = None
         if rank == 0:  # rank 1 never joins the call: rank 0's waits must time out, not hang
             comm.run("allgather", out, x)
@@ -170,7 +176,7 @@ def test_watchdog_timeout_surfaces():
     assert res[0][1] == 6
 
 
-# ---------------------------------------------------------------- full sizes, real peers, sampled
+# ---------------------------------------------------------------- full sizes, real peers, every element
 
 FULL_CASES = [  # (coll, dtype, total bytes, input kind); bench.py's workload is the first
     ("allgather", "bfloat16", 1 << 30, "bits"),
@@ -181,13 +187,11 @@ FULL_CASES = [  # (coll, dtype, total bytes, input kind); bench.py's workload is
     ("allreduce", "float32", 1 << 28, "uniform"),
     ("reducescatter", "bfloat16", 1 << 30, "uniform"),
 ]
-FULL_TOL = {"float32": 1e-6, "bfloat16": 1e-2}  # north star: relative to the fp64 sum
 
 
 def _full_worker(rank, n, port, q):
     import torch.distributed as dist
 
-    import oracle
     from paper_2111_04867_b200 import taccl
     from paper_2111_04867_b200.generator import default_schedules
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -203,38 +207,32 @@ def _full_worker(rank, n, port, q):
             count = total // es if coll == "allreduce" else total // es // n
             rows_in = n if coll in ("alltoall", "reducescatter") else 1
             rows_out = n if coll in ("allgather", "alltoall") else 1
-            g = torch.Generator(device="cuda").manual_seed(211104867 + 1000 * 3 + rank)
-            if kind == "uniform":  # U[1,2) (bf16: rounded)
-                x = (torch.rand(rows_in * count, device="cuda", generator=g) + 1.0).to(tdt)
-            elif dtype == "int32":
-                x = torch.randint(-2**31, 2**31 - 1, (rows_in * count,), dtype=torch.int32, device="cuda", generator=g)
-            else:
-                x = torch.randint(-2**15, 2**15, (rows_in * count,), dtype=torch.int16, device="cuda",
-                                  generator=g).view(tdt)
+            def make_input(src):  # rank src's seeded input (regenerated identically on any B200)
+                g = torch.Generator(device="cuda").manual_seed(211104867 + 1000 * 3 + src)
+                if kind == "uniform":  # U[1,2) (bf16: rounded)
+                    return (torch.rand(rows_in * count, device="cuda", generator=g) + 1.0).to(tdt)
+                if dtype == "int32":
+                    return torch.randint(-2**31, 2**31 - 1, (rows_in * count,), dtype=torch.int32, device="cuda", generator=g)
+                return torch.randint(-2**15, 2**15, (rows_in * count,), dtype=torch.int16, device="cuda", generator=g).view(tdt)
+
+            x = make_input(rank)
             out = torch.empty(rows_out * count, dtype=tdt, device="cuda")
             out.view(torch.uint8).fill_(0xA5)
+            comm.register(out)
+            comm.register(x)
             comm.run(coll, out, x)  # the bench's call: registered user buffers, size-selected schedule
             torch.cuda.synchronize()
             comm.check()
-            # the sampled problem (every collective acts element-wise along count): each rank's
-            # input rows at the sampled columns, exchanged over gloo, fed to the oracle
-            idx = torch.from_numpy(np.sort(np.random.default_rng(11).choice(count, 4096, replace=False))).cuda()
-            iv = torch.int16 if dtype == "bfloat16" else torch.int32
-            xv, ov = x.view(iv), out.view(iv)
-            sub = torch.cat([xv[r * count:(r + 1) * count][idx] for r in range(rows_in)]).cpu().numpy()
-            subs = [None] * n
-            dist.all_gather_object(subs, sub)
-            got = torch.cat([ov[qq * count:(qq + 1) * count][idx] for qq in range(rows_out)]).cpu().numpy()
-            if kind == "uniform":  # north star: float AR/RS within FULL_TOL of the fp64 sum
-                fv = np.uint16 if dtype == "bfloat16" else np.float32
-                fs = [s.view(fv) for s in subs]
-                want = oracle.expected_allreduce_f64(fs, dtype) if coll == "allreduce" else \
-                    oracle.expected_reducescatter_f64(fs, dtype)[rank]
-                rel = np.abs(oracle.collectives.to_f64(got.view(fv), dtype) - want) / np.abs(want)
-                ok = bool(rel.max() <= FULL_TOL[dtype])
-            else:
-                want = oracle.expected_outputs(coll, subs, "int32")[rank]
-                ok = bool(np.array_equal(got, want))
+            # EVERY element of this rank's output vs the oracle's definition on all ranks' inputs
+            # (regenerated here from their seeds), column block by column block (tests/fullsize.py)
+            from fullsize import check_blocked
+            ins = [x if src == rank else make_input(src) for src in range(n)]
+            ok, detail = check_blocked(coll, n, count, dtype, kind != "uniform", ins, {rank: out})
+            if not ok:
+                print(f"rank {rank} {coll} {dtype}: {detail}", flush=True)
+            del ins
+            comm.unregister(out)
+            comm.unregister(x)
             results.append(ok)
             for h in hs:
                 comm.free(h)
@@ -248,10 +246,10 @@ def _full_worker(rank, n, port, q):
 
 
 @pytest.mark.parametrize("n", [2, 4])
-def test_full_size_multiprocess_sampled(n):
+def test_full_size_multiprocess(n):
     # BASELINE.json's 1 GiB sizes through the real multi-process path (CUDA IPC peers, the
-    # default size-specialised sets, the launch configuration bench.py times), outputs checked
-    # at sampled elements against the oracle on the sampled slices of every rank's input
+    # default size-specialised sets, the launch configuration bench.py times), every output
+    # element checked against the oracle's definition on all ranks' inputs
     if NGPU < n:
         pytest.skip(f"needs {n} GPUs, have {NGPU}")
     import torch.multiprocessing as mp

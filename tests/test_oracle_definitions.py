@@ -221,3 +221,47 @@ def test_float32_add_is_single_rounding():
     for x, y, g in zip(a, b, got):
         # float64 sum of two float32 is exact here; one rounding to float32 must match
         assert g == np.float32(np.float64(x) + np.float64(y))
+
+
+# ---------------------------------------------------------------- bf16 -> fp64 conversion
+# oracle.collectives.bf16_to_f64 / to_f64 convert BOTH the fp64 reference inputs and the GPU
+# outputs in every bf16 tolerance check, so a wrong shift or half would distort both alike.
+# Pinned to hand-decoded values (bf16 = the top 16 bits of an IEEE binary32: 1 sign, 8
+# exponent, 7 fraction bits) and to torch's own bf16 -> float64 conversion.
+BF16_HAND = [  # bits, value (decoded by hand from sign/exponent/fraction)
+    (0x3F80, 1.0), (0xC000, -2.0), (0x0001, 2.0 ** -133), (0x0080, 2.0 ** -126),
+    (0x7F80, math.inf), (0xFF80, -math.inf), (0x8000, -0.0), (0x0000, 0.0),
+    (0x3FC0, 1.5), (0x4049, 3.140625), (0x7F7F, (2 - 2.0 ** -7) * 2.0 ** 127), (0xBF81, -(1 + 2.0 ** -7)),
+]
+
+
+def test_bf16_to_f64_hand_values():
+    from oracle.collectives import bf16_to_f64, to_f64
+    bits = np.array([b for b, _ in BF16_HAND], np.uint16)
+    want = [v for _, v in BF16_HAND]
+    for f in (bf16_to_f64(bits), to_f64(bits, "bfloat16")):
+        assert f.dtype == np.float64
+        assert f.tolist() == want
+        assert [math.copysign(1, x) for x in f] == [math.copysign(1, x) for x in want]  # -0.0 keeps its sign
+    nan = bf16_to_f64(np.array([0x7FC0, 0xFFC1], np.uint16))
+    assert np.isnan(nan).all()
+
+
+def test_bf16_to_f64_matches_torch_on_every_pattern():
+    torch = pytest.importorskip("torch")
+    from oracle.collectives import bf16_to_f64
+    bits = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)  # all 65536 bf16 patterns
+    ours = bf16_to_f64(bits)
+    theirs = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).to(torch.float64).numpy()
+    both_nan = np.isnan(ours) & np.isnan(theirs)
+    assert np.array_equal(ours[~both_nan], theirs[~both_nan])
+    assert np.array_equal(np.isnan(ours), np.isnan(theirs))
+    assert np.array_equal(np.signbit(ours[~both_nan]), np.signbit(theirs[~both_nan]))
+
+
+def test_to_f64_other_dtypes_are_plain_widening():
+    from oracle.collectives import to_f64
+    f = np.array([1.5, -0.1, 3.4e38, 1e-45], np.float32)
+    assert to_f64(f, "float32").tolist() == [float(x) for x in f]  # exact widening of binary32
+    i = np.array([-2**31, 2**31 - 1, 0], np.int32)
+    assert to_f64(i, "int32").tolist() == [-2.0 ** 31, 2.0 ** 31 - 1, 0.0]

@@ -126,3 +126,57 @@ def test_instance_expansion_invariant_on_golden():
             a = oracle.run(prog, ins, dtype)
             b = oracle.run(exp, ins, dtype)
             assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_instance_subchunk_floor_split_by_hand():
+    # reading G3 / docs/SCHEDULE.md: subchunk j of a chunk of c_e elements is
+    # [floor(j*c_e/m), floor((j+1)*c_e/m)). c_e = 4, m = 3 -> [0,1), [1,2), [2,4): instance 2
+    # carries two elements of every chunk. C1's AG ring (p=2) on count 8 (c_e = 4): an input
+    # element lands in the output exactly where the Allgather definition puts it, and every
+    # one of the 3 instances moves its own subchunk (tagged by instance through a poisoned copy).
+    prog = oracle.parse(golden("c1_ag_ring_n2_p2.xml"))
+    prog.instances = 3
+    exp = oracle.expand_instances(prog)
+    assert exp.subchunks == 3 and exp.chunks_per_rank == 6
+    ins = [np.arange(8, dtype=np.int32) + 100 * r for r in range(2)]
+    outs = oracle.run(exp, ins, "int32")
+    for o in outs:
+        assert o.tolist() == list(range(8)) + list(range(100, 108))
+    # the element ranges the expanded chunks name (chunk q' = subchunk q' % 3 of chunk q' // 3)
+    from oracle import simulate
+    seen = []
+    orig_read = simulate._execute
+
+    def spy(prog_, graph, order, bufs, read, write, reduce):
+        def w(buf, off, cnt, vals):
+            seen.append((off, len(vals)))
+            return write(buf, off, cnt, vals)
+        return orig_read(prog_, graph, order, bufs, read, w, reduce)
+    simulate._execute = spy
+    try:
+        oracle.run(exp, ins, "int32")
+    finally:
+        simulate._execute = orig_read
+    sizes = {off % 3: n for off, n in seen}
+    assert sizes == {0: 1, 1: 1, 2: 2}
+
+
+@pytest.mark.parametrize("coll,algo,n,p,m,count", [
+    ("allgather", "ring", 4, 1, 3, 10), ("allgather", "direct", 3, 2, 4, 2 * 7),
+    ("alltoall", "direct", 4, 1, 3, 5), ("allreduce", "ring", 4, 1, 3, 4 * 5),
+    ("allreduce", "direct", 3, 2, 4, 3 * 2 * 3), ("reducescatter", "ring", 3, 1, 2, 7)])
+def test_instance_expansion_invariant_ragged(coll, algo, n, p, m, count):
+    # expanded (m instances, floor split; c_e not a multiple of m) == unexpanded, bit for bit,
+    # on generated programs; and both equal the collective's definition (int32)
+    from paper_2111_04867_b200.generator import generate
+    from paper_2111_04867_b200.inputs import allreduce_input
+    prog = oracle.parse(generate(coll, algo, n, p, m))
+    ce = oracle.chunk_elems(coll, n, p, count)
+    assert ce % m != 0
+    exp = oracle.expand_instances(prog)
+    assert oracle.validate(exp).ok
+    e_in = n * count if coll in ("alltoall", "reducescatter") else count
+    ins = [allreduce_input(e_in, "int32", "bits", 31, r) for r in range(n)]
+    a, b = oracle.run(prog, ins, "int32"), oracle.run(exp, ins, "int32")
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert all(np.array_equal(x, y) for x, y in zip(a, oracle.expected_outputs(coll, ins, "int32")))
