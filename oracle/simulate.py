@@ -156,9 +156,35 @@ def add(a: np.ndarray, b: np.ndarray, dtype: str) -> np.ndarray:
     raise ValueError(dtype)
 
 
-def run(prog: Program, inputs, dtype: str, graph=None, order=None):
+class _Val:
+    """bf16 partials mode: a range's bits plus its fp32 partials (None unless every chunk of
+    the range holds one) — what a read returns and a send carries."""
+    __slots__ = ("bits", "part")
+
+    def __init__(self, bits, part):
+        self.bits, self.part = bits, part
+
+
+class _Reduced(_Val):
+    """The result of an rrc in bf16 partials mode: bits = RNE(acc), part = acc (fp32)."""
+
+
+def run(prog: Program, inputs, dtype: str, graph=None, order=None, bf16: str = "partials"):
     """Numeric execution. inputs: one 1-D array per rank (dtype storage per DTYPES, bf16 as
-    uint16 bits). Returns the per-rank output arrays."""
+    uint16 bits). Returns the per-rank output arrays.
+
+    bf16 selects the bfloat16 reduction semantics (reading G6, DESIGN.md §2 R6); int32 and
+    float32 are unaffected (a float32 partial is the float32 value itself):
+    * "partials" (the executor's): every chunk an `rrc` writes keeps its fp32 accumulator as a
+      partial next to the RNE-rounded bf16 bits. An operand of a later `rrc` — its local
+      source, or the message of a send — is read as those fp32 partials when every chunk of
+      its range holds one, else as the bf16 bits widened (exactly). `r` and `cpy` write bf16
+      bits and drop the destination's partials (so a value that leaves a reduction chain
+      through a receive or a copy is rounded once, there). The rrc adds in fp32 (RNE).
+      Consequence: a chain of rrcs — on one rank or hop to hop across ranks — sums in fp32
+      in chain order and rounds once per value anyone reads as bf16.
+    * "per_step": every rrc rounds to bf16 (correctly rounded bf16 addition of two bf16 values).
+    """
     graph, order = _prepare(prog, graph, order)
     n, p, m = prog.nranks, prog.chunks_per_rank, prog.subchunks
     np_dt, _ = DTYPES[dtype]
@@ -167,8 +193,13 @@ def run(prog: Program, inputs, dtype: str, graph=None, order=None):
     # chunk q of an instance-expanded program (m > 1) is subchunk q % m of the original chunk
     # q // m: elements [floor(j*c_e/m), floor((j+1)*c_e/m)) of it (reading G3)
     ce = chunk_elems(prog.coll, n, p // m, count)
+    if bf16 not in ("partials", "per_step"):
+        raise ValueError(bf16)
+    partials = dtype == "bfloat16" and bf16 == "partials"
 
     def span(q):
+        if m == 1:
+            return q * ce, (q + 1) * ce
         k, j = divmod(q, m)
         return k * ce + (j * ce) // m, k * ce + ((j + 1) * ce) // m
     bufs = []
@@ -179,24 +210,42 @@ def run(prog: Program, inputs, dtype: str, graph=None, order=None):
         o = np.full(g.o_chunks // m * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
         s = np.full(g.s_chunks // m * ce * x.itemsize, 0xA5, np.uint8).view(np_dt)
         bufs.append({"i": x, "o": o, "s": s})
+    part = {}  # partials mode: id(buffer array) -> {chunk: fp32 partial of that chunk}
 
-    def read(buf, off, cnt, where):
-        if m == 1:
-            return buf[off * ce:(off + cnt) * ce].copy()
+    def read_bits(buf, off, cnt):
         return np.concatenate([buf[slice(*span(q))] for q in range(off, off + cnt)])
 
+    def read(buf, off, cnt, where):
+        bits = read_bits(buf, off, cnt)
+        if not partials:
+            return bits
+        have = part.get(id(buf), {})
+        if all(q in have for q in range(off, off + cnt)):
+            return _Val(bits, np.concatenate([have[q] for q in range(off, off + cnt)]))
+        return _Val(bits, None)
+
     def write(buf, off, cnt, vals):
-        if m == 1:
-            buf[off * ce:(off + cnt) * ce] = vals
-            return
+        bits = vals.bits if partials else vals
         at = 0
         for q in range(off, off + cnt):
             a, b = span(q)
-            buf[a:b] = vals[at:at + b - a]
+            buf[a:b] = bits[at:at + b - a]
+            if partials:
+                have = part.setdefault(id(buf), {})
+                if isinstance(vals, _Reduced):  # an rrc's result: keep its fp32 accumulator
+                    have[q] = vals.part[at:at + b - a].copy()
+                else:  # r / cpy: bf16 bits only
+                    have.pop(q, None)
             at += b - a
 
     def reduce(mine, got, where):
-        return add(mine, got, dtype)
+        if not partials:
+            return add(mine, got, dtype)
+        a = mine.part if mine.part is not None else bf16_to_f32(mine.bits)
+        b = got.part if got.part is not None else bf16_to_f32(got.bits)
+        with np.errstate(over="ignore", invalid="ignore"):
+            acc = (a + b).astype(np.float32)  # one IEEE binary32 add, RNE
+        return _Reduced(bf16_round(acc), acc)
 
     _execute(prog, graph, order, bufs, read, write, reduce)
     return [b["o"] for b in bufs]
