@@ -341,6 +341,71 @@ __device__ void reduce_dispatch(int dtype, char* dst, char* const* fwd, int nfwd
 #undef TACCL_RED
 }
 
+// ---------------------------------------------------------------- bf16 partials (reading R6)
+// A bf16 reduction whose operands may be fp32 partials: the local source (s32), each input
+// (bit s of imask) and each forward destination (bit f of fmask) is either bf16 or fp32. All
+// pointers are the step's base pointers; element e of the range that starts at bf16 byte `off`
+// of the step lives at p + off + 2e (bf16) or p + 2 off + 4e (fp32: every fp32 layout is the
+// bf16 layout with byte offsets doubled). acc = src0 + in_0 + ... in fp32 with RNE (chain
+// order); dst = RNE_bf16(acc), dst32 (the destination's shadow, if given) = acc, fwd[f] =
+// acc or RNE_bf16(acc).
+__device__ __forceinline__ void px_ld8(const char* p, bool f32, int64_t off, int64_t v, float* x) {
+  if (f32) {
+    const int4 a = ld_cg(reinterpret_cast<const int4*>(p + 2 * off) + 2 * v);
+    const int4 b = ld_cg(reinterpret_cast<const int4*>(p + 2 * off) + 2 * v + 1);
+    x[0] = __int_as_float(a.x); x[1] = __int_as_float(a.y); x[2] = __int_as_float(a.z); x[3] = __int_as_float(a.w);
+    x[4] = __int_as_float(b.x); x[5] = __int_as_float(b.y); x[6] = __int_as_float(b.z); x[7] = __int_as_float(b.w);
+  } else {
+    Elt<TACCL_BFLOAT16>::unpack(ld_cg(reinterpret_cast<const int4*>(p + off) + v), x);
+  }
+}
+__device__ __forceinline__ void px_st8_f32(char* p, int64_t off, int64_t v, const float* x) {
+  int4* q = reinterpret_cast<int4*>(p + 2 * off) + 2 * v;
+  st_v4(q, make_int4(__float_as_int(x[0]), __float_as_int(x[1]), __float_as_int(x[2]), __float_as_int(x[3])));
+  st_v4(q + 1, make_int4(__float_as_int(x[4]), __float_as_int(x[5]), __float_as_int(x[6]), __float_as_int(x[7])));
+}
+__device__ __noinline__ void cta_reduce_px(char* dst, char* dst32, char* const* fwd, int nfwd, unsigned fmask,
+                                           const char* src0, bool s32, const char* const* ins, int ns, unsigned imask,
+                                           int64_t off, int64_t nelem) {
+  using E = Elt<TACCL_BFLOAT16>;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // 16-byte vectors need every bf16 address 16-aligned and every fp32 address 32-aligned
+  uintptr_t al = (uintptr_t)(dst + off) | (uintptr_t)(s32 ? src0 + 2 * off : src0 + off) |
+                 (dst32 ? (uintptr_t)(dst32 + 2 * off) : 0);
+  for (int s = 0; s < ns; ++s) al |= (uintptr_t)(((imask >> s) & 1) ? ins[s] + 2 * off : ins[s] + off);
+  for (int f = 0; f < nfwd; ++f) al |= (uintptr_t)(((fmask >> f) & 1) ? fwd[f] + 2 * off : fwd[f] + off);
+  const int64_t nv = (al & 15) ? 0 : nelem / 8;
+  for (int64_t v = tid; v < nv; v += nt) {
+    float acc[8], x[8];
+    px_ld8(src0, s32, off, v, acc);
+    for (int s = 0; s < ns; ++s) {
+      px_ld8(ins[s], (imask >> s) & 1, off, v, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
+    }
+    const int4 o = E::pack(acc);
+    st_v4(reinterpret_cast<int4*>(dst + off) + v, o);
+    if (dst32) px_st8_f32(dst32, off, v, acc);
+    for (int f = 0; f < nfwd; ++f) {
+      if ((fmask >> f) & 1) px_st8_f32(fwd[f], off, v, acc);
+      else st_v4(reinterpret_cast<int4*>(fwd[f] + off) + v, o);
+    }
+  }
+  for (int64_t e = nv * 8 + tid; e < nelem; e += nt) {  // unaligned ranges and the tail
+    auto ld1 = [&](const char* p, bool f32) {
+      return f32 ? __ldcg(reinterpret_cast<const float*>(p + 2 * off) + e) : E::load(p + off + 2 * e);
+    };
+    float acc = ld1(src0, s32);
+    for (int s = 0; s < ns; ++s) acc = __fadd_rn(acc, ld1(ins[s], (imask >> s) & 1));
+    E::store(dst + off + 2 * e, acc);
+    if (dst32) reinterpret_cast<float*>(dst32 + 2 * off)[e] = acc;
+    for (int f = 0; f < nfwd; ++f) {
+      if ((fmask >> f) & 1) reinterpret_cast<float*>(fwd[f] + 2 * off)[e] = acc;
+      else E::store(fwd[f] + off + 2 * e, acc);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- TMA bulk-copy pipeline
 // One elected thread streams a piece through kTmaStages shared-memory stages of kTmaStage
 // bytes: cp.async.bulk global->shared (mbarrier complete_tx) then shared->global
@@ -621,6 +686,90 @@ __device__ __forceinline__ bool ll_move(const char* src, char* dst, const char* 
   return true;
 }
 
+// LL step of a bf16 reduction (or send) whose operands may be fp32 partials (reading R6). The
+// bf16 line geometry is kept: piece lines [l0, l1) of every chunk, line l = bf16 elements
+// [4l, 4l+4) of the chunk, ne = valid elements of the line. An fp32 message carries line l as
+// TWO LL lines (elements 4l, 4l+1 and 4l+2, 4l+3; the second only when ne > 2) at slot bytes
+// q*2*llcb + 32*l (+16): its slot is twice a bf16 message's. src: bf16 payload (chunk q at
+// q*cb) or, s32, its fp32 shadow (chunk q at 2*q*cb); dst32: the destination's shadow.
+// out = src (+) in_0 (+) ... in fp32 (RNE, chain order); a send (no input) moves src.
+// Register budget: the LL kernel sits at the 255-register limit, so the inputs are taken one
+// after another (each slot pointer derived from the step when needed — a fused chain's members
+// and forwards from the fused array, else the step's own slot soff2 / the peer's roff2) instead
+// of keeping every input's lines live; one line per thread per pass.
+__device__ __noinline__ bool ll_px(const KRank& R, const KStep& st, const int* fused, int send_peer, char* my_staged,
+                                   int64_t parity_off, const char* src, bool s32, char* dst, char* dst32, int64_t cb,
+                                   int64_t llcb, int64_t l0, int64_t l1, unsigned flag, u64 timeout_ns) {
+  const bool fz = st.op == K_RRC_FUSED;
+  const int nin = fz ? st.fuse_count : st.op == K_SEND ? 0 : 1;
+  const int nfwd = fz ? st.fwd_count : (st.op == K_SEND || st.op == K_RRCS) ? 1 : 0;
+  const unsigned m = (unsigned)(l1 - l0), total = m * (unsigned)st.cnt, nt = blockDim.x;
+  for (unsigned idx = threadIdx.x; idx < total; idx += nt) {
+    const unsigned q = idx / m;
+    const int64_t ll = l0 + (idx - q * m);
+    const int vb = (int)min((int64_t)8, cb - 8 * ll), ne = vb >> 1;
+    const int64_t pb = (int64_t)q * cb + 8 * ll;
+    const int64_t lb = (int64_t)q * llcb + 16 * ll, lb2 = (int64_t)q * 2 * llcb + 32 * ll;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (s32) {
+      const float* sp = reinterpret_cast<const float*>(src + 2 * pb);
+      for (int e = 0; e < ne; ++e) acc[e] = __ldcg(sp + e);
+    } else {
+      const u64 v = ld_bytes(src + pb, vb);
+      for (int e = 0; e < ne; ++e) acc[e] = ll_elt_f(v, e, TACCL_BFLOAT16);
+    }
+#pragma unroll 1
+    for (int i = 0; i < nin; ++i) {
+      const int* fe = fz ? fused + kFuseStride * (st.fuse_begin + i) : nullptr;
+      const bool f32 = fz ? fe[5] != 0 : (st.pflags & P_IN) != 0;
+      const char* in = my_staged + (int64_t)(fz ? fe[3] : st.soff2) * llcb + (f32 ? lb2 : lb);
+      uint4 w0 = ld_volatile_v4(in);
+      uint4 w1 = (f32 && ne > 2) ? ld_volatile_v4(in + 16) : make_uint4(0, flag, 0, flag);
+      u64 t0 = 0;
+      for (int it = 0; w0.y != flag || w0.w != flag || w1.y != flag || w1.w != flag; ++it) {
+        if (w0.y != flag || w0.w != flag) w0 = ld_volatile_v4(in);
+        if (w1.y != flag || w1.w != flag) w1 = ld_volatile_v4(in + 16);
+        if ((it & 63) == 1) {
+          const u64 now = globaltimer();
+          if (!t0) t0 = now;
+          else if (now - t0 > timeout_ns) return false;
+        }
+      }
+      float x[4];
+      if (f32) {
+        x[0] = __uint_as_float(w0.x); x[1] = __uint_as_float(w0.z);
+        x[2] = __uint_as_float(w1.x); x[3] = __uint_as_float(w1.z);
+      } else {
+        const u64 y = (u64)w0.x | ((u64)w0.z << 32);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = ll_elt_f(y, e, TACCL_BFLOAT16);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
+    }
+    u64 v = 0;
+    for (int e = 0; e < ne; ++e) v |= (u64)Elt<TACCL_BFLOAT16>::rn(acc[e]) << (16 * e);
+    if (dst) st_bytes(dst + pb, v, vb);
+    if (dst32) {
+      float* dp = reinterpret_cast<float*>(dst32 + 2 * pb);
+      for (int e = 0; e < ne; ++e) dp[e] = acc[e];
+    }
+#pragma unroll 1
+    for (int f = 0; f < nfwd; ++f) {
+      const int* fw = fz ? fused + st.fwd_begin + kFwdStride * f : nullptr;
+      const bool f32 = fz ? fw[6] != 0 : (st.pflags & P_OUT) != 0;
+      char* out = R.peer_arena[fz ? fw[0] : send_peer] + parity_off + (int64_t)(fz ? fw[4] : st.roff2) * llcb;
+      if (f32) {
+        st_volatile_v4(out + lb2, make_uint4(__float_as_uint(acc[0]), flag, __float_as_uint(acc[1]), flag));
+        if (ne > 2) st_volatile_v4(out + lb2 + 16, make_uint4(__float_as_uint(acc[2]), flag, __float_as_uint(acc[3]), flag));
+      } else {
+        st_volatile_v4(out + lb, ll_line(v, flag));
+      }
+    }
+  }
+  return true;
+}
+
 // local copy for the LL kernel (small, one code path): 16-byte vectors when aligned
 __device__ __forceinline__ void ll_copy(char* dst, const char* src, int64_t n) {
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -651,6 +800,10 @@ __device__ __forceinline__ char* local_base(const Ctx& c, int buf) {
     case KB_S: return c.r->arena + c.a->scratch_off;
     default: return c.r->arena + c.a->staging_off;
   }
+}
+// bf16 partials: the fp32 shadow of o / s (one float per element; bf16 offsets doubled)
+__device__ __forceinline__ char* shadow_base(const Ctx& c, int buf) {
+  return c.r->arena + c.a->shadow_off + (buf == KB_S ? c.a->shadow_s : 0);
 }
 __device__ __forceinline__ char* remote_base(const Ctx& c, int peer, int buf) {
   switch (buf) {
@@ -715,6 +868,46 @@ __device__ __forceinline__ int wait_ready(const u64* p, u64 epoch, int pull, u64
 // input and the plan marked its matched receive-reduce as reading it in place (st.poff >= 0)
 __device__ __forceinline__ bool pulled(const KArgs& A, const KStep& st) {
   return A.pull && st.op == K_SEND && st.poff >= 0;
+}
+
+// Direct kernel, bf16 partials (reading R6): one step whose operands may be fp32 — a send of
+// a source's fp32 shadow into the receiver's (2x) staging slot (P_OUT), or a receive-reduce
+// (K_RRC, K_RRCS, a fused chain member's portion) through cta_reduce_px (out of line). Inlined
+// itself: as a call it forced the kernel's live registers around it into local memory.
+__device__ __forceinline__ void px_step(const Ctx& c, const KStep& st, const int* fused, int send_peer, int64_t stripe,
+                                     int nsplit, int64_t cbytes, char* const* s_fwd, const char* const* s_stage) {
+  const KArgs& A = *c.a;
+  const int j = c.j;
+  if (st.op == K_SEND) {
+    const char* src = shadow_base(c, st.srcbuf) + 2 * (int64_t)st.srcoff * cbytes;
+    char* dst = remote_base(c, send_peer, st.rbuf) + (int64_t)st.roff * cbytes;
+    for_piece(stripe, j, nsplit, st.cnt, cbytes,
+              [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + 2 * off, src + 2 * off, 2 * len); });
+    return;
+  }
+  const bool s32 = (st.pflags & P_SRC) != 0;
+  const char* src = s32 ? shadow_base(c, st.srcbuf) + 2 * (int64_t)st.srcoff * cbytes
+                        : local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
+  char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+  char* d32 = (st.pflags & P_KEEP) ? shadow_base(c, st.dstbuf) + 2 * (int64_t)st.dstoff * cbytes : nullptr;
+  if (st.op != K_RRC_FUSED) {
+    const unsigned im = (st.pflags & P_IN) ? 1u : 0u, fm = (st.pflags & P_OUT) ? 1u : 0u;
+    const int nfwd = st.op == K_RRCS ? 1 : 0;
+    for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+      cta_reduce_px(dst, d32, s_fwd, nfwd, fm, src, s32, s_stage, 1, im, off, len / 2);
+    });
+    return;
+  }
+  unsigned im = 0, fm = 0;  // fp32 member messages / fp32 forwards
+  for (int f = 0; f < st.fuse_count; ++f) im |= (fused[kFuseStride * (st.fuse_begin + f) + 5] ? 1u : 0u) << f;
+  for (int f = 0; f < st.fwd_count; ++f) fm |= (fused[st.fwd_begin + kFwdStride * f + 6] ? 1u : 0u) << f;
+  const int64_t unit = (cbytes % 16 == 0) ? 16 : 2;  // this member's portion: 16-byte aligned cuts
+  for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+    const int64_t nu = len / unit;
+    const int64_t a = off + nu * st.part / st.nparts * unit;
+    const int64_t b = (st.part + 1 == st.nparts) ? off + len : off + nu * (st.part + 1) / st.nparts * unit;
+    if (b > a) cta_reduce_px(dst, d32, s_fwd, st.fwd_count, fm, src, s32, s_stage, st.fuse_count, im, a, (b - a) / 2);
+  });
 }
 
 // LL = staged (small-message) mode, a compile-time specialisation so each variant carries
@@ -859,7 +1052,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
 #pragma unroll
           for (int f = 0; f < kMaxRanks; ++f)
             if (f < st.fwd_count) {
-              const int* fw = fused + st.fwd_begin + 6 * f;
+              const int* fw = fused + st.fwd_begin + kFwdStride * f;
               fws[f] = R.peer_arena[fw[0]] + parity_off + (int64_t)fw[4] * ll_cb;
             }
           nin = st.fuse_count;
@@ -884,6 +1077,17 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         char* dst = (st.op == K_SEND) ? nullptr : local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
         const bool red = st.op == K_RRC || st.op == K_RRCS || fz;
         if (PROBE(22) && st.op == K_SEND) src = nullptr;  // timing probe only: no source load
+        if (A.dtype == TACCL_BFLOAT16 && st.pflags) {  // bf16 partials (reading R6)
+          const bool s32 = (st.pflags & P_SRC) != 0;
+          const char* xs = s32 ? shadow_base(c, st.srcbuf) + 2 * (int64_t)st.srcoff * cbytes : src;
+          char* d32 = (st.pflags & P_KEEP) ? shadow_base(c, st.dstbuf) + 2 * (int64_t)st.dstoff * cbytes : nullptr;
+          const bool ok = ll_px(R, st, fused, tb.send, my_staged, parity_off, xs, s32, dst, d32, cbytes, ll_cb, l0, l1,
+                                ll_flag, A.timeout_ns);
+          if (__syncthreads_or(!ok)) {
+            if (tid == 0) record_error(c, st.op, k);
+            return;
+          }
+        } else {
 #ifdef TACCL_TRACE_FINE
         // fine build: [2+4k] loads issued, [3+4k] waits done, [4+4k] stores issued (thread 0)
         const bool ok = ll_lines<kMaxRanks>(A.dtype, red, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt, l0, l1,
@@ -900,6 +1104,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         if (__syncthreads_or(!ok)) {
           if (tid == 0) record_error(c, st.op, k);
           return;
+        }
         }
       } else {
       if (tid == 0) {
@@ -937,7 +1142,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
                         : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
         if (ok && st.op == K_RRC_FUSED) {  // fused sends of the chain's result (fuse_chain_sends)
           for (int f = 0; f < st.fwd_count && ok; ++f) {
-            const int* fw = fused + st.fwd_begin + 6 * f;  // peer, chan, rbuf, roff, roff2, seq
+            const int* fw = fused + st.fwd_begin + kFwdStride * f;  // peer, chan, rbuf, roff, roff2, seq, P_OUT
             // entry handshake of that send's connection: its receiver is in this call
             if (!LL) {
               const int w = wait_ready(my_ready + flag_slot(fw[0], fw[1], j), c.epoch, A.pull, A.timeout_ns);
@@ -972,6 +1177,10 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         case K_SEND:
         case K_CPY: {
           if (pulled(A, st)) break;  // the receiver loads it in place (pull mode)
+          if (st.op == K_SEND && st.pflags && A.dtype == TACCL_BFLOAT16) {
+            px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
+            break;
+          }
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = st.op == K_CPY ? local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes
                                      : remote_base(c, tb.send, st.rbuf) + (int64_t)st.roff * cbytes;
@@ -995,6 +1204,10 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           const int nfwd = st.op == K_RRCS ? 1 : 0;
+          if (st.pflags && A.dtype == TACCL_BFLOAT16) {  // bf16 partials (reading R6)
+            px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
+            break;
+          }
           for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             reduce_dispatch(A.dtype, dst + off, s_fwd, nfwd, src + off, s_stage, 1, off, len / elt);
           });
@@ -1003,6 +1216,10 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         case K_RRC_FUSED: {  // this member's portion of each range (16-byte aligned cuts)
           const char* src = local_base(c, st.srcbuf) + (int64_t)st.srcoff * cbytes;
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
+          if (st.pflags && A.dtype == TACCL_BFLOAT16) {  // bf16 partials (reading R6)
+            px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
+            break;
+          }
           const int64_t unit = (cbytes % 16 == 0) ? 16 : elt;
           for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             const int64_t nu = len / unit;

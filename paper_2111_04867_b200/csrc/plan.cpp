@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <map>
+#include <set>
 #include <tuple>
 
 #include "taccl_internal.h"
@@ -124,11 +125,15 @@ void fuse_chains(const Gpu& g, const HB& hb, const std::map<std::pair<int, int>,
     const int fb = (int32_t)rp.fused.size() / kFuseStride;
     for (int i = 0; i < K; ++i) {
       const KStep& x = rp.steps[flat.at(chain[i])];
-      for (int v : {chain[i].first, x.seq, x.soff, x.soff2, x.poff}) rp.fused.push_back(v);
+      for (int v : {chain[i].first, x.seq, x.soff, x.soff2, x.poff, x.pflags & P_IN}) rp.fused.push_back(v);
     }
+    // bf16 partials: the chain reads X_1's source (P_SRC of X_1) and its result is kept when X_K
+    // is (the members' intermediate values exist only inside the fused sum)
+    const int chain_pf = (rp.steps[flat.at(head)].pflags & P_SRC) | (rp.steps[flat.at(last)].pflags & P_KEEP);
     for (int i = 0; i < K; ++i) {
       const int fi = flat.at(chain[i]);
       KStep& x = rp.steps[fi];
+      x.pflags = chain_pf;
       x.op = K_RRC_FUSED;
       x.srcbuf = kbuf(first.srcbuf);
       x.srcoff = first.srcoff;
@@ -203,7 +208,7 @@ void fuse_chain_sends(const Program& P, RankPlan& rp, const std::vector<std::vec
     for (int si : sends) {
       KStep& s = rp.steps[si];
       const KTB& kt = rp.tbs[pos(si).first];
-      for (int v : {kt.send, kt.chan, (int)s.rbuf, s.roff, s.roff2, s.seq}) rp.fused.push_back(v);
+      for (int v : {kt.send, kt.chan, (int)s.rbuf, s.roff, s.roff2, s.seq, s.pflags & P_OUT}) rp.fused.push_back(v);
       s.op = K_PUB;
     }
     for (int fi : mem) {
@@ -213,36 +218,123 @@ void fuse_chain_sends(const Program& P, RankPlan& rp, const std::vector<std::vec
   }
 }
 
+// bf16 partials (reading R6; the oracle's run(bf16="partials") states the same rule
+// dynamically). Static form: the state of chunk c of o/s when step X reads it is decided by
+// its last writer before X in happens-before order (unique: the race check orders every two
+// writes of a chunk and every write with every read). X reads a range as fp32 partials iff
+// every chunk's last writer is an rrc. Flags: an rrc whose source range qualifies gets P_SRC;
+// a send whose matched receive is an rrc and whose source range qualifies gets P_OUT and that
+// receive P_IN; every rrc that is the last writer of a chunk some flagged read covers gets
+// P_KEEP (its result must be kept in the shadow). `matched` maps a send to its receive.
+using SKey = std::tuple<int, int, int>;  // (rank, tb, step)
+std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map<SKey, SKey>& matched,
+                                  std::map<SKey, std::set<SKey>>* readers) {
+  std::map<std::tuple<int, int, int>, int> fl;
+  for (const Gpu& g : P.gpus) {
+    const int r = g.id;
+    struct W { int t, k; StepType type; BufId buf; int off, cnt; };
+    std::vector<W> writers;
+    for (const TB& tb : g.tbs)
+      for (const Step& st : tb.steps)
+        if ((st.type == ST_R || st.type == ST_RRC || st.type == ST_CPY) && (st.dstbuf == B_O || st.dstbuf == B_S))
+          writers.push_back({tb.id, st.s, st.type, st.dstbuf, st.dstoff, st.cnt});
+    // the rrcs that are last writers of the range (empty if some chunk's last writer is not one)
+    auto partial_range = [&](int t, int k, BufId buf, int off, int cnt, std::vector<int>* lw) {
+      lw->clear();
+      if (buf != B_O && buf != B_S) return false;
+      for (int c = off; c < off + cnt; ++c) {
+        int best = -1;
+        for (int w = 0; w < (int)writers.size(); ++w) {
+          const W& x = writers[w];
+          if (x.buf != buf || c < x.off || c >= x.off + x.cnt || !hb.before(r, x.t, x.k, r, t, k)) continue;
+          if (best < 0 || hb.before(r, writers[best].t, writers[best].k, r, x.t, x.k)) best = w;
+        }
+        if (best < 0 || writers[best].type != ST_RRC) return false;
+        lw->push_back(best);
+      }
+      return true;
+    };
+    std::vector<std::pair<int, SKey>> keep;  // (writer, reader)
+    std::vector<int> lw;
+    for (const TB& tb : g.tbs)
+      for (const Step& st : tb.steps) {
+        if (st.type == ST_RRC && partial_range(tb.id, st.s, st.srcbuf, st.srcoff, st.cnt, &lw)) {
+          fl[{r, tb.id, st.s}] |= P_SRC;
+          for (int w : lw) keep.push_back({w, SKey{r, tb.id, st.s}});
+        }
+        if (st.type == ST_S) {
+          const auto m = matched.at({r, tb.id, st.s});
+          const Step& rs = P.gpus[std::get<0>(m)].tbs[std::get<1>(m)].steps[std::get<2>(m)];
+          if (rs.type == ST_RRC && partial_range(tb.id, st.s, st.srcbuf, st.srcoff, st.cnt, &lw)) {
+            fl[{r, tb.id, st.s}] |= P_OUT;
+            fl[m] |= P_IN;
+            for (int w : lw) keep.push_back({w, SKey{r, tb.id, st.s}});
+          }
+        }
+      }
+    for (auto [w, rd] : keep) {
+      fl[{r, writers[w].t, writers[w].k}] |= P_KEEP;
+      (*readers)[{r, writers[w].t, writers[w].k}].insert(rd);
+    }
+  }
+  return fl;
+}
+
 std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends, int pull_kinds) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
-  // per-step seq numbers and staging offsets
+  // per-step seq numbers (message index on the tb's connection)
   std::map<std::tuple<int, int, int>, int> seq, soff, soff2;
-  std::vector<int> stage_total(n, 0), stage2_total(n, 0);
-  for (const Gpu& g : P.gpus) {
+  for (const Gpu& g : P.gpus)
     for (const TB& tb : g.tbs) {
       int ns = 0, nr = 0;
       for (const Step& st : tb.steps) {
         if (st.type == ST_S) seq[{g.id, tb.id, st.s}] = ns++;
         if (st.type == ST_R || st.type == ST_RRC) seq[{g.id, tb.id, st.s}] = nr++;
-        if (st.type == ST_RRC) {
-          soff[{g.id, tb.id, st.s}] = stage_total[g.id];
-          stage_total[g.id] += st.cnt;
-        }
-        if (st.type == ST_R || st.type == ST_RRC) {  // staged mode: every receive has a slot
-          soff2[{g.id, tb.id, st.s}] = stage2_total[g.id];
-          stage2_total[g.id] += st.cnt;
-        }
       }
     }
-  }
   // receiving tb of each connection: (receiver, sender, chan) -> tb id
   std::map<std::tuple<int, int, int>, int> recv_tb;
   for (const Gpu& g : P.gpus)
     for (const TB& tb : g.tbs)
       if (tb.recv >= 0) recv_tb[{g.id, tb.recv, tb.chan}] = tb.id;
-
+  // each send's matched receive (reading G1: the k-th send of a connection <-> its k-th receive)
+  std::map<std::tuple<int, int, int>, std::tuple<int, int, int>> matched;
+  for (const Gpu& g : P.gpus)
+    for (const TB& tb : g.tbs)
+      for (const Step& st : tb.steps) {
+        if (st.type != ST_S) continue;
+        const int pt = recv_tb.at({tb.send, g.id, tb.chan});
+        for (const Step& ps : P.gpus[tb.send].tbs[pt].steps)
+          if ((ps.type == ST_R || ps.type == ST_RRC) && seq[{tb.send, pt, ps.s}] == seq[{g.id, tb.id, st.s}]) {
+            matched[{g.id, tb.id, st.s}] = {tb.send, pt, ps.s};
+            break;
+          }
+      }
   HB hb(P);
+  std::map<SKey, std::set<SKey>> keep_readers;  // rrc -> the steps that read its kept partials
+  const std::map<SKey, int> pfl = partial_flags(P, hb, matched, &keep_readers);
+  auto pflag = [&](int r, int t, int k) {
+    auto it = pfl.find({r, t, k});
+    return it == pfl.end() ? 0 : it->second;
+  };
+  // staging offsets: each rrc owns cnt chunks of its rank's staging area (2 cnt when its
+  // message is fp32 partials), in program order (tb, step); staged mode: every receive a slot
+  std::vector<int> stage_total(n, 0), stage2_total(n, 0);
+  for (const Gpu& g : P.gpus)
+    for (const TB& tb : g.tbs)
+      for (const Step& st : tb.steps) {
+        const int w = (pflag(g.id, tb.id, st.s) & P_IN) ? 2 : 1;
+        if (st.type == ST_RRC) {
+          soff[{g.id, tb.id, st.s}] = stage_total[g.id];
+          stage_total[g.id] += w * st.cnt;
+        }
+        if (st.type == ST_R || st.type == ST_RRC) {
+          soff2[{g.id, tb.id, st.s}] = stage2_total[g.id];
+          stage2_total[g.id] += w * st.cnt;
+        }
+      }
+
   for (const Gpu& g : P.gpus) {
     RankPlan& rp = plans[g.id];
     rp.stage_chunks = stage_total[g.id];
@@ -256,6 +348,8 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
       for (const Step& st : tb.steps) {
         KStep ks{};
         ks.poff = -1;
+        ks.pflags = pflag(g.id, tb.id, st.s);
+        if (ks.pflags) rp.partials = true;
         ks.srcbuf = st.srcbuf == B_NONE ? 0 : kbuf(st.srcbuf);
         ks.dstbuf = st.dstbuf == B_NONE ? 0 : kbuf(st.dstbuf);
         ks.srcoff = st.srcoff;
@@ -380,12 +474,57 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
           if (rcs || (a.op == K_RRC && b.op == K_SEND && b.srcbuf == a.dstbuf && b.srcoff == a.dstoff &&
                       b.cnt == a.cnt && b.dep_count == 0 && b.post_count == 0)) {
             a.op = rcs ? K_RCS : K_RRCS;
+            a.pflags = (a.pflags & ~P_OUT) | (b.pflags & P_OUT);  // the forward's message type
             a.rbuf = b.rbuf;
             a.roff = b.roff;
             a.fwd_seq = b.seq;
             a.roff2 = b.roff2;
             b.op = K_SENT;
           }
+        }
+      }
+    }
+    // fused chains whose member messages or forwards are fp32 carry P_MIX, so the kernel
+    // takes the partials path on one flag test
+    for (KStep& x : rp.steps)
+      if (x.op == K_RRC_FUSED) {
+        for (int f = 0; f < x.fuse_count; ++f)
+          if (rp.fused[kFuseStride * (x.fuse_begin + f) + 5]) x.pflags |= P_MIX;
+        for (int f = 0; f < x.fwd_count; ++f)
+          if (rp.fused[x.fwd_begin + kFwdStride * f + 6]) x.pflags |= P_MIX;
+        if (x.pflags) rp.partials = true;
+      }
+    // bf16 partials: a result whose kept partials are read only by sends that the producing
+    // step now performs itself (K_RRCS's K_SENT, a chain's K_PUB) forwards its fp32
+    // accumulator directly — the shadow write would be dead traffic
+    {
+      auto key_of = [&](int fi) {
+        for (int t = 0; t < (int)rp.tbs.size(); ++t)
+          if (fi >= rp.tbs[t].step_begin && fi < rp.tbs[t].step_begin + rp.tbs[t].nsteps)
+            return SKey{g.id, t, fi - rp.tbs[t].step_begin};
+        return SKey{-1, -1, -1};
+      };
+      auto fwd_only = [&](const SKey& w) {
+        auto it = keep_readers.find(w);
+        if (it == keep_readers.end()) return true;
+        for (const SKey& rd : it->second) {
+          if (std::get<0>(rd) != g.id) return false;
+          const int op = rp.steps[flat.at({std::get<1>(rd), std::get<2>(rd)})].op;
+          if (op != K_SENT && op != K_PUB) return false;
+        }
+        return true;
+      };
+      for (size_t i = 0; i < rp.steps.size(); ++i) {
+        KStep& x = rp.steps[i];
+        if (!(x.pflags & P_KEEP)) continue;
+        if (x.op == K_RRCS && fwd_only(key_of((int)i))) x.pflags &= ~P_KEEP;
+        if (x.op == K_RRC_FUSED) {
+          int lastm = -1;
+          for (size_t q = 0; q < rp.steps.size(); ++q)
+            if (rp.steps[q].op == K_RRC_FUSED && rp.steps[q].fuse_begin == x.fuse_begin &&
+                rp.steps[q].part + 1 == rp.steps[q].nparts)
+              lastm = (int)q;
+          if (lastm >= 0 && fwd_only(key_of(lastm))) x.pflags &= ~P_KEEP;
         }
       }
     }

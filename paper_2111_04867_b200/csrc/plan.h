@@ -10,11 +10,12 @@ struct RankPlan {
   std::vector<KTB> tbs;
   std::vector<KStep> steps;
   std::vector<int32_t> deps;   // pairs (tb, step)
-  std::vector<int32_t> fused;  // chain entries (tb, seq, soff, soff2, poff), then forward entries
+  std::vector<int32_t> fused;  // chain entries (kFuseStride ints), then forward entries (kFwdStride)
   int stage_chunks = 0;        // rrc staging this rank needs (chunk units)
   int stage2_chunks = 0;       // staged mode: every receive's slot (chunk units)
   int scratch_chunks = 0;      // EF scratch buffer (chunk units)
   int fused_chains = 0;
+  bool partials = false;       // some step carries bf16 partial flags (needs the shadow region)
 };
 
 // `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables);

@@ -67,6 +67,8 @@ struct Algo {
   std::vector<int> wsum;        // per rank
   int fused_chains = 0;
   bool has_pull = false;  // some send of the direct plan is read in place (pull mode applies)
+  bool partials = false;  // bf16 partial flags on some step (bf16 calls need the shadow region)
+  int max_o_chunks = 0, max_s_chunks = 0;
 };
 
 struct Reg {
@@ -191,7 +193,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S) {
 struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, stripe = 0;
   int split = 1, grid = 0, budget = 0, dep_ctas = 1, staged = 0, indep_cap = 1;
-  int64_t scratch_off = 0, staging_off = 0, need = 0;
+  int64_t scratch_off = 0, staging_off = 0, need = 0, shadow_off = 0, shadow_s = 0;
   std::vector<std::vector<int>> ct;  // [rank][tb] CTAs of the threadblock (0 for non-local ranks)
 };
 
@@ -299,6 +301,13 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   G->scratch_off = kOffScratch + 2 * sb + base_off;
   G->staging_off = G->scratch_off + (((int64_t)a->max_scratch_chunks * G->chunk_bytes + 255) & ~(int64_t)255);
   G->need = G->staging_off + (int64_t)a->max_stage_chunks * G->chunk_bytes;
+  // bf16 partials: the fp32 shadow of o and s (reading R6), after the staging
+  G->shadow_off = G->shadow_s = 0;
+  if (a->partials && elt == 2) {
+    G->shadow_off = (G->need + 255) & ~(int64_t)255;
+    G->shadow_s = 2 * (int64_t)a->max_o_chunks * G->chunk_bytes;
+    G->need = G->shadow_off + G->shadow_s + 2 * (int64_t)a->max_s_chunks * G->chunk_bytes;
+  }
   if ((size_t)G->need > g.arena_bytes)
     return fail(TACCL_ERR_INVALID_ARG, "arena too small: need " + std::to_string(G->need) + " bytes, have " +
                                            std::to_string(g.arena_bytes) + " (raise scratch_bytes / TACCL_SCRATCH_BYTES)");
@@ -342,6 +351,8 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.variant = (int)env_size("TACCL_COPY_VARIANT", 0);
   A.scratch_off = G.scratch_off;
   A.staging_off = G.staging_off;
+  A.shadow_off = G.shadow_off;
+  A.shadow_s = G.shadow_s;
   A.timeout_ns = g.timeout_ns;
   A.trace = g.trace;
   A.trace_ctas = g.trace_ctas;
@@ -568,7 +579,8 @@ taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, c
              " cnt=" + std::to_string(x.cnt) + " seq=" + std::to_string(x.seq) + " poff=" + std::to_string(x.poff) +
              " deps=" + pairs(x.dep_begin, x.dep_count) + " post=" + pairs(x.post_begin, x.post_count) +
              " part=" + std::to_string(x.part) + "/" + std::to_string(x.nparts) +
-             " fuse=" + std::to_string(x.op == K_RRC_FUSED ? x.fuse_count : 0) + " fwd=" + std::to_string(x.fwd_count) + "\n";
+             " fuse=" + std::to_string(x.op == K_RRC_FUSED ? x.fuse_count : 0) + " fwd=" + std::to_string(x.fwd_count) +
+             " pf=" + std::to_string(x.pflags) + "\n";
       }
     }
   } catch (const SchedError& e) {
@@ -735,6 +747,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
   if (!text) return fail(TACCL_ERR_INVALID_ARG, "null text");
   std::unique_ptr<Algo> a(new Algo);
   std::vector<RankPlan> plans, plans_ll;
+  std::vector<int> P_o_chunks;
   try {
     Program P = parse_ef(text, len);
     check_program(P, true);
@@ -760,6 +773,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->instances = P.instances;
     a->min_bytes = P.min_bytes;
     a->max_bytes = P.max_bytes;
+    for (const Gpu& gp : P.gpus) P_o_chunks.push_back(gp.o_chunks);
   } catch (const SchedError& e) {
     return fail(TACCL_ERR_INVALID_SCHEDULE, e.kind + ": " + e.msg);
   }
@@ -780,6 +794,9 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->max_scratch_chunks = std::max(a->max_scratch_chunks, plans[r].scratch_chunks);
     a->max_stage_chunks = std::max(a->max_stage_chunks, plans[r].stage_chunks);
     a->max_stage2_chunks = std::max(a->max_stage2_chunks, plans[r].stage2_chunks);
+    a->partials = a->partials || plans[r].partials || plans_ll[r].partials;
+    a->max_o_chunks = std::max(a->max_o_chunks, P_o_chunks[r]);
+    a->max_s_chunks = std::max(a->max_s_chunks, plans[r].scratch_chunks);
     a->fused_chains += plans[r].fused_chains;
     for (const KStep& k : plans[r].steps) a->has_pull = a->has_pull || (k.op == K_SEND && k.poff >= 0);
     if (a->nranks == 1 && plans[r].steps.size() == 1) {

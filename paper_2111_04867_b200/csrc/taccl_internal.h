@@ -109,9 +109,20 @@ struct KStep {
   int32_t poff;           // receive-reduces whose matched send reads the sender's input: that
                           // send's input offset (chunk units), else -1 (pull mode reads it in
                           // place); K_SEND: >= 0 iff its matched receive reads it in place
+  int32_t pflags;         // bf16 partials (reading R6), bits P_*; bf16 calls only
 };
-// K_RRC_FUSED member entries in the fused array: tb, seq, soff, soff2, poff
-constexpr int kFuseStride = 5;
+// bf16 partials: an rrc's result keeps its fp32 accumulator in the rank's shadow region (one
+// fp32 per element of o and s) when a later reduction reads it; such reads and the sends that
+// feed an rrc move fp32 (2x the bf16 bytes; staging slots of fp32 messages are 2x as large)
+constexpr int P_SRC = 1;   // receive-reduce: its local source is read as fp32 from the shadow
+constexpr int P_IN = 2;    // receive-reduce: the matched send's message is fp32
+constexpr int P_KEEP = 4;  // receive-reduce: also write the fp32 result to the destination's shadow
+constexpr int P_OUT = 8;   // send (or the forward of K_RRCS): transmit fp32 (from the shadow / acc)
+constexpr int P_MIX = 16;  // K_RRC_FUSED: some member message or forward is fp32 (fused array bits)
+// K_RRC_FUSED member entries in the fused array: tb, seq, soff, soff2, poff, P_IN of its message
+constexpr int kFuseStride = 6;
+// forward entries (fuse_chain_sends): peer, chan, rbuf, roff, roff2, seq, P_OUT
+constexpr int kFwdStride = 7;
 
 struct KTB {
   int32_t send, recv, chan;
@@ -196,6 +207,8 @@ struct KArgs {
   int64_t stripe;          // bytes per stripe of a chunk (pieces own every split-th stripe)
   int64_t scratch_off;     // byte offset of the EF scratch buffer inside every arena
   int64_t staging_off;     // byte offset of the rrc staging area inside every arena
+  int64_t shadow_off;      // bf16 partials: byte offset of the fp32 shadow of o inside every arena
+  int64_t shadow_s;        // ... and of the shadow of s, relative to shadow_off
   uint64_t timeout_ns;
   unsigned long long* trace;  // optional %globaltimer stamps, kTraceSlots per CTA (taccl_trace)
   int32_t trace_ctas;         // CTAs that fit in the trace buffer

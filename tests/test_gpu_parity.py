@@ -242,11 +242,18 @@ def test_allreduce_chain_sends_fusion(n, p, m, dtype, mode):
         os.environ.pop("TACCL_CHAIN_SENDS", None)
 
 
+BF16_TOL_SCHEDS = [  # every generator family's bf16 Allreduce, including multi-hop reduction chains
+    ("allreduce", "ring", 8, 1, {}), ("allreduce", "direct", 8, 1, {}), ("allreduce", "oneshot", 8, 1, {}),
+    ("allreduce", "greedy", 8, 1, {"policy": "uc-min"}), ("allreduce", "greedy", 8, 2, {"policy": "uc-max"}),
+    ("allreduce", "milp", 8, 1, {}), ("allreduce", "ring", 4, 1, {}), ("allreduce", "direct", 4, 1, {}),
+    ("reducescatter", "ring", 8, 1, {}), ("reducescatter", "greedy", 8, 2, {}),
+    ("reducescatter", "milp", 8, 1, {"topology": "2x4", "size": 1 << 16})]
+
+
 @pytest.mark.parametrize("algo,n,dtype,tol", [
     ("ring", 8, "float32", 1e-6), ("direct", 8, "float32", 1e-6), ("direct", 4, "float32", 1e-6),
-    ("ring", 4, "bfloat16", 1e-2), ("direct", 8, "bfloat16", 1e-2), ("direct", 4, "bfloat16", 1e-2),
-    ("oneshot", 8, "float32", 1e-6), ("oneshot", 8, "bfloat16", 1e-2)])
-def test_allreduce_tolerance_uniform(algo, n, dtype, tol):
+    ("oneshot", 8, "float32", 1e-6)])
+def test_allreduce_tolerance_uniform_fp32(algo, n, dtype, tol):
     count = n * 40000
     text = generate("allreduce", algo, n, 1, 1)
     ins = [allreduce_input(count, dtype, "uniform", 6, r) for r in range(n)]
@@ -257,15 +264,53 @@ def test_allreduce_tolerance_uniform(algo, n, dtype, tol):
         assert rel.max() <= tol, rel.max()
 
 
-def test_bf16_ring_n8_matches_schedule_rounding():
-    # A bf16 ring rounds every hop's partial sum to bf16 (like NCCL's ring): at n=8 that alone
-    # reaches ~1.2e-2 relative error on U[1,2). The executor
-    # reproduces the schedule's rounding sequence exactly: bit-exact against the oracle.
-    n, count = 8, 8 * 40000
-    text = generate("allreduce", "ring", n, 1, 1)
-    ins = [allreduce_input(count, "bfloat16", "uniform", 6, r) for r in range(n)]
-    got = run_gpu(text, "allreduce", n, "bfloat16", ins)
-    assert_bits_equal(got, oracle.run(oracle.parse(text), ins, "bfloat16"))
+@pytest.mark.parametrize("coll,algo,n,p,kw", BF16_TOL_SCHEDS)
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_bf16_tolerance_uniform(coll, algo, n, p, kw, mode):
+    # north star: bf16 Allreduce within 1e-2 relative of the fp64 sum, for EVERY schedule the
+    # generator makes (ring / greedy / MILP chains hop rank to rank: fp32 partials, reading R6)
+    text = generate(coll, algo, n, p, 1, **kw)
+    count = n * p * 40000 if coll == "allreduce" else p * 40000
+    e_in = n * count if coll == "reducescatter" else count
+    ins = [allreduce_input(e_in, "bfloat16", "uniform", 6, r) for r in range(n)]
+    got = run_gpu(text, coll, n, "bfloat16", ins, mode=mode)
+    ref = oracle.expected_allreduce_f64(ins, "bfloat16")
+    for r, g in enumerate(got):
+        want = ref if coll == "allreduce" else ref[r * count:(r + 1) * count]
+        rel = np.abs(oracle.collectives.to_f64(g, "bfloat16") - want) / np.abs(want)
+        assert rel.max() <= 1e-2, (r, rel.max())
+
+
+BF16_EXACT_SCHEDS = BF16_TOL_SCHEDS + [("allreduce", "ring", 4, 2, {"m": 2}), ("allreduce", "milp", 4, 2, {}),
+                                       ("reducescatter", "direct", 8, 1, {}), ("reducescatter", "ring", 4, 2, {"m": 2})]
+
+
+@pytest.mark.parametrize("coll,algo,n,p,kw", BF16_EXACT_SCHEDS)
+@pytest.mark.parametrize("kind", ["uniform", "normal"])
+@pytest.mark.parametrize("mode", ["direct", "staged", "push"])
+def test_bf16_partials_bit_exact(coll, algo, n, p, kw, kind, mode):
+    # the executor's bf16 reductions are deterministic: fp32 partials along every reduction
+    # chain, one RNE where a value leaves it (reading R6). Bit-exact against the oracle's
+    # partials mode on non-integer inputs (U[1,2) and N(0,1)), in the zero-copy kernel (pull
+    # and push) and the LL kernel
+    kw = dict(kw)
+    m = kw.pop("m", 1)
+    text = generate(coll, algo, n, p, m, **kw)
+    count = n * p * 1003 if coll == "allreduce" else p * 1003
+    e_in = n * count if coll == "reducescatter" else count
+    ins = [allreduce_input(e_in, "bfloat16", kind, 8, r) for r in range(n)]
+    got = run_gpu(text, coll, n, "bfloat16", ins, mode="direct" if mode == "push" else mode, pull=mode != "push")
+    assert_bits_equal(got, oracle.run(oracle.parse(text), ins, "bfloat16", bf16="partials"))
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+@pytest.mark.parametrize("kind", ["uniform", "normal"])
+def test_bf16_partials_relay_golden(mode, kind):
+    # rs_relay_n4: a partial sum relayed through a plain receive is rounded there (reading R6)
+    text = golden("rs_relay_n4.xml")
+    ins = [allreduce_input(4 * 2053, "bfloat16", kind, 9, r) for r in range(4)]
+    got = run_gpu(text, "reducescatter", 4, "bfloat16", ins, mode=mode)
+    assert_bits_equal(got, oracle.run(oracle.parse(text), ins, "bfloat16", bf16="partials"))
 
 
 @pytest.mark.parametrize("dtype,tol", [("float32", 1e-6), ("bfloat16", 1e-2)])

@@ -10,7 +10,7 @@ from paper_2111_04867_b200 import taccl
 from paper_2111_04867_b200.generator import generate
 
 STEP = re.compile(r"\s+(\d+) (\w+) src=(\w+):(\d+) dst=(\w+):(\d+) cnt=(\d+) seq=(\d+) poff=(-?\d+) "
-                  r"deps=([\d:,]*) post=([\d:,]*) part=(\d+)/(\d+) fuse=(\d+) fwd=(\d+)")
+                  r"deps=([\d:,]*) post=([\d:,]*) part=(\d+)/(\d+) fuse=(\d+) fwd=(\d+) pf=(\d+)")
 TB = re.compile(r"tb (\d+) send=(-?\d+) recv=(-?\d+) chan=(\d+) indep=(\d)")
 
 
@@ -26,7 +26,7 @@ def plan(text, rank, ll=False):
         tbs[-1]["steps"].append({"op": m[2], "src": (m[3], int(m[4])), "dst": (m[5], int(m[6])), "cnt": int(m[7]),
                                  "seq": int(m[8]), "poff": int(m[9]), "deps": [d for d in m[10].split(",") if d],
                                  "post": [d for d in m[11].split(",") if d], "part": int(m[12]), "nparts": int(m[13]),
-                                 "fuse": int(m[14])})
+                                 "fuse": int(m[14]), "pf": int(m[16])})
     return tbs
 
 
@@ -110,3 +110,43 @@ def test_plan_dump_errors():
         taccl.plan_dump("<algo", 0)
     with pytest.raises(taccl.TacclError):
         taccl.plan_dump(generate("allgather", "ring", 2, 1, 1), 5)
+
+
+# ---------------------------------------------------------------- bf16 partials (reading R6)
+P_SRC, P_IN, P_KEEP, P_OUT, P_MIX = 1, 2, 4, 8, 16
+
+
+def test_ring_partial_flags_by_hand():
+    # ring AR n=3, rank 0 (generator/templates.py): tb1 receives chunk 2 from rank 1 and
+    # reduces it into o[2] (its first rrc: both operands bf16 -> no P_IN / P_SRC); tb0 sends o[2]
+    # on to rank 2, whose receive is an rrc -> the send is fp32 (P_OUT) from the shadow that the
+    # rrc keeps (P_KEEP). tb1's second rrc (chunk 0) receives rank 1's partial (P_IN); it is
+    # fused with the send of the finished chunk to a plain receive: bf16 forward, nothing kept.
+    text = generate("allreduce", "ring", 3, 1, 1)
+    for ll in (False, True):
+        tb0, tb1 = plan(text, 0, ll)
+        assert [(x["op"], x["pf"]) for x in tb1["steps"]] == [("RRC", P_KEEP), ("RRCS", P_IN), ("SENT", 0), ("SEND", 0)]
+        assert [(x["op"], x["pf"]) for x in tb0["steps"]] == [("SEND", 0), ("SEND", P_OUT), ("RECV", 0), ("RECV", 0)]
+
+
+def test_relay_and_direct_schedules_carry_no_partials():
+    # a reduced value relayed through a plain receive is rounded there; all-pairs (direct)
+    # reductions are one fused chain per chunk whose inputs are the peers' inputs
+    from conftest import golden
+    for text, n in ((golden("rs_relay_n4.xml"), 4), (generate("allreduce", "direct", 4, 1, 1), 4),
+                    (generate("allreduce", "oneshot", 4, 1, 1), 4)):
+        for r in range(n):
+            assert all(x["pf"] == 0 for tb in plan(text, r) for x in tb["steps"])
+
+
+def test_ring_rs_middle_hops_move_fp32():
+    # ring RS n=4: chunk d is reduced along d+1 -> d+2 -> d+3 -> d; every hop after the first
+    # sends a partial (P_OUT on the sender, P_IN on the receiving rrc); rrc+send fusions forward
+    # their fp32 accumulator directly and keep no shadow
+    text = generate("reducescatter", "ring", 4, 1, 1)
+    for r in range(4):
+        steps = [x for tb in plan(text, r) for x in tb["steps"]]
+        ins = [x for x in steps if x["op"] in ("RRC", "RRCS")]
+        assert sum(1 for x in ins if x["pf"] & P_IN) == 2  # 3 receive-reduces, the first is bf16
+        assert all(x["pf"] & P_OUT for x in steps if x["op"] == "RRCS")
+        assert not any(x["pf"] & P_KEEP for x in steps if x["op"] == "RRCS")
