@@ -7,10 +7,10 @@
 A step is one collective call = one launch of the whole hot path (SURVEY.md §8(a) a0–a8).
   N = 1: Allgather with one rank = the local copy path, 1 GiB bf16 output (north star
          "1 GPU (local copy path vs HBM roofline)"); value = read+write bytes / time.
-  N > 1: Allgather, direct (all-pairs, uc-max) schedule, 1 GiB bf16 output, one process per
-         GPU, peers' HBM mapped with CUDA IPC; value = aggregate bus bandwidth over all ranks
-         (N x nccl-tests busbw, busbw = S/t x (N-1)/N); busbw per GPU and its fraction of
-         900 GB/s NVLink are reported beside it.
+  N > 1: Allgather, the size-specialised default schedule set, 1 GiB bf16 output, one process
+         per GPU, peers' HBM mapped with CUDA IPC; value = the metric, bus bandwidth per GPU
+         (nccl-tests busbw = S/t x (N-1)/N, t = max over ranks); its fraction of 900 GB/s
+         NVLink and the whole-job aggregate (N x busbw) are reported beside it.
 Inputs are resident in HBM before the timed region and larger than L2 (126 MB), so no
 flush is needed. Timing: W warm-up calls, barrier + synchronize, K calls between CUDA
 events on the launching stream, synchronize, max over ranks.
@@ -147,6 +147,48 @@ def cpu_oracle_baseline(size_bytes, n, algo, seconds=10.0):
             "host_cores_available": len(os.sched_getaffinity(0))}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def c1_oracle_timing(reps=21):
+    """BASELINE.json configs[0] (C1): the Allgather ring schedule, 2 ranks, 2 chunks per rank,
+    4 KB int32 output (tests/golden/c1_ag_ring_n2_p2.xml), through the CPU oracle: parse +
+    validate and execute timed separately, median of `reps` runs each."""
+    import numpy as np
+
+    import oracle
+    from oracle.validate import build_graph, topo_order
+    text = open(os.path.join(ROOT, "tests", "golden", "c1_ag_ring_n2_p2.xml")).read()
+    ins = [((r << 16) + np.arange(512)).astype(np.int32) for r in range(2)]
+    tv, tx = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        prog = oracle.parse(text)
+        ok = oracle.validate(prog).ok
+        t1 = time.perf_counter()
+        graph = build_graph(prog)
+        order = topo_order(graph)
+        outs = oracle.run(prog, ins, "int32", graph=graph, order=order)
+        t2 = time.perf_counter()
+        tv.append(t1 - t0)
+        tx.append(t2 - t1)
+    j = np.arange(1024)
+    exact = ok and all(np.array_equal(o, ((j >> 9) << 16) + (j & 511)) for o in outs)  # the worked example
+    return {"config": "C1: Allgather ring, 2 ranks, 2 chunks/rank, 4 KB int32 output (CPU oracle)",
+            "parse_validate_ms": round(statistics.median(tv) * 1e3, 4),
+            "execute_ms": round(statistics.median(tx) * 1e3, 4),
+            "runs": reps, "statistic": "median", "bit_exact_vs_worked_example": bool(exact),
+            "cores": f"1 of {len(os.sched_getaffinity(0))}", "cpu_model": cpu_model(),
+            "execute_gbs": round(4096 / statistics.median(tx) / 1e9, 6)}
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -251,7 +293,7 @@ def main():
         busbw = None
     else:
         busbw = S / t_step * busbw_factor(coll, n) / 1e9
-        value = n * busbw
+        value = busbw  # the metric: bus GB/s per GPU (nccl-tests busbw; the aggregate is beside it)
         egress = S * (n - 1) / n  # algorithmic NVLink bytes per launch per GPU
         ach = egress / t_step / 1e9
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_REF, "unit": "GB/s",
@@ -292,7 +334,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         assert torch.equal(h_out.view(torch.int16)[rank * count:(rank + 1) * count], h_in.view(torch.int16))
-        ev = (2.0 * S if n == 1 else n * S * busbw_factor(coll, n)) / te / 1e9
+        ev = (2.0 * S if n == 1 else S * busbw_factor(coll, n)) / te / 1e9
         e2e = {"value": round(ev, 2), "unit": "GB/s", "h2d_bytes_per_step": count * 2,
                "d2h_bytes_per_step": n * count * 2, "ms_per_step": round(te * 1e3, 3),
                "timing": "host wall clock around taccl_run_host (H2D + kernel + D2H + stream sync), max over ranks"}
@@ -307,13 +349,16 @@ def main():
                            "plan": comm.plan_info("allgather", count, taccl.BFLOAT16),
                            "l2": "inputs and outputs > 126 MB L2 (no flush needed)",
                            "value_definition": ("read+write bytes / t (local copy path)" if n == 1 else
-                                                "aggregate busbw = N * S/t * (N-1)/N")},
+                                                "busbw per GPU = S/t * (N-1)/N (nccl-tests; max-over-ranks t)")},
                 "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
         if busbw is not None:
             line["busbw_per_gpu"] = round(busbw, 2)
             line["busbw_frac_of_900"] = round(busbw / NVLINK_NOMINAL, 4)
+            line["aggregate_busbw"] = round(n * busbw, 2)  # whole job: N x busbw
         if n == 1 and not a.no_cpu:
             line["cpu_baseline"] = cpu_oracle_baseline(S, n, algo_used)
+            line["cpu_baseline"]["cpu_model"] = cpu_model()
+            line["c1_oracle"] = c1_oracle_timing()
         print(json.dumps(line))
     if world > 1:
         dist.barrier()

@@ -1078,7 +1078,8 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         const bool red = st.op == K_RRC || st.op == K_RRCS || fz;
         if (PROBE(22) && st.op == K_SEND) src = nullptr;  // timing probe only: no source load
         if (A.dtype == TACCL_BFLOAT16 && st.pflags) {  // bf16 partials (reading R6)
-          const bool s32 = (st.pflags & P_SRC) != 0;
+          // fp32 source: an rrc's P_SRC, or a send of partials (P_OUT: from the shadow)
+          const bool s32 = (st.pflags & P_SRC) || (st.op == K_SEND && (st.pflags & P_OUT));
           const char* xs = s32 ? shadow_base(c, st.srcbuf) + 2 * (int64_t)st.srcoff * cbytes : src;
           char* d32 = (st.pflags & P_KEEP) ? shadow_base(c, st.dstbuf) + 2 * (int64_t)st.dstoff * cbytes : nullptr;
           const bool ok = ll_px(R, st, fused, tb.send, my_staged, parity_off, xs, s32, dst, d32, cbytes, ll_cb, l0, l1,

@@ -326,6 +326,9 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
       for (const Step& st : tb.steps) {
         const int w = (pflag(g.id, tb.id, st.s) & P_IN) ? 2 : 1;
         if (st.type == ST_RRC) {
+          // an fp32 message's slot starts at an even chunk offset: soff * cbytes is then a
+          // multiple of 4 bytes (bf16 chunks are an even number of bytes), as floats need
+          if (w == 2) stage_total[g.id] += stage_total[g.id] & 1;
           soff[{g.id, tb.id, st.s}] = stage_total[g.id];
           stage_total[g.id] += w * st.cnt;
         }

@@ -40,6 +40,50 @@ def gen(coll, al, n):
     return generate(coll, parts[0], n, p, m, pair="split" not in parts[1:])
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_gbs(coll, text, n, S, es, cap):
+    """The oracle (test infrastructure, oracle/) timed on this host, single thread, on the
+    point's own schedule: S / t at S <= cap, else on a cap-byte sample of the same workload
+    (count scaled down). Returns (GB/s, sample bytes, seconds)."""
+    import time
+
+    import numpy as np
+
+    import oracle
+    from paper_2111_04867_b200.inputs import allreduce_input, random_bits
+    Ss = min(S, cap)
+    dtn = "bfloat16" if es == 2 else "float32"
+    count = Ss // es if coll == "allreduce" else Ss // es // n
+    e_in = n * count if coll in ("alltoall", "reducescatter") else count
+    texts = text if isinstance(text, list) else [text]
+    prog = None
+    for t in texts:  # the default set's member for this size
+        p = oracle.parse(t)
+        if p.min_bytes <= S < p.max_bytes:
+            prog = p
+    prog = prog or oracle.parse(texts[-1])
+    if coll in ("allreduce", "reducescatter"):
+        ins = [allreduce_input(e_in, dtn, "intval", 50, r) for r in range(n)]
+    else:
+        ins = [random_bits(e_in, dtn, 50, r) for r in range(n)]
+    from oracle.validate import build_graph, topo_order
+    graph = build_graph(prog)  # parse + happens-before graph outside the timed execution
+    order = topo_order(graph)
+    t0 = time.perf_counter()
+    oracle.run(prog, ins, dtn, graph=graph, order=order)
+    t = time.perf_counter() - t0
+    return Ss / t / 1e9, Ss, t
+
+
 def factor(coll, n):
     if n == 1:
         return 2.0
@@ -107,6 +151,11 @@ def timeit(fn, stream, world, target_ms=50.0):
     return ms, iters
 
 
+HBM_PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6549.8
+CPU = cpu_model()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--colls", default="allgather,alltoall,allreduce,reducescatter")
@@ -117,6 +166,10 @@ def main():
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (no host overhead)")
     ap.add_argument("--algos", default=None, help="comma list overriding the per-collective defaults")
+    ap.add_argument("--oracle-cap", type=int, default=0,
+                    help="time the CPU oracle per point on rank 0 (sample <= this many bytes; 0 = off)")
+    ap.add_argument("--peak-nvlink", type=float, default=705.0,
+                    help="measured per-direction NVLink ceiling for roofline fractions (profiles/r01_p2p_probe.txt)")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -205,8 +258,27 @@ def main():
             rec["taccl_best"] = best[1]
             rec["taccl_best_us"] = best[0]
             rec["taccl_best_busbw"] = rec[f"taccl_{best[1]}_busbw"]
+            # the library's own choice: the size-specialised default set when it was run
+            dflt = "auto" if "taccl_auto_us" in rec else best[1]
+            rec["taccl_default"] = dflt
+            bw = rec[f"taccl_{dflt}_busbw"]
+            if n == 1:  # copy path: read+write bytes vs the measured HBM copy peak
+                rec["roofline_frac"] = round(bw / HBM_PEAK, 4)
+            else:  # busbw vs the measured NVLink ceiling per direction, and vs the nominal 900
+                rec["roofline_frac"] = round(bw / a.peak_nvlink, 4)
+                rec["frac_of_900"] = round(bw / 900.0, 4)
             if "nccl_us" in rec:
-                rec["speedup_vs_nccl"] = round(rec["nccl_us"] / best[0], 3)
+                rec["speedup_vs_nccl"] = round(rec["nccl_us"] / rec[f"taccl_{dflt}_us"], 3)
+                rec["speedup_vs_nccl_best_variant"] = round(rec["nccl_us"] / best[0], 3)
+            if a.oracle_cap:
+                if rank == 0:
+                    gbs, ss, sec = oracle_gbs(coll, gen(coll, dflt, n), n, S, es, a.oracle_cap)
+                    rec["oracle_gbs"] = round(gbs, 4)
+                    rec["oracle_sample_bytes"] = ss
+                    rec["oracle_s"] = round(sec, 4)
+                    rec["oracle_cores"] = f"1 of {len(os.sched_getaffinity(0))} ({CPU})"
+                if world > 1:
+                    dist.barrier()
             if rank == 0:
                 print(json.dumps(rec), flush=True)
                 out_f.write(json.dumps(rec) + "\n")
