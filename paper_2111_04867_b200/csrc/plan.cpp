@@ -531,6 +531,8 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
         }
       }
     }
+    for (const KStep& x : rp.steps)
+      if ((x.pflags & (P_KEEP | P_SRC)) || (x.op == K_SEND && (x.pflags & P_OUT))) rp.shadow = true;
     // pull kinds: by default only plain rrcs read in place — measured on B200
     // (profiles/r01_pull_n2.txt, r01_pull_n4.txt): a plain rrc (RS n=2) goes from push +
     // serialised reduce to one pass (497 -> 642 GB/s busbw); an rrc fused with its send (AR

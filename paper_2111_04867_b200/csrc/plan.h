@@ -15,7 +15,9 @@ struct RankPlan {
   int stage2_chunks = 0;       // staged mode: every receive's slot (chunk units)
   int scratch_chunks = 0;      // EF scratch buffer (chunk units)
   int fused_chains = 0;
-  bool partials = false;       // some step carries bf16 partial flags (needs the shadow region)
+  bool partials = false;       // some step carries bf16 partial flags
+  bool shadow = false;         // some step reads or writes the fp32 shadow of o / s (bf16 calls
+                               // then need the shadow region: 2 x (o + s) bytes)
 };
 
 // `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables);

@@ -67,7 +67,7 @@ struct Algo {
   std::vector<int> wsum;        // per rank
   int fused_chains = 0;
   bool has_pull = false;  // some send of the direct plan is read in place (pull mode applies)
-  bool partials = false;  // bf16 partial flags on some step (bf16 calls need the shadow region)
+  bool shadow = false;  // bf16 partials read/write the fp32 shadow (bf16 calls need its region)
   int max_o_chunks = 0, max_s_chunks = 0;
 };
 
@@ -303,7 +303,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   G->need = G->staging_off + (int64_t)a->max_stage_chunks * G->chunk_bytes;
   // bf16 partials: the fp32 shadow of o and s (reading R6), after the staging
   G->shadow_off = G->shadow_s = 0;
-  if (a->partials && elt == 2) {
+  if (a->shadow && elt == 2) {
     G->shadow_off = (G->need + 255) & ~(int64_t)255;
     G->shadow_s = 2 * (int64_t)a->max_o_chunks * G->chunk_bytes;
     G->need = G->shadow_off + G->shadow_s + 2 * (int64_t)a->max_s_chunks * G->chunk_bytes;
@@ -794,7 +794,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->max_scratch_chunks = std::max(a->max_scratch_chunks, plans[r].scratch_chunks);
     a->max_stage_chunks = std::max(a->max_stage_chunks, plans[r].stage_chunks);
     a->max_stage2_chunks = std::max(a->max_stage2_chunks, plans[r].stage2_chunks);
-    a->partials = a->partials || plans[r].partials || plans_ll[r].partials;
+    a->shadow = a->shadow || plans[r].shadow || plans_ll[r].shadow;
     a->max_o_chunks = std::max(a->max_o_chunks, P_o_chunks[r]);
     a->max_s_chunks = std::max(a->max_s_chunks, plans[r].scratch_chunks);
     a->fused_chains += plans[r].fused_chains;

@@ -8,7 +8,8 @@ from .tuned import default_schedules  # noqa: F401
 
 def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), pair=True, **kw):
     """EF v1 text for (collective, algorithm) — the one-call entry the CLI and tests use.
-    pair=False lowers sends and receives into separate threadblocks."""
+    pair=False lowers sends and receives into separate threadblocks; pair="peer" pairs only by
+    peer (no relay-first threadblocks, lowering.py)."""
     if algo == "hier":
         if nranks % 2:
             raise ValueError("hier needs 2 x k ranks")
@@ -25,4 +26,6 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
     name = f"{alg.name}_m{instances}"
     if not pair:
         name += "_split"
+    elif pair == "peer":
+        name += "_peer"
     return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name, pair=pair)

@@ -13,9 +13,11 @@ The passes, in the paper's order:
   writer of what it reads and, when it writes, on the last writer and every reader since
   (only cross-threadblock edges are emitted; program order covers the rest).
 * Threadblock allocation: each threadblock sends to at most one GPU and
-  receives from at most one GPU; steps keep the abstract order. A peer that is both sent to
-  and received from shares one threadblock; leftover send-only and receive-only peers are
-  paired in order of first use (a ring lands in one threadblock).
+  receives from at most one GPU; steps keep the abstract order. Relay hops first: the peer a
+  rank receives chunks from and the peer it forwards them to (at least two such hops) share
+  a threadblock, so receive and forward are adjacent steps (fused by the executor); then a
+  peer that is both sent to and received from shares one threadblock; leftover send-only and
+  receive-only peers are paired in order of first use (a ring lands in one threadblock).
 * Instances: written as the header's `instances`; the executor runs the
   m copies (docs/SCHEDULE.md).
 """
@@ -166,8 +168,22 @@ def _allocate_tbs(lst, pair=True):
         if ins["type"] in ("r", "rrc") and ins["peer"] not in recv_peers:
             recv_peers.append(ins["peer"])
     tbs, by_send, by_recv = [], {}, {}
+    # relays first: a receive from q whose chunks the next instruction sends on to q' (a ring's
+    # or a relay path's hop) shares a threadblock with the sends to q', so the two steps are
+    # adjacent and the executor runs them as one pass (recv-copy-send / recv-reduce-copy-send,
+    # SURVEY.md §8(f) row 1); pairs with the most such hops first, each peer in one pair
+    if pair and pair != "peer":  # pair="peer": the same-peer pairing alone (A/B measurements)
+        hops = {}
+        for a, b in zip(lst, lst[1:]):
+            if a["type"] in ("r", "rrc") and b["type"] == "s" and b["src"] == a["dst"] and b["cnt"] == a["cnt"]:
+                hops[(a["peer"], b["peer"])] = hops.get((a["peer"], b["peer"]), 0) + 1
+        for (qr, qs), c in sorted(hops.items(), key=lambda kv: (-kv[1], kv[0])):
+            if qr in by_recv or qs in by_send or c < 2:
+                continue
+            by_send[qs] = by_recv[qr] = len(tbs)
+            tbs.append((qs, qr))
     for q in send_peers:
-        if pair and q in recv_peers:
+        if pair and q in recv_peers and q not in by_send and q not in by_recv:
             by_send[q] = by_recv[q] = len(tbs)
             tbs.append((q, q))
     ls = [q for q in send_peers if q not in by_send]
