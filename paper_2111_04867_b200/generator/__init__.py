@@ -6,10 +6,12 @@ from . import templates  # noqa: F401
 from .tuned import default_schedules  # noqa: F401
 
 
-def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), pair=True, **kw):
+def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), pair=True, merge=True,
+             **kw):
     """EF v1 text for (collective, algorithm) — the one-call entry the CLI and tests use.
     pair=False lowers sends and receives into separate threadblocks; pair="peer" pairs only by
-    peer (no relay-first threadblocks, lowering.py)."""
+    peer (no relay-first threadblocks, lowering.py); merge=False keeps every transfer its own
+    step (no contiguity coalescing, lowering.coalesce)."""
     if algo == "hier":
         if nranks % 2:
             raise ValueError("hier needs 2 x k ranks")
@@ -28,4 +30,7 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
         name += "_split"
     elif pair == "peer":
         name += "_peer"
-    return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name, pair=pair)
+    if not merge:
+        name += "_nomerge"
+    return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name, pair=pair,
+                 merge=merge)

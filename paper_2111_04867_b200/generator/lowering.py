@@ -5,6 +5,8 @@ The passes, in the paper's order:
 * Buffer allocation: user input/output, runtime scratch; chunks are
   indices into them; a rank's own chunks are copied input -> output "at the end" (one
   `cpy` threadblock that runs concurrently, reading G9).
+* Contiguity: final deliveries on the same link are merged into one
+  multi-chunk transfer (`coalesce`), so they become one cnt > 1 step.
 * Instruction generation: every transfer becomes a send on the sender and
   a receive (`r`, or `rrc` when it reduces) on the receiver, on concrete buffer indices.
   Transfers of several chunks stay one instruction (`cnt > 1`) when both sides are
@@ -25,7 +27,7 @@ from __future__ import annotations
 
 import math
 
-from .algorithm import Algorithm, a2a_parts
+from .algorithm import Algorithm, Transfer, a2a_parts
 
 
 class LoweringError(Exception):
@@ -40,6 +42,45 @@ def _initial(alg: Algorithm, r: int):
     if alg.coll == "alltoall":
         return {(r * n + d) * p + k: ("i", d * p + k) for d in range(n) for k in range(p)}
     return {k: ("i", k) for k in range(n * p)}  # allreduce, reducescatter
+
+
+def coalesce(alg: Algorithm) -> Algorithm:
+    """Contiguity for the executor (§5.1: chunks sent consecutively over a link
+    can be sent together, saving a per-transfer latency). On B200 one executor step costs ~2-4 us
+    of flag round trips and CTA work at small sizes (the paper's alpha regime), so transfers on the
+    same link are merged into one multi-chunk transfer when that loses no pipelining:
+      * both deliver their chunks to their final holder (the receiver forwards none of them:
+        a forward's timing could be delayed) and both reduce or neither does;
+      * the later one's chunks are already at the sender (strictly) before the earlier one is
+        sent, so waiting for them delays nothing.
+    The merged transfer leaves at the earlier send time and arrives at the later arrival.
+    Lowering then emits it as one cnt > 1 step where both sides are contiguous (_runs)."""
+    arrivals, sends = {}, {}  # (rank, chunk) -> arrival times at / send times from the rank
+    for t in alg.transfers:
+        for c in t.chunks:
+            arrivals.setdefault((t.dst, c), []).append(t.arrive_time)
+            sends.setdefault((t.src, c), []).append(t.send_time)
+
+    def forwarded(r, c, after):  # the rank sends chunk c (e.g. a partial sum) once it arrived
+        return any(x >= after for x in sends.get((r, c), []))
+
+    def ready(r, c, at, by):  # every delivery of c to r before `by` was there before `at`
+        return all(x < at for x in arrivals.get((r, c), []) if x <= by)
+
+    out = Algorithm(alg.name, alg.coll, alg.nranks, alg.chunks_per_rank)
+    groups = {}  # (src, dst) -> index of the open merged transfer in out.transfers
+    for t in sorted(alg.transfers, key=lambda t: (t.send_time, t.src, t.dst)):
+        final = not any(forwarded(t.dst, c, t.arrive_time) for c in t.chunks)
+        g = groups.get((t.src, t.dst, t.reduce)) if final else None
+        if g is not None and all(ready(t.src, c, out.transfers[g].send_time, t.send_time) for c in t.chunks):
+            m = out.transfers[g]
+            out.transfers[g] = Transfer(tuple(sorted(m.chunks + t.chunks)), m.src, m.dst, m.send_time,
+                                        max(m.arrive_time, t.arrive_time), t.reduce)
+            continue
+        out.transfers.append(t)
+        if final:
+            groups[(t.src, t.dst, t.reduce)] = len(out.transfers) - 1
+    return out
 
 
 def _dst_locations(alg: Algorithm):
@@ -230,11 +271,15 @@ def _ranges(ins):
     return reads, writes
 
 
-def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, name=None, pair=True) -> str:
+def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, name=None, pair=True,
+          merge=True) -> str:
     """Lower `alg` to EF v1 text (docs/SCHEDULE.md). pair: share one threadblock between the
-    send to and the receive from the same peer (see _allocate_tbs)."""
+    send to and the receive from the same peer (see _allocate_tbs); merge: coalesce final
+    deliveries on a link into multi-chunk transfers (see coalesce)."""
     if instances < 1:
         raise LoweringError("instances must be >= 1")
+    if merge:
+        alg = coalesce(alg)
     n, p = alg.nranks, alg.chunks_per_rank
     instrs, n_scratch = _instructions(alg)
     _check_pairing(instrs)

@@ -214,3 +214,43 @@ def test_default_sets_cover_all_sizes_once(coll, n):
     for text in default_schedules(coll, n):
         v = oracle.validate(text)
         assert v.ok, f"{v.kind}: {v.msg}"
+
+
+# ---------------------------------------------------------------- contiguity (lowering.coalesce)
+
+def _steps(text, rank=0):
+    prog = oracle.parse(text)
+    return [st for tb in prog.gpus[rank].tbs for st in tb.steps]
+
+
+@pytest.mark.parametrize("n,p", [(2, 4), (4, 2), (8, 4)])
+def test_direct_alltoall_chunks_travel_together(n, p):
+    # chunks sent consecutively over a link may be sent together. A direct
+    # Alltoall's p chunks per peer are final deliveries from the input: one cnt=p send and one
+    # cnt=p receive per peer (`s r s r s r s r` for n=2, p=4 before)
+    st = _steps(generate("alltoall", "direct", n, p, 1))
+    assert sorted(s.type for s in st) == sorted(["s"] * (n - 1) + ["r"] * (n - 1) + ["cpy"])
+    assert all(s.cnt == p for s in st)
+    unmerged = _steps(generate("alltoall", "direct", n, p, 1, merge=False))
+    assert len(unmerged) == 2 * (n - 1) * p + 1
+
+
+def test_ring_hops_keep_their_pipelining():
+    # a ring forwards every chunk: merging the p chunks of a hop would delay the first one's
+    # forward, so a p=2 ring keeps one step per chunk and hop
+    n, p = 4, 2
+    st = _steps(generate("allgather", "ring", n, p, 1))
+    assert sum(s.type == "s" for s in st) == (n - 1) * p and all(s.cnt == 1 for s in st if s.type == "s")
+
+
+def test_merged_schedules_compute_the_same_result():
+    from paper_2111_04867_b200.inputs import allreduce_input
+    for coll, algo, n, p in [("alltoall", "direct", 4, 4), ("reducescatter", "direct", 4, 2),
+                             ("allreduce", "direct", 4, 2), ("alltoall", "hier", 8, 2)]:
+        count = n * p * 5 if coll in ("allreduce",) else p * 5
+        e_in = n * count if coll in ("alltoall", "reducescatter") else count
+        ins = [allreduce_input(e_in, "int32", "bits", 60, r) for r in range(n)]
+        a = oracle.run(oracle.parse(generate(coll, algo, n, p, 1)), ins, "int32")
+        b = oracle.run(oracle.parse(generate(coll, algo, n, p, 1, merge=False)), ins, "int32")
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+        assert all(np.array_equal(x, y) for x, y in zip(a, oracle.expected_outputs(coll, ins, "int32")))
