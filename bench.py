@@ -117,7 +117,7 @@ def resolve_algo(algo, n, S):
     if algo != "auto":
         return algo
     from paper_2111_04867_b200.generator.tuned import ranges
-    return next(al for al, lo, hi in ranges("allgather", n) if lo <= S < hi)
+    return next(r[0] for r in ranges("allgather", n) if r[1] <= S < r[2] and (len(r) == 3 or "bfloat16" in r[3]))
 
 
 def cpu_oracle_baseline(size_bytes, n, algo, seconds=10.0):

@@ -160,8 +160,9 @@ taccl_result_t taccl_unregister_buffer(const void* ptr);
  * matching, acyclicity, races, and the collective's postcondition "each chunk reaches its
  * destination GPUs as specified by the collective"; App. B
  * PAPER.md:1324-1330) and planned for the device. The algorithm is registered under
- * (coll, nranks, [minBytes, maxBytes)) for selection by taccl_run — the paper keeps
- * size-specialised algorithms per collective. `*out` may be NULL.
+ * (coll, nranks, [minBytes, maxBytes), dtypes) for selection by taccl_run — the paper keeps
+ * size-specialised algorithms per collective; the optional dtypes
+ * attribute restricts the element types (docs/SCHEDULE.md). `*out` may be NULL.
  * Ownership: the text is copied (not retained); the library owns the device plan until
  * taccl_free or taccl_comm_destroy. Requires an initialized communicator whose nranks
  * matches. Errors: INVALID_SCHEDULE ("<class>: <message>", first failing check),

@@ -155,6 +155,11 @@ def parse(text: str) -> Program:
     )
     if prog.inplace != 0:
         raise ScheduleError("syntax", "inplace=1 is not supported (reading G10)")
+    # optional dtypes="...": which element types a runtime may select the algorithm for (a
+    # selection attribute only; it changes nothing the program computes)
+    for d in filter(None, (root.get("dtypes") or "").split(",")):
+        if d not in ("int32", "float32", "bfloat16"):
+            raise ScheduleError("syntax", f"dtypes: unknown element type {d!r}")
     gpus = [g for g in root if g.tag == "gpu"]
     if any(g.tag != "gpu" for g in root):
         raise ScheduleError("syntax", "<algo> may only contain <gpu>")

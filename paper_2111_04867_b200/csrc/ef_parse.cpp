@@ -197,6 +197,23 @@ Program parse_ef(const char* text, size_t len) {
     (strcmp(key, "minBytes") == 0 ? prog.min_bytes : prog.max_bytes) = v;
   }
   if (to_int(t, "inplace", 0) != 0) fail("inplace=1 is not supported (reading G10)");
+  // optional dtypes="int32,float32,bfloat16": the element types taccl_run may select this
+  // algorithm for (a size-specialised set can differ per type; default: all)
+  if (t.attrs.count("dtypes")) {
+    prog.dtypes = 0;
+    const std::string& v = t.attrs["dtypes"];
+    size_t i = 0;
+    while (i <= v.size()) {
+      size_t j = v.find(',', i);
+      if (j == std::string::npos) j = v.size();
+      const std::string d = v.substr(i, j - i);
+      if (d == "int32") prog.dtypes |= 1u << TACCL_INT32;
+      else if (d == "float32") prog.dtypes |= 1u << TACCL_FLOAT32;
+      else if (d == "bfloat16") prog.dtypes |= 1u << TACCL_BFLOAT16;
+      else fail("dtypes: unknown element type '" + d + "'");
+      i = j + 1;
+    }
+  }
   if (prog.nranks > 4096 || prog.p > 4096) fail("nranks or chunks_per_rank too large");
 
   // <gpu> elements

@@ -55,6 +55,7 @@ struct Algo {
   Coll coll;
   int nranks, p, instances;
   uint64_t min_bytes, max_bytes;
+  uint32_t dtypes = 7;  // element types this algorithm is selected for (EF dtypes attribute)
   int max_scratch_chunks = 0, max_stage_chunks = 0, max_stage2_chunks = 0, max_steps_cnt = 1;
   // n = 1 plan that is one input -> output `cpy` (no deps): runs as the lean copy kernel
   bool lean_copy = false;
@@ -180,10 +181,10 @@ uint64_t select_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
   return (uint64_t)n * count * elt;
 }
 
-Algo* select_algo(taccl_coll_t coll, uint64_t S) {
+Algo* select_algo(taccl_coll_t coll, uint64_t S, taccl_dtype_t dtype) {
   for (auto it = g.algos.rbegin(); it != g.algos.rend(); ++it) {  // latest load wins
     Algo* a = *it;
-    if ((int)a->coll == (int)coll && a->nranks == g.nranks && S >= a->min_bytes &&
+    if ((int)a->coll == (int)coll && a->nranks == g.nranks && S >= a->min_bytes && ((a->dtypes >> dtype) & 1) &&
         (a->max_bytes == UINT64_MAX || S < a->max_bytes))
       return a;
   }
@@ -435,7 +436,7 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
   if (!sendbuf || !recvbuf) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
   const size_t ib = in_bytes(coll, count, elt, n), ob = out_bytes(coll, count, elt, n);
   const bool overlapping = (const char*)sendbuf < (const char*)recvbuf + ob && (const char*)recvbuf < (const char*)sendbuf + ib;
-  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n));
+  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n), dtype);
   if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
   Geometry G;
   if ((rc = geometry(a, coll, count, elt, 1, base_off, &G))) return rc;
@@ -773,6 +774,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->instances = P.instances;
     a->min_bytes = P.min_bytes;
     a->max_bytes = P.max_bytes;
+    a->dtypes = P.dtypes;
     for (const Gpu& gp : P.gpus) P_o_chunks.push_back(gp.o_chunks);
   } catch (const SchedError& e) {
     return fail(TACCL_ERR_INVALID_SCHEDULE, e.kind + ": " + e.msg);
@@ -846,7 +848,7 @@ taccl_result_t taccl_run_emulated(taccl_coll_t coll, const void* const* sendbufs
   if (!sendbufs || !recvbufs) return fail(TACCL_ERR_INVALID_ARG, "null buffer array");
   if (count == 0) return TACCL_SUCCESS;
   const int elt = elt_size(dtype), n = g.nranks;
-  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n));
+  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n), dtype);
   if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
   Geometry G;
   if ((rc = geometry(a, coll, count, elt, n, 0, &G))) return rc;
@@ -938,7 +940,7 @@ taccl_result_t taccl_plan_info(taccl_coll_t coll, size_t count, taccl_dtype_t dt
   taccl_result_t rc = check_common(coll, count, dtype);
   if (rc) return rc;
   const int elt = elt_size(dtype);
-  Algo* a = select_algo(coll, select_bytes(coll, count, elt, g.nranks));
+  Algo* a = select_algo(coll, select_bytes(coll, count, elt, g.nranks), dtype);
   if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
   Geometry G;
   if ((rc = geometry(a, coll, count, elt, 1, 0, &G))) return rc;

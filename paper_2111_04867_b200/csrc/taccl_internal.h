@@ -43,6 +43,7 @@ struct Program {
   Coll coll = C_AG;
   int nranks = 0, p = 1, instances = 1;
   uint64_t min_bytes = 0, max_bytes = 0;  // max_bytes == UINT64_MAX means inf
+  uint32_t dtypes = 7;                    // bit taccl_dtype_t: element types it is selected for
   std::vector<Gpu> gpus;
 };
 

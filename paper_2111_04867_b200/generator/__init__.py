@@ -7,7 +7,7 @@ from .tuned import default_schedules  # noqa: F401
 
 
 def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), pair=True, merge=True,
-             **kw):
+             dtypes=None, **kw):
     """EF v1 text for (collective, algorithm) — the one-call entry the CLI and tests use.
     pair=False lowers sends and receives into separate threadblocks; pair="peer" pairs only by
     peer (no relay-first threadblocks, lowering.py); merge=False keeps every transfer its own
@@ -33,4 +33,4 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
     if not merge:
         name += "_nomerge"
     return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name, pair=pair,
-                 merge=merge)
+                 merge=merge, dtypes=dtypes)

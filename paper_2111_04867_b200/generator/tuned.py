@@ -15,18 +15,20 @@ MiB = 1 << 20
 INF = math.inf
 
 
+BF16 = ("bfloat16",)
+WIDE = ("int32", "float32")
+
+
 def ranges(coll: str, n: int):
-    """[(algo, min_bytes, max_bytes)] covering [0, inf) for `coll` at n ranks; algo may carry
-    a chunk-partitioning suffix `_pK` (K chunks per rank)."""
+    """[(algo, min_bytes, max_bytes[, dtypes])] covering [0, inf) for `coll` at n ranks, for
+    every element type; algo may carry a chunk-partitioning suffix `_pK` (K chunks per rank,
+    PAPER.md:702-711); an entry with a dtypes tuple is selected only for those types."""
     if n == 1:
         return [("direct", 0, INF)]
     if coll == "allgather":
         return [("direct", 0, INF)] if n == 2 else [("direct", 0, 128 * MiB), ("ring", 128 * MiB, INF)]
     if coll == "alltoall":
         return [("direct", 0, INF)]
-    # rings round every hop's bf16 partial (reading R4): at n >= 8 that reaches 1.2e-2 relative
-    # error on U[1,2) inputs, above the north star's 1e-2, so large-n sets keep the direct
-    # (one rounding per element) schedules
     if coll == "allreduce":
         if n == 2:
             return [("oneshot", 0, 16 * MiB), ("direct", 16 * MiB, INF)]
@@ -34,12 +36,14 @@ def ranges(coll: str, n: int):
         if n >= 8:
             return [("oneshot", 0, small), ("direct", small, INF)]
         # below 128 MiB the direct schedule (multi-input reduce with every load in flight) is
-        # ahead of the ring (r01_sweep_n4_graph.jsonl: 64 MiB 185 vs 203 us); at 128-256 MiB
-        # the plain ring is (two boxes: 128 MiB 342-344 vs ring_p2 354-369 us, 256 MiB 633-641
-        # vs 649-672); from 512 MiB 2 chunks per rank pipeline the ring's 2(n-1) hops better
-        # (512 MiB 1226 vs 1237-1259 us; profiles/r01_ar_variants_n4.txt)
-        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("ring", 128 * MiB, 512 * MiB),
-                ("ring_p2", 512 * MiB, INF)]
+        # ahead of the ring (r01_sweep_n4_graph.jsonl: 64 MiB 185 vs 203 us). bf16: a ring
+        # carries fp32 partials on its n-2 middle hops (reading R6; 2x those bytes), so direct
+        # stays ahead at every size (profiles/r02_sweep_ar_ring_ab_n4.txt: 128 MiB 366 vs 463
+        # us, 512 MiB 1356 vs 1723). int32/fp32 partials are the values themselves: there the
+        # ring is ahead at 128-256 MiB (round 1: 342-344 vs 365 us) and 2 chunks per rank
+        # pipeline its 2(n-1) hops best from 512 MiB (profiles/r01_ar_variants_n4.txt)
+        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("direct", 128 * MiB, INF, BF16),
+                ("ring", 128 * MiB, 512 * MiB, WIDE), ("ring_p2", 512 * MiB, INF, WIDE)]
     if coll == "reducescatter":
         if n == 2 or n >= 8:
             return [("direct", 0, INF)]
@@ -51,7 +55,8 @@ def default_schedules(coll: str, n: int):
     """EF texts of the default set for (coll, n), each carrying its size range."""
     from . import generate
     out = []
-    for algo, lo, hi in ranges(coll, n):
+    for algo, lo, hi, *dt in ranges(coll, n):
         name, _, p = algo.partition("_p")
-        out.append(generate(coll, name, n, int(p) if p else 1, 1, min_bytes=lo, max_bytes=hi))
+        out.append(generate(coll, name, n, int(p) if p else 1, 1, min_bytes=lo, max_bytes=hi,
+                            dtypes=dt[0] if dt else None))
     return out

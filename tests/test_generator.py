@@ -207,10 +207,11 @@ def test_measured_profile_topology_synthesizes_correct_schedules():
 def test_default_sets_cover_all_sizes_once(coll, n):
     # size-specialised sets: contiguous, disjoint, [0, inf)
     from paper_2111_04867_b200.generator.tuned import default_schedules, ranges
-    rs = ranges(coll, n)
-    assert rs[0][1] == 0 and rs[-1][2] == math.inf
-    for (_, _, hi), (_, lo, _) in zip(rs, rs[1:]):
-        assert hi == lo
+    for dt in ("int32", "float32", "bfloat16"):  # every element type sees a partition of [0, inf)
+        rs = [r[:3] for r in ranges(coll, n) if len(r) == 3 or dt in r[3]]
+        assert rs[0][1] == 0 and rs[-1][2] == math.inf
+        for (_, _, hi), (_, lo, _) in zip(rs, rs[1:]):
+            assert hi == lo
     for text in default_schedules(coll, n):
         v = oracle.validate(text)
         assert v.ok, f"{v.kind}: {v.msg}"

@@ -387,6 +387,26 @@ def test_default_set_selects_by_size(coll, n, counts):
         comm.destroy()
 
 
+def test_dtypes_attribute_restricts_selection():
+    # EF dtypes="...": an algorithm is selected only for the listed element types
+    n, count = 2, 2 * 1024
+    comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=16 << 20)
+    try:
+        comm.load(generate("allreduce", "direct", n, 1, 1, dtypes=("bfloat16",)))
+        ins = [allreduce_input(count, "int32", "bits", 20, r) for r in range(n)]
+        dev_in = [to_dev(x, "int32") for x in ins]
+        dev_out = [torch.empty(count, dtype=torch.int32, device="cuda") for _ in range(n)]
+        with pytest.raises(taccl.TacclError) as e:
+            comm.run_emulated("allreduce", dev_out, dev_in)
+        assert e.value.code == 3  # NO_ALGO
+        comm.load(generate("allreduce", "ring", n, 1, 1, dtypes=("int32", "float32")))
+        comm.run_emulated("allreduce", dev_out, dev_in)
+        torch.cuda.synchronize()
+        assert_bits_equal([to_host(o, "int32", ins[0]) for o in dev_out], oracle.expected_outputs("allreduce", ins, "int32"))
+    finally:
+        comm.destroy()
+
+
 # ---------------------------------------------------------------- host-buffer runs (e2e path)
 
 @pytest.mark.parametrize("coll,count,piece", [("allgather", 1 << 16, 1 << 12), ("allgather", 1000, 0),
