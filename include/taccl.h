@@ -152,6 +152,34 @@ taccl_result_t taccl_register_buffer(const void* ptr, size_t bytes, const void* 
  * Errors: NOT_INITIALIZED, NOT_REGISTERED (no registration starts at ptr). */
 taccl_result_t taccl_unregister_buffer(const void* ptr);
 
+/* ---- symmetric multicast pool (NVLink SHARP) ------------------------------------------ */
+
+/* B200 extension (reading N1, §5 "pool"): the NVSwitch can reduce in the switch —
+ * multimem.ld_reduce returns the sum of every GPU's copy of an address, multimem.st writes all
+ * copies — which needs memory bound to a multicast object. The pool is that memory: one
+ * cuMemCreate allocation of the same size per rank, every peer's mapped here (so ordinary
+ * schedules reach pool buffers too), and one multicast object bound over all of them.
+ * Collective, in three phases with a host exchange between them (the Python binding's
+ * Comm.create_pool drives them over torch.distributed):
+ *   1. taccl_pool_export(bytes): allocate, and for rank 0 create the multicast object; writes a
+ *      TACCL_HANDLE_BYTES blob naming this rank's descriptor socket.
+ *   2. taccl_pool_connect(all blobs, rank order): exchange the allocation/multicast handles as
+ *      POSIX file descriptors over Unix domain sockets, map every peer, add this device to the
+ *      multicast object.
+ *   3. (after every rank finished phase 2) taccl_pool_bind: bind this rank's memory to the
+ *      multicast object, map it, clear the barrier flags; *base / *bytes = the allocatable
+ *      range. Every rank must then pass a host barrier before any collective uses the pool.
+ * taccl_pool_alloc: symmetric bump allocation (call in the same order with the same sizes on
+ * every rank; 4 KiB aligned). A taccl_run whose sendbuf and recvbuf both lie in the pool may
+ * select multicast-reduce algorithms (EF step `mr`); other calls skip them.
+ * Errors: NOT_INITIALIZED (no multi-process communicator / wrong phase order), UNSUPPORTED (no
+ * multicast support), CUDA (driver calls, descriptor exchange), INVALID_ARG (pool exhausted).
+ * The pool lives until taccl_comm_destroy. */
+taccl_result_t taccl_pool_export(size_t bytes, void* blob, size_t* len);
+taccl_result_t taccl_pool_connect(const void* all_blobs, size_t len_each);
+taccl_result_t taccl_pool_bind(void** base, size_t* bytes);
+taccl_result_t taccl_pool_alloc(size_t bytes, void** ptr);
+
 /* ---- north-star calls ------------------------------------------------------------------ */
 
 /* taccl_load_algo: the paper's lowered TACCL-EF program (§6.1: buffers,

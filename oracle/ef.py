@@ -25,7 +25,7 @@ class ScheduleError(Exception):
 
 
 COLLS = ("allgather", "alltoall", "allreduce", "reducescatter")
-STEP_TYPES = ("s", "r", "rrc", "cpy", "nop")
+STEP_TYPES = ("s", "r", "rrc", "cpy", "nop", "mr")
 BUFS = ("i", "o", "s")
 
 
@@ -187,10 +187,10 @@ def parse(text: str) -> Program:
                 if typ not in STEP_TYPES:
                     raise ScheduleError("syntax", f"rank {r} tb {t} step {k}: type={typ!r}")
                 step = Step(sid, typ, deps=_deps(st.get("deps", "")))
-                if typ in ("s", "rrc", "cpy"):
+                if typ in ("s", "rrc", "cpy", "mr"):
                     step.srcbuf = _buf(st, "srcbuf")
                     step.srcoff = _int(st, "srcoff", 0)
-                if typ in ("r", "rrc", "cpy"):
+                if typ in ("r", "rrc", "cpy", "mr"):
                     step.dstbuf = _buf(st, "dstbuf")
                     step.dstoff = _int(st, "dstoff", 0)
                 if typ != "nop":

@@ -37,11 +37,17 @@ def _steps(prog: Program, graph, order):
         yield v, r, tb, tb.steps[k]
 
 
-def _execute(prog: Program, graph, order, bufs, read, write, reduce):
+def _execute(prog: Program, graph, order, bufs, read, write, reduce, mreduce=None):
     """Shared engine. bufs[r][buf] is a rank's buffer; read/write move cnt chunks."""
     queues = {key: deque() for key in graph.conns}
     for v, r, tb, st in _steps(prog, graph, order):
         where = (r, tb.id, st.s)
+        if st.type == "mr":  # multicast reduce: sum over every rank's src, to every rank's dst
+            vals = [read(bufs[q][st.srcbuf], st.srcoff, st.cnt, where) for q in range(prog.nranks)]
+            out = mreduce(vals, where)
+            for q in range(prog.nranks):
+                write(bufs[q][st.dstbuf], st.dstoff, st.cnt, out)
+            continue
         if st.type == "cpy":
             write(bufs[r][st.dstbuf], st.dstoff, st.cnt, read(bufs[r][st.srcbuf], st.srcoff, st.cnt, where))
         elif st.type == "s":
@@ -104,7 +110,13 @@ def run_symbolic(prog: Program, graph=None, order=None, check=True):
             out.append((a[0], tuple(x + y for x, y in zip(a[1], b[1]))))
         return out
 
-    _execute(prog, graph, order, bufs, read, write, reduce)
+    def mreduce(vals, where):
+        out = vals[0]
+        for x in vals[1:]:
+            out = reduce(out, x, where)
+        return out
+
+    _execute(prog, graph, order, bufs, read, write, reduce, mreduce)
     outs = [b["o"] for b in bufs]
     if check:
         post = postcondition(prog.coll, n, p)
@@ -247,5 +259,30 @@ def run(prog: Program, inputs, dtype: str, graph=None, order=None, bf16: str = "
             acc = (a + b).astype(np.float32)  # one IEEE binary32 add, RNE
         return _Reduced(bf16_round(acc), acc)
 
-    _execute(prog, graph, order, bufs, read, write, reduce)
+    def mreduce(vals, where):
+        """mr (reading N1): the switch sums every rank's bits in one reduction —
+        int32 wraps, float32 adds (rank order), bfloat16 accumulates in fp32 (rank order) and
+        rounds once (multimem.ld_reduce .acc::f32). Partials are not visible to the switch:
+        it reads and writes bf16 bits only."""
+        bits = [x.bits if partials else x for x in vals]
+        if dtype == "int32":
+            acc = np.zeros(bits[0].size, np.uint32)
+            for x in bits:
+                acc = acc + x.view(np.uint32)
+            res = acc.view(np.int32)
+        elif dtype == "float32":
+            acc = bits[0].astype(np.float32).copy()
+            with np.errstate(over="ignore", invalid="ignore"):
+                for x in bits[1:]:
+                    acc = (acc + x).astype(np.float32)
+            res = acc
+        else:
+            acc = bf16_to_f32(bits[0]).copy()
+            with np.errstate(over="ignore", invalid="ignore"):
+                for x in bits[1:]:
+                    acc = (acc + bf16_to_f32(x)).astype(np.float32)
+            res = bf16_round(acc)
+        return _Val(res, None) if partials else res
+
+    _execute(prog, graph, order, bufs, read, write, reduce, mreduce)
     return [b["o"] for b in bufs]

@@ -7,6 +7,11 @@ Each check restates a rule of the paper or a reading listed in DESIGN.md:
   (NCCL const sendbuff); readings G1, G2.
 * match — reading G1: the k-th send on connection (A->B, chan) pairs with the k-th
   receive on B ("split into two instructions for the sender and receiver").
+* mr (multicast reduce, the NVLink SHARP step; docs/SCHEDULE.md, reading N1): the
+  k-th `mr` of every rank forms group k; member r reduces src[x_r..] over EVERY rank and writes
+  the sum to dst[y_r..] of EVERY rank. Every step before any member happens before every
+  member, and every member before any step after one (a barrier); its accesses are checked on
+  every rank's buffers.
 * cycle — steps in a threadblock run sequentially and wait on their dependencies
   (PAPER.md:746–752); a cycle in that relation is a deadlock.
 * race — conflicting accesses must be ordered ("dependencies for each
@@ -40,6 +45,7 @@ class Graph:
     match: dict            # recv node id -> send node id
     send_to_recv: dict     # send node id -> recv node id
     conns: dict            # (A, B, chan) -> list of (send id, recv id)
+    groups: list = field(default_factory=list)  # mr group k -> member node ids (rank order)
 
 
 # ------------------------------------------------------------------------------ structure
@@ -84,6 +90,10 @@ def check_structure(prog: Program):
                     errs.append(f"{where}: receive in a tb with no recv peer (V2)")
                 if st.type != "nop" and st.cnt < 1:
                     errs.append(f"{where}: cnt must be >= 1")
+                if st.type == "mr" and (tb.send != -1 or tb.recv != -1):
+                    errs.append(f"{where}: multicast reduce in a tb with a peer (its peer is the switch)")
+                if st.type == "mr" and prog.coll not in ("allreduce", "reducescatter"):
+                    errs.append(f"{where}: multicast reduce in a non-reducing collective")
                 if st.dstbuf == "i":
                     errs.append(f"{where}: writes the input buffer (read-only)")
                 for buf, off in ((st.srcbuf, st.srcoff), (st.dstbuf, st.dstoff)):
@@ -146,7 +156,32 @@ def build_graph(prog: Program) -> Graph:
             send_to_recv[si] = ri
             pairs.append((si, ri))
         conns[key] = pairs
-    return Graph(nodes, index, succ, match, send_to_recv, conns)
+    # multicast reduce groups: the k-th mr step of every rank (in tb, step order)
+    mrs = [[index[(g.id, tb.id, st.s)] for tb in g.tbs for st in tb.steps if st.type == "mr"] for g in prog.gpus]
+    groups = []
+    if any(mrs):
+        if len({len(m) for m in mrs}) != 1:
+            raise ScheduleError("match", "multicast reduce: ranks have " + "/".join(str(len(m)) for m in mrs)
+                                + " mr steps")
+        pred = {v: [] for v in range(len(nodes))}
+        for u, vs in enumerate(succ):
+            for v in vs:
+                pred[v].append(u)
+        out = [list(vs) for vs in succ]
+        for k in range(len(mrs[0])):
+            members = [m[k] for m in mrs]
+            cnts = {prog.gpus[nodes[v][0]].tbs[nodes[v][1]].steps[nodes[v][2]].cnt for v in members}
+            if len(cnts) != 1:
+                raise ScheduleError("match", f"multicast reduce group {k}: cnt differs across ranks")
+            for q in members:  # a barrier: preds of any member -> every member -> succs of any
+                for r in members:
+                    if r != q:
+                        succ[r].extend(x for x in out[q] if x not in members)
+                        for x in pred[q]:
+                            if x not in members:
+                                succ[x].append(r)
+            groups.append(members)
+    return Graph(nodes, index, succ, match, send_to_recv, conns, groups)
 
 
 def topo_order(graph: Graph):
@@ -208,6 +243,11 @@ def _accesses(prog: Program, graph: Graph, mode: str):
         for tb in g.tbs:
             for st in tb.steps:
                 v = graph.index[(g.id, tb.id, st.s)]
+                if st.type == "mr":  # reads and writes the same ranges on every rank
+                    for q in range(prog.nranks):
+                        acc.append((q, st.srcbuf, st.srcoff, st.srcoff + st.cnt, False, v, v, v))
+                        acc.append((q, st.dstbuf, st.dstoff, st.dstoff + st.cnt, True, v, v, v))
+                    continue
                 if st.srcbuf is not None:
                     acc.append((g.id, st.srcbuf, st.srcoff, st.srcoff + st.cnt, False, v, v, v))
                 if st.dstbuf is not None:

@@ -10,7 +10,7 @@ LIB = os.path.join(HERE, "libtaccl.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["ef_parse.cpp", "check.cpp", "plan.cpp", "runtime.cpp", "executor.cu"]
+SOURCES = ["ef_parse.cpp", "check.cpp", "plan.cpp", "pool.cpp", "runtime.cpp", "executor.cu"]
 
 
 def _stale():

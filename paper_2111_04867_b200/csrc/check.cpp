@@ -53,6 +53,10 @@ void check_structure(const Program& P) {
         if (st.type == ST_S && tb.send == -1) fail("structure", w + ": send in a tb with no send peer (V2)");
         if ((st.type == ST_R || st.type == ST_RRC) && tb.recv == -1) fail("structure", w + ": receive in a tb with no recv peer (V2)");
         if (st.type != ST_NOP && st.cnt < 1) fail("structure", w + ": cnt < 1");
+        if (st.type == ST_MR && (tb.send != -1 || tb.recv != -1))
+          fail("structure", w + ": multicast reduce in a tb with a peer (its peer is the switch)");
+        if (st.type == ST_MR && P.coll != C_AR && P.coll != C_RS)
+          fail("structure", w + ": multicast reduce in a non-reducing collective");
         if (st.dstbuf == B_I) fail("structure", w + ": writes the input buffer (read-only)");
         if (st.srcbuf != B_NONE && (long long)st.srcoff + st.cnt > g.nchunks(st.srcbuf))
           fail("structure", w + ": source range exceeds buffer (V4)");
@@ -73,6 +77,7 @@ struct Graph {
   std::map<std::tuple<int, int, int>, int> id;
   std::vector<std::vector<int>> succ;
   std::vector<int> match;                         // recv node -> send node, else -1
+  std::vector<std::vector<int>> groups;           // mr group k -> member nodes (rank order)
   std::map<std::tuple<int, int, int>, std::vector<std::pair<int, int>>> conns;  // (A,B,c)->(send,recv)
 };
 
@@ -115,6 +120,42 @@ Graph build(const Program& P) {
       G.succ[ss[q]].push_back(rr[q]);
       G.match[rr[q]] = ss[q];
       pairs.emplace_back(ss[q], rr[q]);
+    }
+  }
+  // multicast reduce groups: the k-th mr step of every rank (tb, step order) is a barrier —
+  // every predecessor of a member precedes every member, every member precedes every successor
+  std::vector<std::vector<int>> mrs(P.nranks);
+  bool any = false;
+  for (const Gpu& g : P.gpus)
+    for (const TB& tb : g.tbs)
+      for (const Step& st : tb.steps)
+        if (st.type == ST_MR) {
+          mrs[g.id].push_back(G.id[{g.id, tb.id, st.s}]);
+          any = true;
+        }
+  if (any) {
+    for (int r = 1; r < P.nranks; ++r)
+      if (mrs[r].size() != mrs[0].size()) fail("match", "multicast reduce: ranks have different numbers of mr steps");
+    const int N = (int)G.nodes.size();
+    std::vector<std::vector<int>> pred(N), out = G.succ;
+    for (int u = 0; u < N; ++u)
+      for (int v : G.succ[u]) pred[v].push_back(u);
+    for (size_t k = 0; k < mrs[0].size(); ++k) {
+      std::vector<int> mem;
+      for (int r = 0; r < P.nranks; ++r) mem.push_back(mrs[r][k]);
+      auto cnt_of = [&](int v) { auto [r, t, s] = G.nodes[v]; return P.gpus[r].tbs[t].steps[s].cnt; };
+      for (int v : mem)
+        if (cnt_of(v) != cnt_of(mem[0])) fail("match", "multicast reduce group " + std::to_string(k) + ": cnt differs across ranks");
+      auto member = [&](int x) { return std::find(mem.begin(), mem.end(), x) != mem.end(); };
+      for (int q : mem)
+        for (int r : mem) {
+          if (r == q) continue;
+          for (int x : out[q])
+            if (!member(x)) G.succ[r].push_back(x);
+          for (int x : pred[q])
+            if (!member(x)) G.succ[x].push_back(r);
+        }
+      G.groups.push_back(mem);
     }
   }
   return G;
@@ -206,6 +247,13 @@ void check_races(const Program& P, const Graph& G, const Reach& R, bool direct) 
     for (const TB& tb : g.tbs)
       for (const Step& st : tb.steps) {
         int v = G.id.at({g.id, tb.id, st.s});
+        if (st.type == ST_MR) {  // reads and writes the same ranges on every rank
+          for (int q = 0; q < P.nranks; ++q) {
+            by[{q, st.srcbuf}].push_back({st.srcoff, st.srcoff + st.cnt, false, v, v, v});
+            by[{q, st.dstbuf}].push_back({st.dstoff, st.dstoff + st.cnt, true, v, v, v});
+          }
+          continue;
+        }
         if (st.srcbuf != B_NONE) by[{g.id, st.srcbuf}].push_back({st.srcoff, st.srcoff + st.cnt, false, v, v, v});
         if (st.dstbuf != B_NONE) {
           int start = (st.type == ST_R && direct) ? G.match[v] : v;
@@ -219,9 +267,11 @@ void check_races(const Program& P, const Graph& G, const Reach& R, bool direct) 
         if (a.node == b.node || !(a.write || b.write)) continue;
         if (a.hi <= b.lo || b.hi <= a.lo) continue;
         if (R.has(a.end, b.start) || R.has(b.end, a.start)) continue;
-        auto [r, ta, ka] = G.nodes[a.node];
-        auto [r2, tb_, kb] = G.nodes[b.node];
-        (void)r2;
+        auto [ra, ta, ka] = G.nodes[a.node];
+        auto [rb, tb_, kb] = G.nodes[b.node];
+        (void)ra;
+        (void)rb;
+        const int r = key.first;
         fail("race", "rank " + std::to_string(r) + " " + bufname((BufId)key.second) + "[" +
                          std::to_string(std::max(a.lo, b.lo)) + ":" + std::to_string(std::min(a.hi, b.hi)) +
                          "]: steps tb" + std::to_string(ta) + ":s" + std::to_string(ka) + " and tb" +
@@ -296,6 +346,31 @@ void symbolic(const Program& P, const Graph& G, const std::vector<int>& order) {
           for (int s = 0; s < n; ++s) mine[i].contrib[s] += got[i].contrib[s];
         }
         wr(st.dstbuf, st.dstoff, mine);
+        break;
+      }
+      case ST_MR: {  // sum of every rank's src tokens, written to every rank's dst
+        auto rdq = [&](int q) {
+          std::vector<Tok> out;
+          for (int i = 0; i < st.cnt; ++i) {
+            const Tok& x = B[st.srcbuf][q][st.srcoff + i];
+            if (x.chunk < 0) fail("uninit", where(r, t, k) + " reads rank " + std::to_string(q) + " chunk " +
+                                                std::to_string(st.srcoff + i) + " before any write");
+            out.push_back(x);
+          }
+          return out;
+        };
+        std::vector<Tok> acc = rdq(0);
+        for (int q = 1; q < n; ++q) {
+          std::vector<Tok> got = rdq(q);
+          for (int i = 0; i < st.cnt; ++i) {
+            if (acc[i].chunk != got[i].chunk)
+              fail("postcondition", where(r, t, k) + " reduces chunk " + std::to_string(acc[i].chunk) + " with chunk " +
+                                        std::to_string(got[i].chunk));
+            for (int s2 = 0; s2 < n; ++s2) acc[i].contrib[s2] += got[i].contrib[s2];
+          }
+        }
+        for (int q = 0; q < n; ++q)
+          for (int i = 0; i < st.cnt; ++i) B[st.dstbuf][q][st.dstoff + i] = acc[i];
         break;
       }
       case ST_NOP: break;

@@ -258,12 +258,13 @@ Program parse_ef(const char* text, size_t len) {
             else if (ty == "rrc") st.type = ST_RRC;
             else if (ty == "cpy") st.type = ST_CPY;
             else if (ty == "nop") st.type = ST_NOP;
+            else if (ty == "mr") st.type = ST_MR;
             else fail(where + " step " + std::to_string(st.s) + ": type=\"" + ty + "\"");
-            if (st.type == ST_S || st.type == ST_RRC || st.type == ST_CPY) {
+            if (st.type == ST_S || st.type == ST_RRC || st.type == ST_CPY || st.type == ST_MR) {
               st.srcbuf = to_buf(t, "srcbuf");
               st.srcoff = (int)to_int(t, "srcoff", 0);
             }
-            if (st.type == ST_R || st.type == ST_RRC || st.type == ST_CPY) {
+            if (st.type == ST_R || st.type == ST_RRC || st.type == ST_CPY || st.type == ST_MR) {
               st.dstbuf = to_buf(t, "dstbuf");
               st.dstoff = (int)to_int(t, "dstoff", 0);
             }

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include "pool.h"
 #include "taccl_internal.h"
 
 namespace taccl {
@@ -404,6 +405,69 @@ __device__ __noinline__ void cta_reduce_px(char* dst, char* dst32, char* const* 
       else E::store(fwd[f] + off + 2 * e, acc);
     }
   }
+}
+
+// ---------------------------------------------------------------- multicast reduce (NVLink SHARP)
+// dst = sum over every rank of src, at multicast addresses (reading N1): multimem.ld_reduce
+// makes the NVSwitch load the n copies and add them (bf16: fp32 accumulation, one RNE;
+// int32: wrapping u32 adds, scalar — the switch has no integer vector form), multimem.st
+// writes the result to every rank's copy. 16-byte aligned ranges, whole vectors (the runtime
+// selects multicast-reduce algorithms only for 16-byte chunks). U loads in flight per thread.
+__device__ __forceinline__ uint4 mm_ld_reduce(const char* p, int dtype) {
+  uint4 v;
+  if (dtype == TACCL_BFLOAT16) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  } else if (dtype == TACCL_FLOAT32) {
+    float a, b, c, d;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(p) : "memory");
+    v = make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d));
+  } else {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.x) : "l"(p) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.y) : "l"(p + 4) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.z) : "l"(p + 8) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.w) : "l"(p + 12) : "memory");
+  }
+  return v;
+}
+__device__ __forceinline__ void mm_st(char* p, uint4 v) {  // 16 bytes to every rank's copy
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w)) : "memory");
+}
+__device__ __noinline__ void cta_mr(char* mdst, const char* msrc, int64_t nbytes, int dtype) {
+  constexpr int U = 4;
+  const int64_t nv = nbytes >> 4, nt = blockDim.x;
+  int64_t i = threadIdx.x;
+  for (; i + (U - 1) * nt < nv; i += U * nt) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = mm_ld_reduce(msrc + 16 * (i + u * nt), dtype);
+#pragma unroll
+    for (int u = 0; u < U; ++u) mm_st(mdst + 16 * (i + u * nt), v[u]);
+  }
+  for (; i < nv; i += nt) mm_st(mdst + 16 * i, mm_ld_reduce(msrc + 16 * i, dtype));
+}
+// the multicast-reduce barrier: publish this rank's arrival for (phase, group, piece) to every
+// rank's copy (one multimem.st with release semantics), then wait for every rank's word.
+// Returns false on timeout. Thread 0 only.
+__device__ bool mr_barrier(const KRank& R, int nranks, int phase, int group, int piece, unsigned epoch, u64 timeout_ns) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  unsigned* mc = reinterpret_cast<unsigned*>(R.nv_mc) + mr_flag(phase, group, piece, R.rank);
+  asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(mc), "r"(epoch) : "memory");
+  for (int q = 0; q < nranks; ++q) {
+    const unsigned* w = R.nv_uc + mr_flag(phase, group, piece, q);
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+    if ((int)(v - epoch) >= 0) continue;
+    const u64 t0 = globaltimer();
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+      if ((int)(v - epoch) >= 0) break;
+      if (globaltimer() - t0 > timeout_ns) return false;
+    }
+  }
+  return true;
 }
 
 // ---------------------------------------------------------------- TMA bulk-copy pipeline
@@ -1154,6 +1218,8 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
                           : remote_base(c, fw[0], fw[2]) + (int64_t)fw[3] * cbytes;
           }
         }
+        if (ok && st.op == K_MR && !LL)  // every rank's piece j of this group arrived
+          ok = mr_barrier(R, A.nranks, 0, st.seq, j, (unsigned)c.epoch, A.timeout_ns);
         if (!ok) {
           record_error(c, what, k);
           s_abort = 1;
@@ -1232,6 +1298,19 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         }
         case K_RECV:  // zero-copy: the bytes are already in place
           break;
+        case K_MR: {  // multicast reduce of this piece, then every rank's piece j must be written
+          const char* src = R.mc_in + (int64_t)st.srcoff * cbytes;  // (src/dst: i and o only)
+          char* dst = R.mc_out + (int64_t)st.dstoff * cbytes;
+          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_mr(dst + off, src + off, len, A.dtype); });
+          __syncthreads();
+          if (tid == 0 && !mr_barrier(R, A.nranks, 1, st.seq, j, (unsigned)c.epoch, A.timeout_ns)) {
+            record_error(c, st.op, k);
+            s_abort = 1;
+          }
+          __syncthreads();
+          if (s_abort) return;
+          break;
+        }
         case K_RCS: {  // the bytes landed in dst (zero-copy); push them on to the send's peer
           const char* src = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           char* dst = s_fwd[0];

@@ -232,12 +232,17 @@ std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map
   std::map<std::tuple<int, int, int>, int> fl;
   for (const Gpu& g : P.gpus) {
     const int r = g.id;
-    struct W { int t, k; StepType type; BufId buf; int off, cnt; };
+    struct W { int r, t, k; StepType type; BufId buf; int off, cnt; };
     std::vector<W> writers;
     for (const TB& tb : g.tbs)
       for (const Step& st : tb.steps)
         if ((st.type == ST_R || st.type == ST_RRC || st.type == ST_CPY) && (st.dstbuf == B_O || st.dstbuf == B_S))
-          writers.push_back({tb.id, st.s, st.type, st.dstbuf, st.dstoff, st.cnt});
+          writers.push_back({r, tb.id, st.s, st.type, st.dstbuf, st.dstoff, st.cnt});
+    for (const Gpu& g2 : P.gpus)  // a multicast reduce writes every rank's destination (bits only)
+      for (const TB& tb : g2.tbs)
+        for (const Step& st : tb.steps)
+          if (st.type == ST_MR && (st.dstbuf == B_O || st.dstbuf == B_S))
+            writers.push_back({g2.id, tb.id, st.s, st.type, st.dstbuf, st.dstoff, st.cnt});
     // the rrcs that are last writers of the range (empty if some chunk's last writer is not one)
     auto partial_range = [&](int t, int k, BufId buf, int off, int cnt, std::vector<int>* lw) {
       lw->clear();
@@ -246,8 +251,8 @@ std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map
         int best = -1;
         for (int w = 0; w < (int)writers.size(); ++w) {
           const W& x = writers[w];
-          if (x.buf != buf || c < x.off || c >= x.off + x.cnt || !hb.before(r, x.t, x.k, r, t, k)) continue;
-          if (best < 0 || hb.before(r, writers[best].t, writers[best].k, r, x.t, x.k)) best = w;
+          if (x.buf != buf || c < x.off || c >= x.off + x.cnt || !hb.before(x.r, x.t, x.k, r, t, k)) continue;
+          if (best < 0 || hb.before(writers[best].r, writers[best].t, writers[best].k, x.r, x.t, x.k)) best = w;
         }
         if (best < 0 || writers[best].type != ST_RRC) return false;
         lw->push_back(best);
@@ -272,9 +277,9 @@ std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map
           }
         }
       }
-    for (auto [w, rd] : keep) {
-      fl[{r, writers[w].t, writers[w].k}] |= P_KEEP;
-      (*readers)[{r, writers[w].t, writers[w].k}].insert(rd);
+    for (auto [w, rd] : keep) {  // (only rrcs qualify as last writers here: same rank)
+      fl[{writers[w].r, writers[w].t, writers[w].k}] |= P_KEEP;
+      (*readers)[{writers[w].r, writers[w].t, writers[w].k}].insert(rd);
     }
   }
   return fl;
@@ -344,6 +349,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
     rp.stage2_chunks = stage2_total[g.id];
     rp.scratch_chunks = g.s_chunks;
     std::map<std::pair<int, int>, int> flat;  // (tb, step) -> index in rp.steps
+    int mr_group = 0;                         // k-th multicast reduce of this rank = group k
     std::vector<std::vector<std::pair<int, int>>> deps, post;  // per flat step
     for (const TB& tb : g.tbs) {
       KTB kt{tb.send, tb.recv, tb.chan, (int32_t)rp.steps.size(), (int32_t)tb.steps.size()};
@@ -402,6 +408,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
             break;
           }
           case ST_CPY: ks.op = K_CPY; break;
+          case ST_MR: ks.op = K_MR; ks.seq = mr_group++; break;  // group index (barrier slots)
           default: ks.op = K_NOP; break;
         }
         flat[{tb.id, st.s}] = (int)rp.steps.size();
@@ -559,7 +566,9 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
       bool indep = kt.send < 0 && kt.recv < 0;
       for (int i = 0; i < kt.nsteps && indep; ++i) {
         const KStep& ks = rp.steps[kt.step_begin + i];
-        indep = ks.dep_count == 0 && ks.post_count == 0 && !ks.need_done;
+        // a multicast reduce's piece j meets piece j of every rank at its barriers: it keeps
+        // the launch-wide split (identical on all ranks)
+        indep = ks.dep_count == 0 && ks.post_count == 0 && !ks.need_done && ks.op != K_MR;
       }
       kt.indep = indep;
     }

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "plan.h"
+#include "pool.h"
 #include "taccl_internal.h"
 
 using namespace taccl;
@@ -68,6 +69,7 @@ struct Algo {
   std::vector<int> wsum;        // per rank
   int fused_chains = 0;
   bool has_pull = false;  // some send of the direct plan is read in place (pull mode applies)
+  bool has_mr = false;    // multicast reduce steps: needs the symmetric pool (NVLink SHARP)
   bool shadow = false;  // bf16 partials read/write the fp32 shadow (bf16 calls need its region)
   int max_o_chunks = 0, max_s_chunks = 0;
 };
@@ -95,6 +97,7 @@ struct Comm {
   // host-run pipeline (taccl_run_host): copy streams and events, created on first use
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_in[2] = {}, ev_k[2] = {}, ev_out[2] = {};
+  Pool pool;  // symmetric multicast pool (taccl_pool_*), for multicast-reduce algorithms
 };
 
 Comm g;
@@ -181,9 +184,12 @@ uint64_t select_bytes(taccl_coll_t coll, size_t count, int elt, int n) {
   return (uint64_t)n * count * elt;
 }
 
-Algo* select_algo(taccl_coll_t coll, uint64_t S, taccl_dtype_t dtype) {
+// mr_ok: the call may run multicast-reduce algorithms (both buffers in the symmetric pool,
+// 16-byte aligned chunks); others are skipped so an ordinary algorithm for the range runs
+Algo* select_algo(taccl_coll_t coll, uint64_t S, taccl_dtype_t dtype, bool mr_ok = false) {
   for (auto it = g.algos.rbegin(); it != g.algos.rend(); ++it) {  // latest load wins
     Algo* a = *it;
+    if (a->has_mr && !mr_ok) continue;
     if ((int)a->coll == (int)coll && a->nranks == g.nranks && S >= a->min_bytes && ((a->dtypes >> dtype) & 1) &&
         (a->max_bytes == UINT64_MAX || S < a->max_bytes))
       return a;
@@ -222,7 +228,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   // LL up to 2 MiB of output for AG/A2A/AR and 4 MiB for RS (measured crossovers vs the
   // direct kernel at n=2 and n=4, profiles/r01_ll_threshold.txt); TACCL_STAGED_MAX overrides
   const int64_t ll_max = (int64_t)env_size("TACCL_STAGED_MAX", coll == TACCL_REDUCESCATTER ? (4 << 20) : (2 << 20));
-  G->staged = (int64_t)a->max_stage2_chunks * ll_cb <= sb && total_bytes <= ll_max ? 1 : 0;
+  G->staged = (int64_t)a->max_stage2_chunks * ll_cb <= sb && total_bytes <= ll_max && !a->has_mr ? 1 : 0;
   // bytes per CTA: LL lines are latency-bound, so LL pieces are small (4 KiB of payload per
   // CTA measured best at n=2 up to 1 MiB, profiles/r01_small_sweep_n2.txt)
   const int64_t min_piece = G->staged ? (int64_t)env_size("TACCL_LL_MIN_PIECE", 4 << 10)
@@ -326,7 +332,7 @@ bool lean(const Algo* a, const Geometry& G) {
 taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int elt,
                       const std::vector<int>& ranks, const void* const* sends, void* const* recvs,
                       char* const (*peer_out)[kMaxRanks], void* stream,
-                      const char* const (*peer_in)[kMaxRanks] = nullptr) {
+                      const char* const (*peer_in)[kMaxRanks] = nullptr, bool mr = false) {
   if (lean(a, G)) {  // n = 1, one input -> output copy
     std::string err;
     const int64_t cb = G.chunk_bytes;
@@ -340,6 +346,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   KArgs A;
   memset(&A, 0, sizeof(A));
   A.nlocal = (int)ranks.size();
+  A.nranks = g.nranks;
   A.split = G.split;
   A.dep_ctas = G.dep_ctas;
   A.indep_cap = G.indep_cap;
@@ -375,6 +382,12 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
       R.peer_out[q] = peer_out[i][q];
       R.peer_arena[q] = g.peer_arena[q];
       R.peer_in[q] = peer_in ? peer_in[i][q] : nullptr;
+    }
+    if (mr) {  // multicast addresses of this call's buffers and the pool's barrier flags
+      R.mc_in = g.pool.mcva + ((const char*)sends[i] - g.pool.uc);
+      R.mc_out = g.pool.mcva + ((char*)recvs[i] - g.pool.uc);
+      R.nv_mc = g.pool.mcva;
+      R.nv_uc = (unsigned*)g.pool.uc;
     }
     R.rank = r;
     R.ntb = dp.ntb;
@@ -436,11 +449,23 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
   if (!sendbuf || !recvbuf) return fail(TACCL_ERR_INVALID_ARG, "null buffer");
   const size_t ib = in_bytes(coll, count, elt, n), ob = out_bytes(coll, count, elt, n);
   const bool overlapping = (const char*)sendbuf < (const char*)recvbuf + ob && (const char*)recvbuf < (const char*)sendbuf + ib;
-  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n), dtype);
+  // multicast-reduce algorithms need both buffers in the symmetric pool and whole 16-byte
+  // vectors per chunk; an exactly in-place call is fine for them (each rank's multicast reduce
+  // reads and writes only its own share, after every rank arrived)
+  auto in_pool = [&](const void* p, size_t b) {
+    return g.pool.up && (const char*)p >= g.pool.uc && (const char*)p + b <= g.pool.uc + g.pool.bytes;
+  };
+  const bool pooled = n > 1 && in_pool(sendbuf, ib) && in_pool(recvbuf, ob) && (!overlapping || sendbuf == recvbuf);
+  Algo* a = select_algo(coll, select_bytes(coll, count, elt, n), dtype, pooled);
+  if (a && a->has_mr) {  // chunk alignment decides too: fall back to an ordinary algorithm
+    Geometry G0;
+    if (geometry(a, coll, count, elt, 1, base_off, &G0) != TACCL_SUCCESS || G0.chunk_bytes % 16)
+      a = select_algo(coll, select_bytes(coll, count, elt, n), dtype, false);
+  }
   if (!a) return fail(TACCL_ERR_NO_ALGO, "no loaded algorithm for this collective, nranks and size");
   Geometry G;
   if ((rc = geometry(a, coll, count, elt, 1, base_off, &G))) return rc;
-  if (overlapping) {
+  if (overlapping && !a->has_mr) {
     // in-place / overlapping call (NCCL allows AG with sendbuf = recvbuf + rank*count and AR
     // with sendbuf = recvbuf; reading G10): the schedules read the input while peers write
     // the output, so the input is first copied (same stream, before the launch) to a private
@@ -487,7 +512,7 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
   std::vector<int> ranks{g.rank};
   const void* s[1] = {sendbuf};
   void* r[1] = {recvbuf};
-  return launch(a, G, dtype, elt, ranks, s, r, peer_out, stream, have_in ? peer_in : nullptr);
+  return launch(a, G, dtype, elt, ranks, s, r, peer_out, stream, have_in ? peer_in : nullptr, a->has_mr);
 }
 
 taccl_result_t upload(const RankPlan& rp, DevPlan* dp) {
@@ -561,7 +586,7 @@ taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, c
         ll ? build_plans(P, fuse, rrcs, env_size("TACCL_NO_CHAIN_SENDS_LL", 0) == 0)
            : build_plans(P, fuse, rrcs, env_size("TACCL_CHAIN_SENDS", 0) != 0, (int)env_size("TACCL_PULL_KINDS", 1));
     const RankPlan& rp = plans[rank];
-    static const char* ops[] = {"SEND", "RECV", "RRC", "CPY", "NOP", "RRC_FUSED", "RRCS", "SENT", "PUB", "RCS"};
+    static const char* ops[] = {"SEND", "RECV", "RRC", "CPY", "NOP", "RRC_FUSED", "RRCS", "SENT", "PUB", "RCS", "MR"};
     static const char* bufs[] = {"i", "o", "s", "stage"};
     auto pairs = [&](int b, int c) {
       std::string x;
@@ -672,6 +697,7 @@ taccl_result_t taccl_comm_destroy(void) {
     delete a;
   }
   for (auto& kv : g.ipc_open) cudaIpcCloseMemHandle(kv.second);
+  pool_destroy(g.pool);
   for (char* a : g.arenas) cudaFree(a);
   if (g.h2d) {
     cudaStreamDestroy(g.h2d);
@@ -743,6 +769,50 @@ taccl_result_t taccl_unregister_buffer(const void* ptr) {
   return TACCL_SUCCESS;
 }
 
+taccl_result_t taccl_pool_export(size_t bytes, void* out, size_t* len) {
+  if (!g.up || g.emulated || g.nranks < 2) return fail(TACCL_ERR_NOT_INITIALIZED, "no multi-process communicator");
+  if (g.pool.up || g.pool.phys) return fail(TACCL_ERR_INVALID_ARG, "pool already created");
+  if (!out || !len || !bytes) return fail(TACCL_ERR_INVALID_ARG, "bad arguments");
+  std::string err;
+  if (!pool_export(g.pool, g.rank, g.nranks, g.device, bytes + kPoolFlagBytes, out, len, &err)) {
+    pool_destroy(g.pool);
+    return fail(TACCL_ERR_UNSUPPORTED, "pool: " + err);
+  }
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_pool_connect(const void* all, size_t len_each) {
+  if (!g.up || !g.pool.phys) return fail(TACCL_ERR_NOT_INITIALIZED, "taccl_pool_export first");
+  std::string err;
+  if (!pool_connect(g.pool, all, len_each, &err)) return fail(TACCL_ERR_CUDA, "pool: " + err);
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_pool_bind(void** base, size_t* bytes) {
+  if (!g.up || !g.pool.uc) return fail(TACCL_ERR_NOT_INITIALIZED, "taccl_pool_connect first");
+  std::string err;
+  if (!pool_bind(g.pool, &err)) return fail(TACCL_ERR_CUDA, "pool: " + err);
+  // ordinary algorithms reach pool buffers through the peers' unicast mappings
+  Reg rg;
+  rg.lo = (uintptr_t)g.pool.uc;
+  rg.hi = rg.lo + g.pool.bytes;
+  for (int q = 0; q < g.nranks; ++q) rg.peer_base[q] = g.pool.peer[q];
+  g.regs.push_back(rg);
+  if (base) *base = g.pool.uc + kPoolFlagBytes;
+  if (bytes) *bytes = g.pool.bytes - kPoolFlagBytes;
+  return TACCL_SUCCESS;
+}
+
+taccl_result_t taccl_pool_alloc(size_t bytes, void** ptr) {
+  if (!g.up || !g.pool.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no symmetric pool (taccl_pool_bind)");
+  if (!ptr) return fail(TACCL_ERR_INVALID_ARG, "null pointer");
+  const size_t at = (g.pool.used + 4095) & ~(size_t)4095;
+  if (at + bytes > g.pool.bytes) return fail(TACCL_ERR_INVALID_ARG, "pool exhausted");
+  g.pool.used = at + bytes;
+  *ptr = g.pool.uc + at;
+  return TACCL_SUCCESS;
+}
+
 taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) {
   if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
   if (!text) return fail(TACCL_ERR_INVALID_ARG, "null text");
@@ -800,6 +870,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->max_o_chunks = std::max(a->max_o_chunks, P_o_chunks[r]);
     a->max_s_chunks = std::max(a->max_s_chunks, plans[r].scratch_chunks);
     a->fused_chains += plans[r].fused_chains;
+    for (const KStep& k : plans[r].steps) a->has_mr = a->has_mr || k.op == K_MR;
     for (const KStep& k : plans[r].steps) a->has_pull = a->has_pull || (k.op == K_SEND && k.poff >= 0);
     if (a->nranks == 1 && plans[r].steps.size() == 1) {
       const KStep& k = plans[r].steps[0];

@@ -12,7 +12,9 @@
 namespace taccl {
 
 // ---------------------------------------------------------------- parsed program (host)
-enum StepType : int8_t { ST_S = 0, ST_R = 1, ST_RRC = 2, ST_CPY = 3, ST_NOP = 4 };
+// ST_MR: multicast reduce (NVLink SHARP, reading N1): the k-th mr step of every rank
+// forms group k; member r sums src[x_r..] over every rank and writes it to dst[y_r..] of every rank
+enum StepType : int8_t { ST_S = 0, ST_R = 1, ST_RRC = 2, ST_CPY = 3, ST_NOP = 4, ST_MR = 5 };
 enum BufId : int8_t { B_NONE = -1, B_I = 0, B_O = 1, B_S = 2 };
 enum Coll : int8_t { C_AG = 0, C_A2A = 1, C_AR = 2, C_RS = 3 };
 
@@ -84,8 +86,10 @@ enum KOp : int8_t {
   K_SENT = 7,      // a send already performed (and published) by the preceding K_RRCS
   K_PUB = 8,       // a send whose bytes the fused chain it follows already stored (fuse_chain_sends):
                    // publish the data flag only
-  K_RCS = 9        // recv fused with the next step's send of what it received (recv-copy-send,
+  K_RCS = 9,       // recv fused with the next step's send of what it received (recv-copy-send,
                    // relays): LL: one pass over the lines; direct: wait, then push dst onward
+  K_MR = 10        // multicast reduce (group seq): barrier, multimem.ld_reduce of src over every
+                   // rank + multimem.st to every rank's dst (its pieces), barrier; direct kernel
 };
 enum KBuf : int8_t { KB_I = 0, KB_O = 1, KB_S = 2, KB_STAGE = 3 };
 
@@ -182,6 +186,10 @@ struct KRank {
   char* peer_out[kMaxRanks];    // peer's output buffer (this call's recvbuf on the peer)
   char* peer_arena[kMaxRanks];  // peer's arena (flags, scratch, staging)
   const char* peer_in[kMaxRanks];  // pull mode: peer's input buffer (this call's sendbuf on the peer)
+  char* mc_in;             // multicast reduce: this call's sendbuf / recvbuf at their multicast
+  char* mc_out;            // addresses (symmetric pool), else null
+  char* nv_mc;             // the pool's barrier flags: multicast address ...
+  unsigned* nv_uc;         // ... and this rank's local copy
   int32_t rank, ntb, ncta;  // ncta: CTAs of this rank in the launch
   int32_t budget;          // CTAs of this rank: tb t gets tb_ctas(weight_t, wsum, ...)
   int32_t wsum, pad;
@@ -190,6 +198,7 @@ struct KRank {
 struct KArgs {
   KRank r[kMaxRanks];
   int32_t nlocal;          // local ranks in this launch
+  int32_t nranks;          // ranks of the communicator (multicast-reduce barriers)
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
   int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT); timing probes
                            // only, results invalid: 9 = no fence before data flags, 20 = LL

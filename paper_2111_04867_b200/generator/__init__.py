@@ -12,6 +12,8 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
     pair=False lowers sends and receives into separate threadblocks; pair="peer" pairs only by
     peer (no relay-first threadblocks, lowering.py); merge=False keeps every transfer its own
     step (no contiguity coalescing, lowering.coalesce)."""
+    if algo == "nvls":  # multicast reduce through the switch: written directly (templates.nvls_text)
+        return templates.nvls_text(coll, nranks, chunks, instances, min_bytes, max_bytes, dtypes)
     if algo == "hier":
         if nranks % 2:
             raise ValueError("hier needs 2 x k ranks")

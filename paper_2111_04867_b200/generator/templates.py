@@ -153,6 +153,29 @@ def direct_allreduce(n, p=1):
                      f"ar_direct_n{n}_p{p}")
 
 
+def nvls_text(coll, n, p=1, instances=1, min_bytes=0, max_bytes=float("inf"), dtypes=None):
+    """EF v1 text of the Allreduce through the switch (NVLink SHARP; reading N1):
+    rank r, one threadblock (its peer is the switch), ONE multicast-reduce step (`mr`) over its
+    own p chunks r*p .. r*p+p-1 — multimem.ld_reduce sums the n copies in the NVSwitch,
+    multimem.st writes the result to every rank. Per GPU the links carry ~S out and ~S in
+    (1/n of it as the reduced result) instead of RS ++ AG's 2(n-1)/n S each way (PAPER.md:
+    720-728). There are no point-to-point transfers, so nothing is lowered."""
+    if coll != "allreduce":
+        raise ValueError("nvls: allreduce only")
+    mx = "inf" if max_bytes == float("inf") else str(int(max_bytes))
+    out = [f'<algo name="ar_nvls_n{n}_p{p}_m{instances}" coll="allreduce" nranks="{n}" chunks_per_rank="{p}" '
+           f'instances="{instances}" minBytes="{int(min_bytes)}" maxBytes="{mx}" inplace="0"'
+           + (f' dtypes="{",".join(dtypes)}"' if dtypes else "") + '>']
+    for r in range(n):
+        out.append(f' <gpu id="{r}" i_chunks="{n * p}" o_chunks="{n * p}" s_chunks="0">')
+        out.append('  <tb id="0" send="-1" recv="-1" chan="0">')
+        out.append(f'   <step s="0" type="mr" srcbuf="i" srcoff="{r * p}" dstbuf="o" dstoff="{r * p}" cnt="{p}" deps=""/>')
+        out.append('  </tb>')
+        out.append(' </gpu>')
+    out.append('</algo>')
+    return "\n".join(out) + "\n"
+
+
 # ------------------------------------------------------------------------------ registry
 
 TEMPLATES = {

@@ -40,22 +40,40 @@ def ranges(coll: str, n: int):
         # carries fp32 partials on its n-2 middle hops (reading R6; 2x those bytes), so direct
         # stays ahead at every size (profiles/r02_sweep_ar_ring_ab_n4.txt: 128 MiB 366 vs 463
         # us, 512 MiB 1356 vs 1723). int32/fp32 partials are the values themselves: there the
-        # ring is ahead at 128-256 MiB (round 1: 342-344 vs 365 us) and 2 chunks per rank
-        # pipeline its 2(n-1) hops best from 512 MiB (profiles/r01_ar_variants_n4.txt)
+        # relay-first ring (one recv-reduce-copy-send pass per hop) is ahead from 128 MiB
+        # (profiles/r02_sweep_n4_fp32_ar.txt: 128 MiB 329 vs 350 us, 1 GiB 2436 vs 2676; ring_p2
+        # 2493)
         return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("direct", 128 * MiB, INF, BF16),
-                ("ring", 128 * MiB, 512 * MiB, WIDE), ("ring_p2", 512 * MiB, INF, WIDE)]
+                ("ring", 128 * MiB, INF, WIDE)]
     if coll == "reducescatter":
         if n == 2 or n >= 8:
             return [("direct", 0, INF)]
-        return [("direct", 0, 32 * MiB), ("ring", 32 * MiB, INF)]
+        # bf16 rings carry fp32 partials on n-2 of n-1 hops (reading R6): 0.58-0.72x NCCL at
+        # 32 MiB-1 GiB (profiles/r02_sweep_n4_graph.txt), so bf16 stays direct; int32/fp32 keep
+        # round 1's ring from 32 MiB
+        return [("direct", 0, 32 * MiB), ("direct", 32 * MiB, INF, BF16), ("ring", 32 * MiB, INF, WIDE)]
     raise ValueError(coll)
 
 
-def default_schedules(coll: str, n: int):
-    """EF texts of the default set for (coll, n), each carrying its size range."""
+def multicast_ranges(coll: str, n: int):
+    """Multicast-reduce (NVLink SHARP) entries, loaded after the partition so they win their
+    range whenever a call can run them (both buffers in the symmetric pool, 16-byte chunks;
+    otherwise the runtime falls back to the partition's entry). At n = 2 the switch saves no
+    bytes and costs a round trip (round 1 probe: 394 vs 700 GB/s busbw); from n = 4 it moves
+    ~S per GPU each way instead of 1.5 S (profiles/r01_nvls_probe.txt). int32 has no vector
+    form in the switch (scalar adds), so floats only."""
+    if coll != "allreduce" or n < 4:
+        return []
+    return [("nvls", 16 * MiB, INF, ("bfloat16", "float32"))]
+
+
+def default_schedules(coll: str, n: int, multicast: bool = True):
+    """EF texts of the default set for (coll, n), each carrying its size range; multicast
+    entries (multicast_ranges) last."""
     from . import generate
     out = []
-    for algo, lo, hi, *dt in ranges(coll, n):
+    extra = multicast_ranges(coll, n) if multicast else []
+    for algo, lo, hi, *dt in ranges(coll, n) + extra:
         name, _, p = algo.partition("_p")
         out.append(generate(coll, name, n, int(p) if p else 1, 1, min_bytes=lo, max_bytes=hi,
                             dtypes=dt[0] if dt else None))

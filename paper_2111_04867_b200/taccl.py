@@ -53,6 +53,10 @@ def lib():
             "taccl_buffer_export": ([c_vp, c_size, c_vp, ctypes.POINTER(c_size)], c_int),
             "taccl_register_buffer": ([c_vp, c_size, c_vp, c_size], c_int),
             "taccl_unregister_buffer": ([c_vp], c_int),
+            "taccl_pool_export": ([c_size, c_vp, ctypes.POINTER(c_size)], c_int),
+            "taccl_pool_connect": ([c_vp, c_size], c_int),
+            "taccl_pool_bind": ([ctypes.POINTER(c_vp), ctypes.POINTER(c_size)], c_int),
+            "taccl_pool_alloc": ([c_size, ctypes.POINTER(c_vp)], c_int),
             "taccl_load_algo": ([c_cp, c_size, ctypes.POINTER(c_vp)], c_int),
             "taccl_run": ([c_int, c_vp, c_vp, c_size, c_int, c_vp], c_int),
             "taccl_run_emulated": ([c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_size, c_int, c_vp], c_int),
@@ -173,6 +177,42 @@ class Comm:
         _check(lib().taccl_buffer_export(ctypes.c_void_p(ptr), nbytes, blob, ctypes.byref(n)))
         allb = self._all_gather_bytes(blob.raw[:n.value])
         _check(lib().taccl_register_buffer(ctypes.c_void_p(ptr), nbytes, allb, HANDLE_BYTES))
+
+    def create_pool(self, nbytes):
+        """Collective: the symmetric multicast pool (include/taccl.h taccl_pool_*), so
+        multicast-reduce (NVLink SHARP) algorithms can run on tensors from pool_tensor()."""
+        blob = ctypes.create_string_buffer(HANDLE_BYTES)
+        n = ctypes.c_size_t(0)
+        rc = lib().taccl_pool_export(nbytes, blob, ctypes.byref(n))
+        err = last_error() if rc else ""
+        allb = self._all_gather_bytes(blob.raw if rc == 0 else b"\0" * HANDLE_BYTES)  # every rank joins
+        if rc:
+            raise TacclError(rc, err)
+        if any(int.from_bytes(allb[q * HANDLE_BYTES:q * HANDLE_BYTES + 4], "little") != 0x7acc1c0d
+               for q in range(self.nranks)):
+            raise TacclError(5, "a peer could not create its pool")
+        _check(lib().taccl_pool_connect(allb, HANDLE_BYTES))
+        self._barrier()  # every device added to the multicast object before anyone binds
+        base, size = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().taccl_pool_bind(ctypes.byref(base), ctypes.byref(size)))
+        self._barrier()  # flags cleared everywhere before any collective uses them
+        return size.value
+
+    def pool_tensor(self, numel, dtype):
+        """A tensor in the symmetric pool (same offset on every rank: allocate in the same order
+        with the same sizes everywhere)."""
+        import torch
+        nbytes = numel * torch.empty((), dtype=dtype).element_size()
+        p = ctypes.c_void_p()
+        _check(lib().taccl_pool_alloc(nbytes, ctypes.byref(p)))
+
+        class _Mem:  # zero-copy view (CUDA array interface); the pool owns the memory
+            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (p.value, False), "version": 3}
+        return torch.as_tensor(_Mem(), device="cuda").view(dtype)
+
+    def _barrier(self):
+        import torch.distributed as dist
+        dist.barrier(group=self.group)
 
     def unregister(self, t):
         """Local: forget the mapping of `t`'s storage (call before the tensor is freed)."""

@@ -265,3 +265,94 @@ def test_full_size_multiprocess(n):
     for rank, results, err in sorted(res, key=lambda x: x[0]):
         assert err is None, f"rank {rank}: {err}"
         assert all(results), f"rank {rank}: failing cases {[c for c, ok in zip(FULL_CASES, results) if not ok]}"
+
+
+# ---------------------------------------------------------------- multicast reduce (NVLink SHARP)
+
+NVLS_CASES = [  # (dtype, count per rank-chunk multiple, kind, in_place); counts keep 16-byte chunks
+    ("bfloat16", 8 * 4096, "uniform", False),
+    ("bfloat16", 8 * (1 << 18), "normal", False),
+    ("float32", 8 * 4096, "intval", False),
+    ("int32", 8 * 1024, "bits", False),
+    ("bfloat16", 8 * 4096, "uniform", True),
+    ("bfloat16", 8 * (3 << 20), "uniform", False),  # 48 MiB of bf16: many pieces per CTA
+]
+
+
+def _nvls_worker(rank, n, port, q):
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2111_04867_b200 import taccl
+    from paper_2111_04867_b200.generator import generate
+    from paper_2111_04867_b200.inputs import allreduce_input
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}
+    view = {"int32": np.int32, "float32": np.int32, "bfloat16": np.int16}
+    tview = {"int32": torch.int32, "float32": torch.int32, "bfloat16": torch.int16}
+    try:
+        comm = taccl.Comm(rank=rank, nranks=n, device=rank, scratch_bytes=64 << 20)
+        comm.create_pool(1 << 30)
+        nv = generate("allreduce", "nvls", n, 1, 1)
+        comm.load(generate("allreduce", "direct", n, 1, 1))  # the fallback for non-pool calls
+        comm.load(nv)
+        results = []
+        for dtype, count, kind, in_place in NVLS_CASES:
+            ins = [allreduce_input(count, dtype, kind, 23, r) for r in range(n)]
+            x = comm.pool_tensor(count, tdt[dtype])
+            x.view(tview[dtype]).copy_(torch.from_numpy(ins[rank].view(view[dtype])).view(tview[dtype]))
+            out = x if in_place else comm.pool_tensor(count, tdt[dtype])
+            for _ in range(3):  # repeated calls: epochs of the multicast barriers
+                if not in_place:
+                    out.view(torch.uint8).fill_(0xA5)
+                else:
+                    x.view(tview[dtype]).copy_(torch.from_numpy(ins[rank].view(view[dtype])).view(tview[dtype]))
+                comm.run("allreduce", out, x)
+            torch.cuda.synchronize()
+            comm.check()
+            got = out.view(tview[dtype]).cpu().numpy().view(ins[0].dtype)
+            want = oracle.run(oracle.parse(nv), ins, dtype)[rank]
+            if kind == "normal":  # the switch's fp32 accumulation order is its own: norm-wise bound
+                ref = oracle.expected_allreduce_f64(ins, dtype)
+                scale = sum(np.abs(oracle.collectives.to_f64(v, dtype)) for v in ins)
+                ok = bool((np.abs(oracle.collectives.to_f64(got, dtype) - ref) / scale).max() <= 1e-2)
+            else:  # integers wrap exactly; U[1,2) bf16 and integer-valued fp32 sum exactly in fp32
+                ok = bool(np.array_equal(got, want))
+            results.append(ok)
+        # not in the pool -> the multicast algorithm is skipped, the direct one runs
+        xs = torch.from_numpy(allreduce_input(n * 1024, "int32", "bits", 24, rank)).cuda()
+        os_ = torch.empty_like(xs)
+        comm.register(os_)
+        comm.run("allreduce", os_, xs)
+        torch.cuda.synchronize()
+        alls = [allreduce_input(n * 1024, "int32", "bits", 24, r) for r in range(n)]
+        results.append(bool(np.array_equal(os_.cpu().numpy(), oracle.expected_outputs("allreduce", alls, "int32")[rank])))
+        comm.destroy()
+        q.put((rank, results, None))
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_multicast_reduce_parity(n):
+    # the EF multicast-reduce step through the symmetric pool: multimem.ld_reduce/st over the
+    # NVSwitch between processes (POSIX-fd handle exchange), vs the oracle
+    if NGPU < n:
+        pytest.skip(f"needs {n} GPUs, have {NGPU}")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nvls_worker, args=(r, n, port, q)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(n)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, results, err in sorted(res, key=lambda x: x[0]):
+        assert err is None, f"rank {rank}: {err}"
+        assert all(results), f"rank {rank}: {results}"

@@ -147,11 +147,11 @@ def test_instance_subchunk_floor_split_by_hand():
     seen = []
     orig_read = simulate._execute
 
-    def spy(prog_, graph, order, bufs, read, write, reduce):
+    def spy(prog_, graph, order, bufs, read, write, reduce, *rest):
         def w(buf, off, cnt, vals):
             seen.append((off, len(vals)))
             return write(buf, off, cnt, vals)
-        return orig_read(prog_, graph, order, bufs, read, w, reduce)
+        return orig_read(prog_, graph, order, bufs, read, w, reduce, *rest)
     simulate._execute = spy
     try:
         oracle.run(exp, ins, "int32")
