@@ -24,7 +24,8 @@ import torch.distributed as dist  # noqa: E402
 from paper_2111_04867_b200 import taccl  # noqa: E402
 from paper_2111_04867_b200.generator import generate  # noqa: E402
 
-ALGOS = {"allgather": ["direct", "ring", "auto"], "alltoall": ["direct"], "allreduce": ["direct", "ring", "oneshot", "auto"],
+ALGOS = {"allgather": ["direct", "ring", "auto"], "alltoall": ["direct"],
+         "allreduce": ["direct", "ring", "oneshot", "nvls", "auto"],
          "reducescatter": ["direct", "ring", "auto"]}
 
 
@@ -168,6 +169,7 @@ def main():
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (no host overhead)")
     ap.add_argument("--algos", default=None, help="comma list overriding the per-collective defaults")
+    ap.add_argument("--pool", action="store_true", help="buffers in the symmetric multicast pool (NVLS eligible)")
     ap.add_argument("--oracle-cap", type=int, default=0,
                     help="time the CPU oracle per point on rank 0 (sample <= this many bytes; 0 = off)")
     ap.add_argument("--peak-nvlink", type=float, default=705.0,
@@ -184,11 +186,17 @@ def main():
     comm = taccl.Comm(rank=rank, nranks=n, device=local, scratch_bytes=2 * S_max + (64 << 20))
     dt = torch.bfloat16 if a.dtype == "bfloat16" else torch.float32
     es = 2 if dt == torch.bfloat16 else 4
-    # buffers sized for the largest message; registered once (zero-copy)
-    big_in = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
-    big_out = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
-    comm.register(big_out)
-    comm.register(big_in)  # pull mode (receive-reduce reads peers' inputs in place)
+    # buffers sized for the largest message; registered once (zero-copy); --pool: both in the
+    # symmetric multicast pool (multicast-reduce algorithms eligible; peers mapped by the pool)
+    if a.pool and n > 1:
+        comm.create_pool(2 * S_max + (8 << 20))
+        big_in = comm.pool_tensor(S_max // es + 64, dt)
+        big_out = comm.pool_tensor(S_max // es + 64, dt)
+    else:
+        big_in = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
+        big_out = torch.empty(S_max // es + 64, dtype=dt, device="cuda")
+        comm.register(big_out)
+        comm.register(big_in)  # pull mode (receive-reduce reads peers' inputs in place)
     stream = torch.cuda.Stream() if a.graph else torch.cuda.current_stream()
     torch.cuda.set_stream(stream)
     tf = (lambda f, st, w: timeit_graph(f, st, w)) if a.graph else timeit
