@@ -435,8 +435,8 @@ __device__ __forceinline__ void mm_st(char* p, uint4 v) {  // 16 bytes to every 
   asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
                "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w)) : "memory");
 }
-__device__ __noinline__ void cta_mr(char* mdst, const char* msrc, int64_t nbytes, int dtype) {
-  constexpr int U = 4;
+template <int U>
+__device__ __noinline__ void cta_mr_u(char* mdst, const char* msrc, int64_t nbytes, int dtype) {
   const int64_t nv = nbytes >> 4, nt = blockDim.x;
   int64_t i = threadIdx.x;
   for (; i + (U - 1) * nt < nv; i += U * nt) {
@@ -447,6 +447,15 @@ __device__ __noinline__ void cta_mr(char* mdst, const char* msrc, int64_t nbytes
     for (int u = 0; u < U; ++u) mm_st(mdst + 16 * (i + u * nt), v[u]);
   }
   for (; i < nv; i += nt) mm_st(mdst + 16 * i, mm_ld_reduce(msrc + 16 * i, dtype));
+}
+// u: vectors in flight per thread (KArgs.mr_unroll, env TACCL_MR_UNROLL: 1, 2, 4 or 8)
+__device__ __forceinline__ void cta_mr(char* mdst, const char* msrc, int64_t nbytes, int dtype, int u) {
+  switch (u) {
+    case 1: cta_mr_u<1>(mdst, msrc, nbytes, dtype); break;
+    case 2: cta_mr_u<2>(mdst, msrc, nbytes, dtype); break;
+    case 8: cta_mr_u<8>(mdst, msrc, nbytes, dtype); break;
+    default: cta_mr_u<4>(mdst, msrc, nbytes, dtype); break;
+  }
 }
 // the multicast-reduce barrier: publish this rank's arrival for (phase, group, piece) to every
 // rank's copy (one multimem.st with release semantics), then wait for every rank's word.
@@ -1301,7 +1310,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
         case K_MR: {  // multicast reduce of this piece, then every rank's piece j must be written
           const char* src = R.mc_in + (int64_t)st.srcoff * cbytes;  // (src/dst: i and o only)
           char* dst = R.mc_out + (int64_t)st.dstoff * cbytes;
-          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_mr(dst + off, src + off, len, A.dtype); });
+          for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_mr(dst + off, src + off, len, A.dtype, A.mr_unroll); });
           __syncthreads();
           if (tid == 0 && !mr_barrier(R, A.nranks, 1, st.seq, j, (unsigned)c.epoch, A.timeout_ns)) {
             record_error(c, st.op, k);

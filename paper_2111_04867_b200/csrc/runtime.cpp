@@ -283,7 +283,9 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   // when possible, so every stripe starts cache-line / page aligned
   int64_t gb = elt;
   while (gb < 4096 && G->chunk_bytes % (gb * 2) == 0) gb *= 2;
-  const int64_t smax = (int64_t)env_size("TACCL_STRIPE", 64 << 10);
+  // multicast reduces stream best in 16 KiB stripes (profiles/r02_nvls_scan_n4.txt: 64 MiB
+  // 172 vs 183 us at 64 KiB)
+  const int64_t smax = (int64_t)env_size("TACCL_STRIPE", a->has_mr ? (16 << 10) : (64 << 10));
   int64_t st = gb;
   while (st * 2 <= smax && st * 2 * G->split <= G->chunk_bytes) st *= 2;
   G->stripe = st;
@@ -347,6 +349,9 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   memset(&A, 0, sizeof(A));
   A.nlocal = (int)ranks.size();
   A.nranks = g.nranks;
+  // one multimem.ld_reduce in flight per thread measured best (profiles/r02_nvls_scan_n4.txt:
+  // 64 MiB 173 us at 1, 177 at 2, 183 at 4, 194 at 8)
+  A.mr_unroll = (int)env_size("TACCL_MR_UNROLL", 1);
   A.split = G.split;
   A.dep_ctas = G.dep_ctas;
   A.indep_cap = G.indep_cap;

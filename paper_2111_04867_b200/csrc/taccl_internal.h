@@ -199,6 +199,7 @@ struct KArgs {
   KRank r[kMaxRanks];
   int32_t nlocal;          // local ranks in this launch
   int32_t nranks;          // ranks of the communicator (multicast-reduce barriers)
+  int32_t mr_unroll;       // multicast reduce: 16-byte vectors in flight per thread
   int32_t split;           // pieces per chunk (instances x lanes); flags are per piece
   int32_t variant;         // data-movement variant (env TACCL_COPY_VARIANT); timing probes
                            // only, results invalid: 9 = no fence before data flags, 20 = LL

@@ -269,10 +269,12 @@ def test_full_size_multiprocess(n):
 
 # ---------------------------------------------------------------- multicast reduce (NVLink SHARP)
 
-NVLS_CASES = [  # (dtype, count per rank-chunk multiple, kind, in_place); counts keep 16-byte chunks
+NVLS_CASES = [  # (dtype, count, kind, in_place); counts keep 16-byte chunks
     ("bfloat16", 8 * 4096, "uniform", False),
     ("bfloat16", 8 * (1 << 18), "normal", False),
+    ("bfloat16", 8 * 4096, "intval", False),
     ("float32", 8 * 4096, "intval", False),
+    ("float32", 8 * 4096, "uniform", False),
     ("int32", 8 * 1024, "bits", False),
     ("bfloat16", 8 * 4096, "uniform", True),
     ("bfloat16", 8 * (3 << 20), "uniform", False),  # 48 MiB of bf16: many pieces per CTA
@@ -314,11 +316,16 @@ def _nvls_worker(rank, n, port, q):
             comm.check()
             got = out.view(tview[dtype]).cpu().numpy().view(ins[0].dtype)
             want = oracle.run(oracle.parse(nv), ins, dtype)[rank]
-            if kind == "normal":  # the switch's fp32 accumulation order is its own: norm-wise bound
+            tol = 1e-2 if dtype == "bfloat16" else 1e-6
+            if kind == "normal":  # the switch's accumulation and rounding are its own: norm-wise bound
                 ref = oracle.expected_allreduce_f64(ins, dtype)
                 scale = sum(np.abs(oracle.collectives.to_f64(v, dtype)) for v in ins)
-                ok = bool((np.abs(oracle.collectives.to_f64(got, dtype) - ref) / scale).max() <= 1e-2)
-            else:  # integers wrap exactly; U[1,2) bf16 and integer-valued fp32 sum exactly in fp32
+                ok = bool((np.abs(oracle.collectives.to_f64(got, dtype) - ref) / scale).max() <= tol)
+            elif kind == "uniform":  # north star: within 1e-2 / 1e-6 of the fp64 sum (the switch
+                # rounds bf16 its own way, profiles/r02_nvls_rounding.txt: not bit-exact vs RNE)
+                ref = oracle.expected_allreduce_f64(ins, dtype)
+                ok = bool((np.abs(oracle.collectives.to_f64(got, dtype) - ref) / np.abs(ref)).max() <= tol)
+            else:  # integers wrap exactly; integer-valued floats: every partial sum is exact
                 ok = bool(np.array_equal(got, want))
             results.append(ok)
         # not in the pool -> the multicast algorithm is skipped, the direct one runs
