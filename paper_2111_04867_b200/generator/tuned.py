@@ -64,7 +64,9 @@ def multicast_ranges(coll: str, n: int):
     form in the switch (scalar adds), so floats only."""
     if coll != "allreduce" or n < 4:
         return []
-    return [("nvls", 16 * MiB, INF, ("bfloat16", "float32"))]
+    # n = 4 (profiles/r02_sweep_nvls_n4.txt): bf16 ahead of direct and NCCL from 16 MiB; fp32
+    # ahead until the relay-first ring takes over at 128 MiB
+    return [("nvls", 16 * MiB, INF, ("bfloat16",)), ("nvls", 16 * MiB, 128 * MiB, ("float32",))]
 
 
 def default_schedules(coll: str, n: int, multicast: bool = True):
