@@ -63,6 +63,11 @@ struct Algo {
   int lean_srcoff = 0, lean_dstoff = 0, lean_cnt = 0;
   std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
   std::vector<DevPlan> plans_ll;  // the same program planned for the LL kernel (chain sends fused)
+  // the direct plan with fused chains also reading their peers' inputs in place (pull kinds
+  // | 4): used for chunks >= TACCL_PULL_CHAIN_MIN (default 64 MiB), where the in-place loads
+  // beat push + staging (profiles/r02_rs_scan_n4.txt: RS n=4 1 GiB 1373 vs 1470 us) — below,
+  // the pushes overlap the reduction better (16 MiB: 51 vs 37 us). Empty if no chain pulls.
+  std::vector<DevPlan> plans_pc;
   std::vector<int> ntb;         // per rank
   std::vector<std::vector<int>> weights;  // per rank, per tb
   std::vector<std::vector<int>> indep;    // per rank, per tb
@@ -369,11 +374,14 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.timeout_ns = g.timeout_ns;
   A.trace = g.trace;
   A.trace_ctas = g.trace_ctas;
+  const bool pull_on = peer_in && !G.staged && g.nranks > 1 && env_size("TACCL_PULL", 1) != 0;
+  const bool pull_chains = pull_on && !a->plans_pc.empty() &&
+                           G.chunk_bytes >= (int64_t)env_size("TACCL_PULL_CHAIN_MIN", 64ull << 20);
   int cta = 0, smem = 0;
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
     KRank& R = A.r[i];
-    const DevPlan& dp = G.staged ? a->plans_ll[r] : a->plans[r];
+    const DevPlan& dp = G.staged ? a->plans_ll[r] : pull_chains ? a->plans_pc[r] : a->plans[r];
     R.plan = (const char*)dp.mem;
     R.plan_bytes = dp.bytes;
     R.steps_off = dp.steps_off;
@@ -419,7 +427,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   // default plain rrcs only: plan.cpp); TACCL_PULL=0 turns the mode off
   // (only for plans with pulled steps: for the others the mode changes nothing, and a rank
   // running in place next to one that does not is legal)
-  A.pull = (peer_in && a->has_pull && !G.staged && g.nranks > 1 && env_size("TACCL_PULL", 1) != 0) ? 1 : 0;
+  A.pull = (pull_on && (a->has_pull || pull_chains)) ? 1 : 0;
   std::string err;
   const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -699,6 +707,8 @@ taccl_result_t taccl_comm_destroy(void) {
       if (p.mem) cudaFree(p.mem);
     for (auto& p : a->plans_ll)
       if (p.mem) cudaFree(p.mem);
+    for (auto& p : a->plans_pc)
+      if (p.mem) cudaFree(p.mem);
     delete a;
   }
   for (auto& kv : g.ipc_open) cudaIpcCloseMemHandle(kv.second);
@@ -822,7 +832,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
   if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
   if (!text) return fail(TACCL_ERR_INVALID_ARG, "null text");
   std::unique_ptr<Algo> a(new Algo);
-  std::vector<RankPlan> plans, plans_ll;
+  std::vector<RankPlan> plans, plans_ll, plans_pc;
   std::vector<int> P_o_chunks;
   try {
     Program P = parse_ef(text, len);
@@ -842,6 +852,8 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     // direct kernel (profiles/r01_chain_sends_ll_n4.txt): two plans, picked per call
     plans = build_plans(P, fuse, rrcs, env_size("TACCL_CHAIN_SENDS", 0) != 0, (int)env_size("TACCL_PULL_KINDS", 1));
     plans_ll = build_plans(P, fuse, rrcs, env_size("TACCL_NO_CHAIN_SENDS_LL", 0) == 0);
+    const int pk = (int)env_size("TACCL_PULL_KINDS", 1);
+    if (!(pk & 4)) plans_pc = build_plans(P, fuse, rrcs, env_size("TACCL_CHAIN_SENDS", 0) != 0, pk | 4);
     a->name = P.name;
     a->coll = P.coll;
     a->nranks = P.nranks;
@@ -856,6 +868,13 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
   }
   a->plans.assign(a->nranks, DevPlan());
   a->plans_ll.assign(a->nranks, DevPlan());
+  // keep the pulled-chain plan only if it differs (some fused chain reads a peer's input)
+  bool pc = false;
+  for (const RankPlan& rp : plans_pc)
+    for (size_t i = 0; i < rp.steps.size(); ++i)
+      if (rp.steps[i].op == K_RRC_FUSED)
+        for (int f = 0; f < rp.steps[i].fuse_count; ++f) pc = pc || rp.fused[kFuseStride * (rp.steps[i].fuse_begin + f) + 4] >= 0;
+  if (pc) a->plans_pc.assign(a->nranks, DevPlan());
   a->ntb.assign(a->nranks, 0);
   for (int r = 0; r < a->nranks; ++r) {
     a->ntb[r] = (int)plans[r].tbs.size();
@@ -890,6 +909,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     if (g.emulated || r == g.rank) {
       taccl_result_t rc = upload(plans[r], &a->plans[r]);
       if (!rc) rc = upload(plans_ll[r], &a->plans_ll[r]);
+      if (!rc && pc) rc = upload(plans_pc[r], &a->plans_pc[r]);
       if (rc) return rc;
     }
   }
@@ -905,6 +925,8 @@ taccl_result_t taccl_free(taccl_algo_t algo) {
   for (auto& p : (*it)->plans)
     if (p.mem) cudaFree(p.mem);
   for (auto& p : (*it)->plans_ll)
+    if (p.mem) cudaFree(p.mem);
+  for (auto& p : (*it)->plans_pc)
     if (p.mem) cudaFree(p.mem);
   delete *it;
   g.algos.erase(it);

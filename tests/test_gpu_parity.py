@@ -346,6 +346,24 @@ def test_reducescatter_exact(algo, n, p, m, dtype, mode):
     assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
 
 
+@pytest.mark.parametrize("coll,n,p", [("reducescatter", 4, 1), ("reducescatter", 8, 2), ("allreduce", 4, 1)])
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
+def test_pulled_chain_plan(coll, n, p, dtype):
+    # the large-chunk plan whose fused chains load every peer's input in place
+    # (TACCL_PULL_CHAIN_MIN=0 selects it at any size): same bits as the oracle
+    os.environ["TACCL_PULL_CHAIN_MIN"] = "0"
+    try:
+        count = p * 1013 * (n if coll == "allreduce" else 1)
+        text = generate(coll, "direct", n, p, 1)
+        e_in = n * count if coll == "reducescatter" else count
+        kind = "bits" if dtype == "int32" else "uniform"
+        ins = [allreduce_input(e_in, dtype, kind, 25, r) for r in range(n)]
+        got = run_gpu(text, coll, n, dtype, ins, mode="direct")
+        assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
+    finally:
+        os.environ.pop("TACCL_PULL_CHAIN_MIN", None)
+
+
 @pytest.mark.parametrize("algo,n,dtype,tol", [("direct", 8, "float32", 1e-6), ("ring", 4, "float32", 1e-6),
                                               ("direct", 8, "bfloat16", 1e-2), ("ring", 4, "bfloat16", 1e-2)])
 def test_reducescatter_tolerance_uniform(algo, n, dtype, tol):
