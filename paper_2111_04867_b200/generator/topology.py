@@ -19,12 +19,17 @@ from dataclasses import dataclass, field
 NVLINK_ALPHA_US = 0.7            # Table 1
 NVLINK5_BETA_US_PER_MB = (1 << 20) / 900e9 * 1e6   # 1.165 us/MB at 900 GB/s
 IB_ALPHA_US, IB_BETA_US_PER_MB = 1.7, 106.0        # Table 1
-# Measured on this pool's B200s through this executor (tools/alphabeta.py over the graph-mode
-# sweeps, profiles/r01_alphabeta.json): one connection per GPU (ring hop) streams at 714 GB/s
-# (beta 1.468 us/MB) with ~6 us per hop of flag/fence overhead (direct kernel); n-1 concurrent
-# connections share ~690 GB/s per GPU (the paper's multi-connection effect).
-B200_NVLINK_ALPHA_US = 6.6
-B200_NVLINK_BETA_US_PER_MB = 1.468
+# Measured on this pool's B200s the paper's way (k chunks one after another
+# vs all at once on one link, least squares; tools/ab_profile.py through this executor,
+# generator/profiler.py, profiles/r02_alphabeta.json): zero-copy kernel alpha 5.35 us, beta
+# 1.43 us/MB (733 GB/s per connection, both directions busy), plus ~9.4 us per call; LL kernel
+# (<= 2 MiB) alpha 2.58 us, beta 3.65 us/MB. The connection-count sweep (PAPER.md:405-418,
+# tools/nvlink_probe.cu, profiles/r02_nvlink_probe.jsonl) at 1 GiB per GPU: 695 / 694 / 623
+# GB/s accumulated egress over 1 / 2 / 3 concurrent connections (4 GPUs) — the paper's
+# multi-connection effect on NVLink 5.
+B200_NVLINK_ALPHA_US = 5.35
+B200_NVLINK_BETA_US_PER_MB = 1.43
+B200_LL_ALPHA_US, B200_LL_BETA_US_PER_MB = 2.58, 3.65
 
 
 @dataclass(frozen=True)
