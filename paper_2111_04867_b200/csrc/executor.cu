@@ -1440,7 +1440,80 @@ __global__ void __launch_bounds__(256) taccl_copy_kernel(char* __restrict__ dst,
   }
 }
 
+// Lean multicast reduce: a plan that is ONE `mr` step per rank with no dependencies (the nvls
+// Allreduce template) runs without the interpreter — every CTA b of every rank grid-strides
+// over the same 16-byte vectors of its rank's share, so CTA b's barriers pair with CTA b of
+// every rank: pre-barrier (every rank entered this call: its input is final), the multicast
+// reduce, post-barrier (no rank leaves while another still reads or writes its buffers).
+// 2 CTAs per SM of 512 threads (the interpreter holds 1). Epoch protocol as the interpreter's.
+__global__ void __launch_bounds__(512, 2) taccl_mr_kernel(const __grid_constant__ KArgs A, int64_t src_off,
+                                                         int64_t dst_off, int64_t nbytes) {
+  const KRank& R = A.r[0];
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(R.arena + kOffCtrl);
+  __shared__ u64 s_epoch;
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) {
+    const u64 ep = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
+    s_epoch = ep;
+    s_abort = 0;
+    if (blockIdx.x != 0) {
+      const unsigned one = 1u + (unsigned)(ep >> 62);
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&ctrl->finished), "r"(one) : "memory");
+    }
+    if (!mr_barrier(R, A.nranks, 0, blockIdx.x / kMaxSplit, blockIdx.x % kMaxSplit, (unsigned)ep, A.timeout_ns)) {
+      s_abort = 1;
+      if (atomicCAS(&ctrl->error, 0u, 1u) == 0u) ctrl->err_what = K_MR;
+    }
+  }
+  __syncthreads();
+  const u64 epoch = s_epoch;
+  if (!s_abort) {
+    const char* src = R.mc_in + src_off;
+    char* dst = R.mc_out + dst_off;
+    const int64_t nv = nbytes >> 4, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += nt)
+      mm_st(dst + 16 * i, mm_ld_reduce(src + 16 * i, A.dtype));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (!s_abort && !mr_barrier(R, A.nranks, 1, blockIdx.x / kMaxSplit, blockIdx.x % kMaxSplit, (unsigned)epoch, A.timeout_ns))
+      if (atomicCAS(&ctrl->error, 0u, 1u) == 0u) ctrl->err_what = K_MR;
+    if (blockIdx.x == 0) {  // the rank's epoch advances once every CTA has read it
+      const unsigned want = gridDim.x - 1;
+      volatile unsigned* fin = &ctrl->finished;
+      const u64 t0 = globaltimer();
+      while (*fin < want)
+        if (globaltimer() - t0 > A.timeout_ns) {
+          if (atomicCAS(&ctrl->error, 0u, 1u) == 0u) ctrl->err_what = K_NOP;
+          break;
+        }
+      ctrl->finished = 0;
+      *reinterpret_cast<volatile u64*>(&ctrl->epoch) = epoch + 1;
+    }
+  }
+}
+
 }  // namespace
+
+int mr_grid(int device) {
+  static int sms = 0;
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, taccl_mr_kernel, 512, 0) != cudaSuccess || per < 1) per = 1;
+  const char* e = getenv("TACCL_MR_CTAS_PER_SM");  // knob for measurements (default 2)
+  const int want = e && atoi(e) > 0 ? atoi(e) : 2;
+  return sms * std::min(per, want);
+}
+
+int launch_mr(const KArgs& a, int64_t src_off, int64_t dst_off, int64_t bytes, int grid, void* stream, std::string* err) {
+  taccl_mr_kernel<<<grid, 512, 0, (cudaStream_t)stream>>>(a, src_off, dst_off, bytes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("multicast-reduce launch: ") + cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
 
 int copy_grid(int64_t bytes) {
   static int sms = 0;

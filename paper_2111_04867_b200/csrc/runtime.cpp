@@ -60,6 +60,9 @@ struct Algo {
   int max_scratch_chunks = 0, max_stage_chunks = 0, max_stage2_chunks = 0, max_steps_cnt = 1;
   // n = 1 plan that is one input -> output `cpy` (no deps): runs as the lean copy kernel
   bool lean_copy = false;
+  // one `mr` step per rank, no dependencies (nvls template): the lean multicast-reduce kernel
+  bool lean_mr = false;
+  std::vector<int> mr_srcoff, mr_dstoff, mr_cnt;  // per rank
   int lean_srcoff = 0, lean_dstoff = 0, lean_cnt = 0;
   std::vector<DevPlan> plans;   // indexed by rank (only local ranks filled)
   std::vector<DevPlan> plans_ll;  // the same program planned for the LL kernel (chain sends fused)
@@ -345,6 +348,31 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     const int64_t cb = G.chunk_bytes;
     if (launch_copy((char*)recvs[0] + a->lean_dstoff * cb, (const char*)sends[0] + a->lean_srcoff * cb,
                     a->lean_cnt * cb, stream, &err))
+      return fail(TACCL_ERR_CUDA, err);
+    ++g.launches;
+    ++g_launches;
+    return TACCL_SUCCESS;
+  }
+  if (mr && a->lean_mr && ranks.size() == 1) {  // one multicast reduce per rank
+    KArgs M;
+    memset(&M, 0, sizeof(M));
+    const int r = ranks[0];
+    KRank& R = M.r[0];
+    R.arena = g.peer_arena[r];
+    R.rank = r;
+    R.mc_in = g.pool.mcva + ((const char*)sends[0] - g.pool.uc);
+    R.mc_out = g.pool.mcva + ((char*)recvs[0] - g.pool.uc);
+    R.nv_mc = g.pool.mcva;
+    R.nv_uc = (unsigned*)g.pool.uc;
+    M.nlocal = 1;
+    M.nranks = g.nranks;
+    M.dtype = dtype;
+    M.elt = elt;
+    M.timeout_ns = g.timeout_ns;
+    std::string err;
+    const int64_t cb = G.chunk_bytes;
+    if (launch_mr(M, (int64_t)a->mr_srcoff[r] * cb, (int64_t)a->mr_dstoff[r] * cb, (int64_t)a->mr_cnt[r] * cb,
+                  mr_grid(g.device), stream, &err))
       return fail(TACCL_ERR_CUDA, err);
     ++g.launches;
     ++g_launches;
@@ -896,6 +924,17 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->fused_chains += plans[r].fused_chains;
     for (const KStep& k : plans[r].steps) a->has_mr = a->has_mr || k.op == K_MR;
     for (const KStep& k : plans[r].steps) a->has_pull = a->has_pull || (k.op == K_SEND && k.poff >= 0);
+    {
+      const RankPlan& rp = plans[r];
+      const bool one_mr = rp.steps.size() == 1 && rp.steps[0].op == K_MR && rp.steps[0].dep_count == 0 &&
+                          (rp.steps[0].srcbuf == KB_I || rp.steps[0].srcbuf == KB_O) && rp.steps[0].dstbuf == KB_O;
+      if (r == 0) a->lean_mr = env_size("TACCL_NO_LEAN_MR", 0) == 0;
+      a->lean_mr = a->lean_mr && one_mr;
+      a->mr_srcoff.push_back(one_mr ? rp.steps[0].srcoff : 0);
+      a->mr_dstoff.push_back(one_mr ? rp.steps[0].dstoff : 0);
+      a->mr_cnt.push_back(one_mr ? rp.steps[0].cnt : 0);
+      if (one_mr && rp.steps[0].srcbuf == KB_O) a->lean_mr = false;  // in-place-in-o forms: interpreter
+    }
     if (a->nranks == 1 && plans[r].steps.size() == 1) {
       const KStep& k = plans[r].steps[0];
       if (k.op == K_CPY && k.srcbuf == KB_I && k.dstbuf == KB_O && k.dep_count == 0 &&

@@ -276,6 +276,10 @@ int launch_executor(const KArgs& a, int grid, int smem, void* stream, std::strin
 // single-step local-copy plans (n = 1): dst[0, bytes) = src[0, bytes) in one lean kernel
 int launch_copy(char* dst, const char* src, int64_t bytes, void* stream, std::string* err);
 int copy_grid(int64_t bytes);  // its grid size
+// single-step multicast-reduce plans (the nvls Allreduce): every CTA of every rank reduces the
+// same grid-stride vectors of [src_off, src_off + bytes) of its share (16-byte multiple)
+int launch_mr(const KArgs& a, int64_t src_off, int64_t dst_off, int64_t bytes, int grid, void* stream, std::string* err);
+int mr_grid(int device);
 constexpr int kPlanSmemMax = (48 << 10) / kDirectPerSM;  // plans up to this size are staged in smem
 int executor_max_ctas(int device, std::string* err);  // co-resident CTA capacity
 

@@ -281,7 +281,7 @@ NVLS_CASES = [  # (dtype, count, kind, in_place); counts keep 16-byte chunks
 ]
 
 
-def _nvls_worker(rank, n, port, q):
+def _nvls_worker(rank, n, port, q, lean=True):
     import torch.distributed as dist
 
     import oracle
@@ -289,6 +289,8 @@ def _nvls_worker(rank, n, port, q):
     from paper_2111_04867_b200.generator import generate
     from paper_2111_04867_b200.inputs import allreduce_input
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if not lean:  # the interpreter's K_MR step instead of the lean multicast-reduce kernel
+        os.environ["TACCL_NO_LEAN_MR"] = "1"
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=n)
     tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}
@@ -344,8 +346,9 @@ def _nvls_worker(rank, n, port, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("lean", [True, False])
 @pytest.mark.parametrize("n", [2, 4])
-def test_multicast_reduce_parity(n):
+def test_multicast_reduce_parity(n, lean):
     # the EF multicast-reduce step through the symmetric pool: multimem.ld_reduce/st over the
     # NVSwitch between processes (POSIX-fd handle exchange), vs the oracle
     if NGPU < n:
@@ -354,7 +357,7 @@ def test_multicast_reduce_parity(n):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_nvls_worker, args=(r, n, port, q)) for r in range(n)]
+    procs = [ctx.Process(target=_nvls_worker, args=(r, n, port, q, lean)) for r in range(n)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(n)]
