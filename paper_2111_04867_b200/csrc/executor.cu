@@ -1445,7 +1445,8 @@ __global__ void __launch_bounds__(256) taccl_copy_kernel(char* __restrict__ dst,
 // over the same 16-byte vectors of its rank's share, so CTA b's barriers pair with CTA b of
 // every rank: pre-barrier (every rank entered this call: its input is final), the multicast
 // reduce, post-barrier (no rank leaves while another still reads or writes its buffers).
-// 2 CTAs per SM of 512 threads (the interpreter holds 1). Epoch protocol as the interpreter's.
+// One CTA per SM of 512 threads (40 registers; more CTAs per SM measured slower: the switch,
+// not the issue rate, bounds it). Epoch protocol as the interpreter's.
 __global__ void __launch_bounds__(512, 2) taccl_mr_kernel(const __grid_constant__ KArgs A, int64_t src_off,
                                                          int64_t dst_off, int64_t nbytes) {
   const KRank& R = A.r[0];
@@ -1500,8 +1501,10 @@ int mr_grid(int device) {
   if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
   int per = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, taccl_mr_kernel, 512, 0) != cudaSuccess || per < 1) per = 1;
-  const char* e = getenv("TACCL_MR_CTAS_PER_SM");  // knob for measurements (default 2)
-  const int want = e && atoi(e) > 0 ? atoi(e) : 2;
+  // one CTA per SM measured best (profiles/r02_nvls_lean_scan_n4.txt: 64 MiB 170.6 us at 1,
+  // 182 at 2-4; 1 MiB 24.3 vs 31.7); TACCL_MR_CTAS_PER_SM overrides
+  const char* e = getenv("TACCL_MR_CTAS_PER_SM");
+  const int want = e && atoi(e) > 0 ? atoi(e) : 1;
   return sms * std::min(per, want);
 }
 
