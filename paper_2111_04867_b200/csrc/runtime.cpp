@@ -279,14 +279,18 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   }
   if (forced) {
     lanes = (int)forced;
+    G->split = a->instances * lanes;
   } else {
-    // pieces = CTAs of each dependent tb, each piece >= min_piece
-    const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes / a->instances;
-    const int64_t by_bytes = std::max<int64_t>(1, step_bytes / min_piece);
-    const int by_ctas = std::max(1, per_dep / a->instances);
-    lanes = (int)std::max<int64_t>(1, std::min<int64_t>({by_bytes, (int64_t)by_ctas, (int64_t)(kMaxSplit / a->instances)}));
+    // pieces = CTAs of each dependent tb, each piece >= min_piece. The schedule's instances
+    // (subchunks that follow the parent's path, run in parallel to fill a
+    // link) set the MINIMUM piece count: the executor's pieces are already parallel lanes, so
+    // when CTAs and bytes allow more pieces than m, m adds nothing (a multiple-of-m split
+    // only cost CTAs: A2A n=4 1 GiB m=8 1284 vs 1197 us, profiles/r02_c3_grid_n4.txt)
+    const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes;
+    const int64_t natural = std::max<int64_t>(1, std::min<int64_t>({step_bytes / min_piece, (int64_t)per_dep, (int64_t)kMaxSplit}));
+    G->split = (int)std::min<int64_t>(kMaxSplit, std::max<int64_t>(a->instances, natural));
+    lanes = (G->split + a->instances - 1) / a->instances;
   }
-  G->split = a->instances * lanes;
   // stripes: a power of two (<= TACCL_STRIPE, default 64 KiB) that also divides the chunk
   // when possible, so every stripe starts cache-line / page aligned
   int64_t gb = elt;
