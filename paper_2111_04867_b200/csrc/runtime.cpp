@@ -287,7 +287,8 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
     // when CTAs and bytes allow more pieces than m, m adds nothing (a multiple-of-m split
     // only cost CTAs: A2A n=4 1 GiB m=8 1284 vs 1197 us, profiles/r02_c3_grid_n4.txt)
     const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes;
-    const int64_t natural = std::max<int64_t>(1, std::min<int64_t>({step_bytes / min_piece, (int64_t)per_dep, (int64_t)kMaxSplit}));
+    const int64_t ppc = std::max<int64_t>(1, (int64_t)env_size("TACCL_PIECES_PER_CTA", 1));  // A/B knob
+    const int64_t natural = std::max<int64_t>(1, std::min<int64_t>({step_bytes / min_piece, (int64_t)per_dep * ppc, (int64_t)kMaxSplit}));
     G->split = (int)std::min<int64_t>(kMaxSplit, std::max<int64_t>(a->instances, natural));
     lanes = (G->split + a->instances - 1) / a->instances;
   }
