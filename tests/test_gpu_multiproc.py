@@ -366,3 +366,54 @@ def test_multicast_reduce_parity(n, lean):
     for rank, results, err in sorted(res, key=lambda x: x[0]):
         assert err is None, f"rank {rank}: {err}"
         assert all(results), f"rank {rank}: {results}"
+
+
+def _mismatch_worker(rank, n, port, q):
+    import torch.distributed as dist
+    from paper_2111_04867_b200 import taccl
+    from paper_2111_04867_b200.generator import generate
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TACCL_TIMEOUT_S="2")
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    try:
+        comm = taccl.Comm(rank=rank, nranks=n, device=rank, scratch_bytes=64 << 20)
+        comm.load(generate("reducescatter", "direct", n, 1, 1))
+        count = 3 << 20  # above the LL threshold: the zero-copy kernel, where pull mode applies
+        x = torch.ones(n * count, dtype=torch.bfloat16, device="cuda")
+        out = torch.empty(count, dtype=torch.bfloat16, device="cuda")
+        comm.register(out)
+        comm.register(x)
+        if rank == 0:  # registered input, out of place: pull mode
+            comm.run("reducescatter", out, x)
+        else:  # NCCL's in-place form: the input is copied privately, so this rank pushes
+            comm.run("reducescatter", x[rank * count:(rank + 1) * count], x)
+        torch.cuda.synchronize()
+        code = None
+        try:
+            comm.check()
+        except taccl.TacclError as e:
+            code = e.code
+        q.put((rank, code, None))
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pull_mode_disagreement_is_detected():
+    # one rank in pull mode, its peer not: the entry handshake carries the mode,
+    # the senders abort before moving data, taccl_check reports it — no silent corruption, no hang
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mismatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][2] is None and res[1][2] is None, res
+    assert res[0][1] == 1 and res[1][1] == 1, res  # INVALID_ARG naming the disagreement, both ranks
