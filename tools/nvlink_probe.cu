@@ -36,6 +36,26 @@ struct Dests {
   int c;          // destinations
 };
 
+// mixed: CTAs [0, g/2) push src -> peer dst, CTAs [g/2, g) pull peer src2 -> local dst2
+__global__ void __launch_bounds__(512) push_pull(int4* pdst, const int4* psrc, int4* ldst, const int4* rsrc, long long n16) {
+  const bool pull = blockIdx.x >= gridDim.x / 2;
+  const int b = pull ? blockIdx.x - gridDim.x / 2 : blockIdx.x;
+  const int nb = pull ? gridDim.x - gridDim.x / 2 : gridDim.x / 2;
+  int4* dst = pull ? ldst : pdst;
+  const int4* s = pull ? rsrc : psrc;
+  const long long nt = (long long)nb * blockDim.x;
+  constexpr int U = 8;
+  long long i = (long long)b * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * nt < n16; i += U * nt) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcg(s + i + u * nt);
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[i + u * nt] = v[u];
+  }
+  for (; i < n16; i += nt) dst[i] = __ldcg(s + i);
+}
+
 // CTA b streams to destination b % c (grid-stride over that destination's range): 8 vectors
 // in flight per thread, 16-byte loads and stores (the executor's copy loop)
 __global__ void __launch_bounds__(512) push_multi(Dests d, const int4* __restrict__ src) {
@@ -130,6 +150,33 @@ int main(int argc, char** argv) {
     printf("{\"probe\": \"direction\", \"ctas\": %d, \"bytes\": %lld, \"push_uni_GBps\": %.1f, "
            "\"pull_uni_GBps\": %.1f, \"push_bi_GBps\": %.1f, \"n_devices\": %d}\n",
            ctas, Vd, Vd / (uni / 1e3) / 1e9, Vd / (pull / 1e3) / 1e9, Vd / (bi / 1e3) / 1e9, ndev);
+    fflush(stdout);
+  }
+  // 1b. mixed: GPUs 0 and 1 each move V to the other, half pushed and half pulled, at once
+  for (int ctas : {148, 296}) {
+    const long long half = Vd / 2;
+    float worst = 0;
+    for (int w = 0; w < 2; ++w) {
+      for (int d = 0; d < 2; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
+      for (int d = 0; d < 2; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventRecord(e0[d], st[d]));
+        for (int r = 0; r < 5; ++r)  // push the first half into the peer, pull the peer's second half
+          push_pull<<<ctas, 512, 0, st[d]>>>((int4*)dst[1 - d], (const int4*)src[d], (int4*)(dst[d] + half),
+                                             (const int4*)(src[1 - d] + half), half / 16);
+        CK(cudaEventRecord(e1[d], st[d]));
+      }
+      worst = 0;
+      for (int d = 0; d < 2; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventSynchronize(e1[d]));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0[d], e1[d]));
+        worst = ms > worst ? ms : worst;
+      }
+    }
+    printf("{\"probe\": \"mixed\", \"ctas\": %d, \"bytes\": %lld, \"push_half_pull_half_bi_GBps\": %.1f}\n", ctas, Vd,
+           Vd / (worst / 5 / 1e3) / 1e9);
     fflush(stdout);
   }
   // 2. connection count at fixed volume per GPU, all GPUs exchanging at once
