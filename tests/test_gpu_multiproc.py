@@ -330,6 +330,20 @@ def _nvls_worker(rank, n, port, q, lean=True):
             else:  # integers wrap exactly; integer-valued floats: every partial sum is exact
                 ok = bool(np.array_equal(got, want))
             results.append(ok)
+        # ordinary schedules on pool tensors: peers reached through the pool's unicast mappings
+        for coll, algo in (("allgather", "ring"), ("alltoall", "direct"), ("reducescatter", "direct")):
+            comm.load(generate(coll, algo, n, 1, 1))
+            cnt = 3 << 18  # 0.75 Mi elements: the zero-copy kernel
+            e_in = n * cnt if coll in ("alltoall", "reducescatter") else cnt
+            e_out = cnt if coll == "reducescatter" else n * cnt
+            ins = [allreduce_input(e_in, "int32", "bits", 26, r) for r in range(n)]
+            xi = comm.pool_tensor(e_in, torch.int32)
+            xi.copy_(torch.from_numpy(ins[rank]))
+            xo = comm.pool_tensor(e_out, torch.int32)
+            comm.run(coll, xo, xi)
+            torch.cuda.synchronize()
+            comm.check()
+            results.append(bool(np.array_equal(xo.cpu().numpy(), oracle.expected_outputs(coll, ins, "int32")[rank])))
         # not in the pool -> the multicast algorithm is skipped, the direct one runs
         xs = torch.from_numpy(allreduce_input(n * 1024, "int32", "bits", 24, rank)).cuda()
         os_ = torch.empty_like(xs)
