@@ -64,9 +64,10 @@ def multicast_ranges(coll: str, n: int):
     form in the switch (scalar adds), so floats only."""
     if coll != "allreduce" or n < 4:
         return []
-    # n = 4 (profiles/r02_sweep_nvls_n4.txt): bf16 ahead of direct and NCCL from 16 MiB; fp32
-    # ahead until the relay-first ring takes over at 128 MiB
-    return [("nvls", 16 * MiB, INF, ("bfloat16",)), ("nvls", 16 * MiB, 128 * MiB, ("float32",))]
+    # n = 4 (profiles/r02_nvls_lean_scan_n4.txt, lean multicast kernel): ahead of direct from
+    # 4 MiB (4 MiB 31.8 vs 35.3 us, 8 MiB 41.9 vs 44.4, 64 MiB 170.6 vs 184); fp32 until the
+    # relay-first ring takes over at 128 MiB
+    return [("nvls", 4 * MiB, INF, ("bfloat16",)), ("nvls", 4 * MiB, 128 * MiB, ("float32",))]
 
 
 def default_schedules(coll: str, n: int, multicast: bool = True):
