@@ -137,9 +137,9 @@ bool send_fds(uint64_t peer_id, int rank, const int* fds, int nfd, std::string* 
 }
 
 bool recv_fds(int listener, int* rank, int* fds, int* nfd, std::string* err) {
-  int s = accept(listener, nullptr, nullptr);
+  int s = accept(listener, nullptr, nullptr);  // SO_RCVTIMEO: 60 s
   if (s < 0) {
-    *err = "accept() on the pool socket failed";
+    *err = "accept() on the pool socket failed or timed out (a peer did not send its handles)";
     return false;
   }
   int hdr[2] = {-1, 0};
@@ -225,6 +225,9 @@ bool pool_export(Pool& P, int rank, int nranks, int dev, size_t want, void* out,
     *err = "pool socket bind/listen failed";
     return false;
   }
+  // a peer that failed before sending its descriptors must not hang this rank forever
+  timeval tv{60, 0};
+  setsockopt(P.listener, SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof(tv));
   Blob b;
   memset(&b, 0, sizeof(b));
   b.magic = kMagicPool;
