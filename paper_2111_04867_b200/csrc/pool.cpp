@@ -157,6 +157,11 @@ bool recv_fds(int listener, int* rank, int* fds, int* nfd, std::string* err) {
     *err = "recvmsg(SCM_RIGHTS) failed";
     return false;
   }
+  const int got = (int)((c->cmsg_len - CMSG_LEN(0)) / sizeof(int));
+  if (hdr[1] < 1 || hdr[1] > 2 || got != hdr[1]) {
+    *err = "pool message carries an unexpected number of descriptors";
+    return false;
+  }
   *rank = hdr[0];
   *nfd = hdr[1];
   memcpy(fds, CMSG_DATA(c), hdr[1] * sizeof(int));
