@@ -46,6 +46,9 @@ e_out = n * count if a.coll in ("allgather", "alltoall") else count
 nl = n if emu else 1
 ins = [torch.ones(e_in, dtype=torch.bfloat16, device="cuda") for _ in range(nl)]
 outs = [torch.empty(e_out, dtype=torch.bfloat16, device="cuda") for _ in range(nl)]
+if not emu:  # registration is explicit and collective
+    comm.register(outs[0])
+    comm.register(ins[0])
 
 
 def call():
