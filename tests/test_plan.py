@@ -150,3 +150,46 @@ def test_ring_rs_middle_hops_move_fp32():
         assert sum(1 for x in ins if x["pf"] & P_IN) == 2  # 3 receive-reduces, the first is bf16
         assert all(x["pf"] & P_OUT for x in steps if x["op"] == "RRCS")
         assert not any(x["pf"] & P_KEEP for x in steps if x["op"] == "RRCS")
+
+
+PARTIAL_SCHEDS = [("allreduce", "ring", 4, 1, {}), ("allreduce", "ring", 8, 2, {}), ("allreduce", "direct", 4, 2, {}),
+                  ("allreduce", "oneshot", 4, 1, {}), ("allreduce", "greedy", 8, 1, {"policy": "uc-min"}),
+                  ("allreduce", "greedy", 4, 2, {"policy": "uc-max"}), ("allreduce", "milp", 4, 2, {}),
+                  ("reducescatter", "ring", 8, 1, {}), ("reducescatter", "greedy", 8, 2, {}),
+                  ("reducescatter", "milp", 8, 1, {"topology": "2x4", "size": 1 << 16}),
+                  ("allreduce", "ring", 4, 1, {"pair": "peer"})]
+
+
+@pytest.mark.parametrize("coll,algo,n,p,kw", PARTIAL_SCHEDS)
+def test_static_partial_flags_match_the_oracles_dynamic_rule(coll, algo, n, p, kw, monkeypatch):
+    # two independent implementations of reading R6: the plan's last-writer analysis (C++,
+    # static, per step) and the oracle's partials mode (Python, dynamic, per message). For
+    # every receive-reduce the oracle executes, the operands it read as fp32 partials must be
+    # exactly the ones the plan flags (P_SRC: local source; P_IN: the matched send's message)
+    import numpy as np
+    import oracle
+    from oracle import simulate
+    from paper_2111_04867_b200.inputs import allreduce_input
+    text = generate(coll, algo, n, p, 1, **kw)
+    seen = {}
+    orig = simulate._execute
+
+    def spy(prog_, graph, order, bufs, read, write, reduce, *rest):
+        def red(mine, got, where):
+            seen[where] = (mine.part is not None, got.part is not None)
+            return reduce(mine, got, where)
+        return orig(prog_, graph, order, bufs, read, write, red, *rest)
+    monkeypatch.setattr(simulate, "_execute", spy)
+    count = n * p * 3 if coll == "allreduce" else p * 3
+    e_in = n * count if coll == "reducescatter" else count
+    oracle.run(oracle.parse(text), [allreduce_input(e_in, "bfloat16", "uniform", 3, r) for r in range(n)], "bfloat16")
+    monkeypatch.setenv("TACCL_NO_FUSE", "1")  # the flags of the original steps, before fusions
+    monkeypatch.setenv("TACCL_NO_RRCS", "1")
+    assert seen
+    for r in range(n):
+        for t, tb in enumerate(plan(text, r)):
+            for k, x in enumerate(tb["steps"]):
+                if x["op"] != "RRC":
+                    continue
+                src32, in32 = seen[(r, t, k)]
+                assert bool(x["pf"] & P_SRC) == src32 and bool(x["pf"] & P_IN) == in32, (r, t, k, x["pf"], seen[(r, t, k)])
