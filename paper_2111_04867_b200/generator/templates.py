@@ -176,6 +176,14 @@ def nvls_text(coll, n, p=1, instances=1, min_bytes=0, max_bytes=float("inf"), dt
     return "\n".join(out) + "\n"
 
 
+def direct_ring_allreduce(n, p=1):
+    """All-pairs reduce-scatter (every partial sum travels one hop: no fp32 partial hops for
+    bf16, reading R6) followed by a ring Allgather (one connection per GPU: the connection-count
+    sweep measured 10% more per-GPU egress over one connection than over three at n=4,
+    profiles/r02_nvlink_probe.jsonl) — PAPER.md:728's combination with mixed templates."""
+    return allreduce(invert_allgather(direct_allgather(n, p)), ring_allgather(n, p), f"ar_direct_ring_n{n}_p{p}")
+
+
 # ------------------------------------------------------------------------------ registry
 
 TEMPLATES = {
@@ -184,6 +192,7 @@ TEMPLATES = {
     ("alltoall", "direct"): direct_alltoall,
     ("allreduce", "ring"): ring_allreduce,
     ("allreduce", "direct"): direct_allreduce,
+    ("allreduce", "direct_ring"): direct_ring_allreduce,
     ("allreduce", "oneshot"): oneshot_allreduce,
     ("reducescatter", "ring"): ring_reducescatter,
     ("reducescatter", "direct"): direct_reducescatter,
