@@ -180,7 +180,7 @@ def direct_ring_allreduce(n, p=1):
     """All-pairs reduce-scatter (every partial sum travels one hop: no fp32 partial hops for
     bf16, reading R6) followed by a ring Allgather (one connection per GPU: the connection-count
     sweep measured 10% more per-GPU egress over one connection than over three at n=4,
-    profiles/r02_nvlink_probe.jsonl) — PAPER.md:728's combination with mixed templates."""
+    profiles/r02_nvlink_probe.jsonl) — PAPER.md:728's combination with mixed templates. Registered as "dring"."""
     return allreduce(invert_allgather(direct_allgather(n, p)), ring_allgather(n, p), f"ar_direct_ring_n{n}_p{p}")
 
 
@@ -192,7 +192,7 @@ TEMPLATES = {
     ("alltoall", "direct"): direct_alltoall,
     ("allreduce", "ring"): ring_allreduce,
     ("allreduce", "direct"): direct_allreduce,
-    ("allreduce", "direct_ring"): direct_ring_allreduce,
+    ("allreduce", "dring"): direct_ring_allreduce,
     ("allreduce", "oneshot"): oneshot_allreduce,
     ("reducescatter", "ring"): ring_reducescatter,
     ("reducescatter", "direct"): direct_reducescatter,
