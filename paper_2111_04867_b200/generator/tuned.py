@@ -43,7 +43,9 @@ def ranges(coll: str, n: int):
         # relay-first ring (one recv-reduce-copy-send pass per hop) is ahead from 128 MiB
         # (profiles/r02_sweep_n4_fp32_ar.txt: 128 MiB 329 vs 350 us, 1 GiB 2436 vs 2676; ring_p2
         # 2493)
-        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("direct", 128 * MiB, INF, BF16),
+        # bf16 from 128 MiB: all-pairs RS + ring AG ("dring": one AG connection per GPU) edges
+        # out direct (profiles/r02_ar_dring_n4.txt: 512 MiB 1277 vs 1296 us, 1 GiB 2499 vs 2560)
+        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("dring", 128 * MiB, INF, BF16),
                 ("ring", 128 * MiB, INF, WIDE)]
     if coll == "reducescatter":
         if n == 2 or n >= 8:
