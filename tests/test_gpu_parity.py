@@ -204,6 +204,7 @@ AR = [
     ("ring", 2, 1, 1), ("ring", 4, 2, 2), ("ring", 8, 1, 4),
     ("direct", 2, 1, 1), ("direct", 4, 1, 2), ("direct", 8, 2, 1), ("direct", 8, 1, 8),
     ("oneshot", 2, 1, 1), ("oneshot", 4, 2, 1), ("oneshot", 8, 1, 2),
+    ("dring", 4, 1, 1), ("dring", 8, 2, 2),
 ]
 
 
@@ -282,6 +283,7 @@ def test_bf16_tolerance_uniform(coll, algo, n, p, kw, mode):
 
 
 BF16_EXACT_SCHEDS = BF16_TOL_SCHEDS + [("allreduce", "ring", 4, 2, {"m": 2}), ("allreduce", "milp", 4, 2, {}),
+                                       ("allreduce", "dring", 4, 1, {}),
                                        ("reducescatter", "direct", 8, 1, {}), ("reducescatter", "ring", 4, 2, {"m": 2})]
 
 
