@@ -184,7 +184,9 @@ int main(int argc, char** argv) {
   for (int d = 0; d < ndev; ++d) all.push_back(d);
   for (long long V = 1ll << 20; V <= maxV; V <<= 2) {
     for (int c = 1; c < ndev; ++c) {
-      const int ctas = sms;  // one CTA per SM, split among the c connections
+      // one CTA per SM, split among the c connections (NVLINK_PROBE_CTAS_PER_SM overrides)
+      const char* cps = getenv("NVLINK_PROBE_CTAS_PER_SM");
+      const int ctas = sms * (cps && atoi(cps) > 0 ? atoi(cps) : 1);
       const int reps = V >= (256ll << 20) ? 5 : 50;
       const float ms = run(all, c, V, ctas, false, reps);
       const double moved = (double)(V / c / 16 * 16) * c;
