@@ -172,6 +172,8 @@ class Comm:
         if self.emulated or self.nranks == 1:
             return
         ptr, nbytes = t.untyped_storage().data_ptr(), t.untyped_storage().nbytes()
+        if self._in_pool(ptr, nbytes):  # pool tensors are mapped on every rank already
+            return
         blob = ctypes.create_string_buffer(HANDLE_BYTES)
         n = ctypes.c_size_t(0)
         _check(lib().taccl_buffer_export(ctypes.c_void_p(ptr), nbytes, blob, ctypes.byref(n)))
@@ -195,6 +197,7 @@ class Comm:
         self._barrier()  # every device added to the multicast object before anyone binds
         base, size = ctypes.c_void_p(), ctypes.c_size_t()
         _check(lib().taccl_pool_bind(ctypes.byref(base), ctypes.byref(size)))
+        self._pool = (base.value, size.value)
         self._barrier()  # flags cleared everywhere before any collective uses them
         return size.value
 
@@ -214,9 +217,15 @@ class Comm:
         import torch.distributed as dist
         dist.barrier(group=self.group)
 
+    def _in_pool(self, ptr, nbytes):
+        base, size = getattr(self, "_pool", (0, 0))
+        return base <= ptr and ptr + nbytes <= base + size
+
     def unregister(self, t):
         """Local: forget the mapping of `t`'s storage (call before the tensor is freed)."""
         if self.emulated or self.nranks == 1:
+            return
+        if self._in_pool(t.untyped_storage().data_ptr(), t.untyped_storage().nbytes()):
             return
         _check(lib().taccl_unregister_buffer(ctypes.c_void_p(t.untyped_storage().data_ptr())))
 

@@ -340,6 +340,7 @@ def _nvls_worker(rank, n, port, q, lean=True):
             xi = comm.pool_tensor(e_in, torch.int32)
             xi.copy_(torch.from_numpy(ins[rank]))
             xo = comm.pool_tensor(e_out, torch.int32)
+            comm.register(xo)  # a no-op for pool tensors (every rank maps the pool already)
             comm.run(coll, xo, xi)
             torch.cuda.synchronize()
             comm.check()
