@@ -171,7 +171,10 @@ taccl_result_t taccl_unregister_buffer(const void* ptr);
  *      range. Every rank must then pass a host barrier before any collective uses the pool.
  * taccl_pool_alloc: symmetric bump allocation (call in the same order with the same sizes on
  * every rank; 4 KiB aligned). A taccl_run whose sendbuf and recvbuf both lie in the pool may
- * select multicast-reduce algorithms (EF step `mr`); other calls skip them.
+ * select multicast-reduce algorithms (EF step `mr`); other calls skip them. The choice is
+ * local, so every rank of a call must agree: either all ranks' buffers lie in the pool at the
+ * same offsets (the symmetric allocation order above gives that) or none does. A disagreement
+ * is not detected before data moves; it surfaces as TIMEOUT from taccl_check.
  * Errors: NOT_INITIALIZED (no multi-process communicator / wrong phase order), UNSUPPORTED (no
  * multicast support), CUDA (driver calls, descriptor exchange), INVALID_ARG (pool exhausted).
  * The pool lives until taccl_comm_destroy. */
