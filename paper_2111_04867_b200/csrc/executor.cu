@@ -84,6 +84,33 @@ __device__ bool wait_ge(const u64* p, u64 target, u64 timeout_ns) {
   }
 }
 
+// streamed messages (KStep.prog): the sender publishes, after every group of KArgs.prog stripes
+// of its piece, word = key << 20 | groups done, key = (epoch mod 2^20) << 24 | (seq + 1). A
+// later key on the slot (the sender's next message, or a later call) means "all of it" —
+// compared modulo 2^44, so the epoch may wrap. Groups stay far below 2^20 (a piece's stripes
+// are >= 4 KiB apart except for small chunks).
+__device__ __forceinline__ u64 prog_key(u64 epoch, int seq) { return ((epoch & 0xFFFFF) << 24) | (u64)(seq + 1); }
+__device__ __forceinline__ bool prog_reached(u64 v, u64 key, int64_t groups) {
+  const int64_t d = (int64_t)(((v >> 20) - key) << 20) >> 20;
+  return d > 0 || (d == 0 && (int64_t)(v & 0xFFFFF) >= groups);
+}
+__device__ bool wait_prog(const u64* p, u64 key, int64_t groups, u64 timeout_ns) {
+  if (prog_reached(ld_acquire_sys(p), key, groups)) return true;
+  const u64 t0 = globaltimer();
+  for (;;) {
+#pragma unroll 1
+    for (int i = 0; i < 256; ++i)
+      if (prog_reached(ld_acquire_sys(p), key, groups)) return true;
+    if (globaltimer() - t0 > timeout_ns) return false;
+  }
+}
+// one thread, after a bar.sync that follows the CTA's stores of the group (causality order;
+// the system-scope fence makes them visible before the word, as for data flags)
+__device__ __forceinline__ void prog_publish(u64* slot, u64 key, int64_t groups) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  st_relaxed_sys(slot, (key << 20) | (u64)groups);
+}
+
 // ---------------------------------------------------------------- CTA-wide data movement
 __device__ __forceinline__ void st_v4_cs(int4* p, int4 v) {
   asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -943,6 +970,74 @@ __device__ __forceinline__ bool pulled(const KArgs& A, const KStep& st) {
   return A.pull && st.op == K_SEND && st.poff >= 0;
 }
 
+// Direct kernel, streamed messages (KStep.prog, plan.cpp mark_streamed): a K_SEND publishes
+// its progress every A.prog stripes; a K_RRC / K_RRC_FUSED member waits, before each group of
+// A.prog stripes, until every input message published that group, then reduces it. Out of line
+// (called once per step and piece) so the stripe loops do not add to the kernel's registers.
+// Returns false after a timeout (recorded; *abort set for the CTA).
+__device__ __forceinline__ bool streamed_step(const Ctx& c, const KStep& st, int k, const KTB* tbs, const int* fused,
+                                           const KTB& tb, int64_t stripe, int nsplit, int64_t cbytes, char* dst,
+                                           const char* src, char* const* s_fwd, const char* const* s_stage,
+                                           volatile int* abort) {
+  const KArgs& A = *c.a;
+  const KRank& R = *c.r;
+  const int j = c.j, tid = threadIdx.x, G = A.prog;
+  int64_t ns = 0;
+  if (st.op == K_SEND) {
+    u64* slot = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffProg) + flag_slot(R.rank, tb.chan, j);
+    const u64 key = prog_key(c.epoch, st.seq);
+    for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+      cta_copy(A.variant, dst + off, src + off, len);
+      if (++ns % G == 0) {
+        __syncthreads();
+        if (tid == 0) prog_publish(slot, key, ns / G);
+      }
+    });
+    if (ns % G) {
+      __syncthreads();
+      if (tid == 0) prog_publish(slot, key, ns / G + 1);
+    }
+    return true;
+  }
+  const u64* my_prog = reinterpret_cast<const u64*>(R.arena + kOffProg);
+  const bool fz = st.op == K_RRC_FUSED;
+  const int64_t unit = (cbytes % 16 == 0) ? 16 : A.elt;
+  for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
+    if (*abort) return;
+    if (ns % G == 0) {  // group ns / G: every input message published it
+      if (tid == 0) {
+        const int nin = fz ? st.fuse_count : 1;
+        for (int f = 0; f < nin && !*abort; ++f) {
+          int peer = tb.recv, chan = tb.chan, seq = st.seq;
+          if (fz) {
+            const int* e = fused + kFuseStride * (st.fuse_begin + f);
+            peer = tbs[e[0]].recv;
+            chan = tbs[e[0]].chan;
+            seq = e[1];
+          }
+          if (!wait_prog(my_prog + flag_slot(peer, chan, j), prog_key(c.epoch, seq), ns / G + 1, A.timeout_ns)) {
+            record_error(c, st.op, k);
+            *abort = 1;
+          }
+        }
+      }
+      __syncthreads();
+      if (*abort) return;
+    }
+    ++ns;
+    if (!fz) {
+      reduce_dispatch(A.dtype, dst + off, s_fwd, 0, src + off, s_stage, 1, off, len / A.elt);
+      return;
+    }
+    // this member's portion of the range (16-byte aligned cuts), as the unstreamed path
+    const int64_t nu = len / unit;
+    const int64_t a = off + nu * st.part / st.nparts * unit;
+    const int64_t b = (st.part + 1 == st.nparts) ? off + len : off + nu * (st.part + 1) / st.nparts * unit;
+    if (b > a) reduce_dispatch(A.dtype, dst + a, s_fwd, st.fwd_count, src + a, s_stage, st.fuse_count, a, (b - a) / A.elt);
+  });
+  return !*abort;
+}
+
 // Direct kernel, bf16 partials (reading R6): one step whose operands may be fp32 — a send of
 // a source's fp32 shadow into the receiver's (2x) staging slot (P_OUT), or a receive-reduce
 // (K_RRC, K_RRCS, a fused chain member's portion) through cta_reduce_px (out of line). Inlined
@@ -1195,13 +1290,16 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           sender_ready = true;
         }
         // staged (LL) mode: no data flags, every line carries its own (ll_lines)
-        if (ok && !LL && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RCS))
+        // (a streamed rrc waits per stripe group instead, in its data loop)
+        if (ok && !LL && (st.op == K_RECV || st.op == K_RRC || st.op == K_RRCS || st.op == K_RCS) &&
+            !(st.op == K_RRC && A.prog && st.prog))
           ok = wait_ge<true>(my_data + flag_slot(tb.recv, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns);
         if (ok && st.op == K_RRC_FUSED) {  // every chain member's input, chain order
           for (int f = 0; f < st.fuse_count && ok; ++f) {
             const int* fz = fused + kFuseStride * (st.fuse_begin + f);
             const KTB o = tbs[fz[0]];
-            if (!LL) ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
+            if (!LL && !(A.prog && st.prog))
+              ok = wait_ge<true>(my_data + flag_slot(o.recv, o.chan, j), E | (u64)(fz[1] + 1), A.timeout_ns);
             s_stage[f] = LL ? my_staged + (int64_t)fz[3] * ll_cb
                        : (A.pull && fz[4] >= 0) ? R.peer_in[o.recv] + (int64_t)fz[4] * cbytes  // pull: in place
                                                  : local_base(c, KB_STAGE) + (int64_t)fz[2] * cbytes;
@@ -1270,6 +1368,8 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
               for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { tma_push(tp, dst + off, src + off, len); });
               tma_finish(tp);
             }
+          } else if (st.op == K_SEND && A.prog && st.prog) {  // streamed: publish every A.prog stripes
+            streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort);
           } else {
             for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           }
@@ -1284,6 +1384,10 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
             px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
             break;
           }
+          if (A.prog && st.prog) {  // streamed: reduce each stripe group once it landed
+            if (!streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort)) return;
+            break;
+          }
           for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) {
             reduce_dispatch(A.dtype, dst + off, s_fwd, nfwd, src + off, s_stage, 1, off, len / elt);
           });
@@ -1294,6 +1398,10 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           char* dst = local_base(c, st.dstbuf) + (int64_t)st.dstoff * cbytes;
           if (st.pflags && A.dtype == TACCL_BFLOAT16) {  // bf16 partials (reading R6)
             px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
+            break;
+          }
+          if (A.prog && st.prog) {  // streamed: reduce each stripe group once every member's landed
+            if (!streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort)) return;
             break;
           }
           const int64_t unit = (cbytes % 16 == 0) ? 16 : elt;
@@ -1364,7 +1472,8 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           // all threads' peer stores are ordered before this by bar.sync (causality order);
           // the system-scope acq_rel fence makes them visible before the flag (cumulativity;
           // K_PUB: the chain members' stores, ordered by their fence + our acquire of done)
-          if (!PROBE(9)) asm volatile("fence.acq_rel.sys;" ::: "memory");  // 9: timing probe only
+          // (a streamed send's last progress word already fenced its stores)
+          if (!PROBE(9) && !(st.op == K_SEND && A.prog && st.prog)) asm volatile("fence.acq_rel.sys;" ::: "memory");
           u64* data = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffData);
           st_relaxed_sys(data + flag_slot(R.rank, tb.chan, j),
                          E | (u64)((st.op == K_RRCS || st.op == K_RCS ? st.fwd_seq : st.seq) + 1));

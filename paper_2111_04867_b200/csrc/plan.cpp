@@ -285,6 +285,74 @@ std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map
   return fl;
 }
 
+// Streamed messages (direct kernel; DESIGN.md §6 "streamed reduces"): a receive-reduce that
+// would otherwise wait for its whole piece before reducing it — all its input messages land
+// while its CTA idles — instead reduces each group of stripes as soon as every input message
+// published that group, so the reduce overlaps the transfers and only the last group is left
+// after them. Marked per receive-reduce (a fused chain as a whole) when (1) no member carries
+// bf16 partials (the partials path moves other bytes per stripe), (2) every input message is
+// sent by a plain K_SEND (not a forward fused into K_RRCS, a chain's K_PUB or a K_RCS relay) and
+// (3) every member is the first step of its threadblock doing data work: a CTA that sends first
+// reaches the reduce when its peers' messages have landed too (paired send+rrc tbs) and the
+// progress stores would be pure cost. Both ends get KStep.prog; the kernel streams only when
+// KArgs.prog (the runtime turns it off in pull mode and for TMA pushes).
+void mark_streamed(std::vector<RankPlan>& plans) {
+  const int n = (int)plans.size();
+  auto first_data = [](const RankPlan& rp, const KTB& kt, int k) {
+    for (int q = 0; q < k; ++q)
+      if (rp.steps[kt.step_begin + q].op != K_NOP) return false;
+    return true;
+  };
+  // the K_SEND on rank q that carries message `seq` of connection (q -> r, chan), or null
+  auto sender = [&](int q, int r, int chan, int seq) -> KStep* {
+    if (q < 0 || q >= n) return nullptr;
+    for (const KTB& pt : plans[q].tbs) {
+      if (pt.send != r || pt.chan != chan) continue;
+      for (int k = 0; k < pt.nsteps; ++k) {
+        KStep& y = plans[q].steps[pt.step_begin + k];
+        if (y.op == K_SEND && y.seq == seq) return &y;
+      }
+    }
+    return nullptr;
+  };
+  for (int r = 0; r < n; ++r) {
+    RankPlan& rp = plans[r];
+    for (int t = 0; t < (int)rp.tbs.size(); ++t) {
+      const KTB& kt = rp.tbs[t];
+      for (int k = 0; k < kt.nsteps; ++k) {
+        KStep& x = rp.steps[kt.step_begin + k];
+        if (x.op == K_RRC) {
+          KStep* s = sender(kt.recv, r, kt.chan, x.seq);
+          if (x.pflags || !s || s->pflags || !first_data(rp, kt, k)) continue;
+          x.prog = s->prog = 1;
+        } else if (x.op == K_RRC_FUSED && x.part == 0) {
+          // the chain's members: the steps sharing its fused entries, one per member tb
+          std::vector<KStep*> members;
+          bool ok = true;
+          for (int t2 = 0; t2 < (int)rp.tbs.size() && ok; ++t2)
+            for (int k2 = 0; k2 < rp.tbs[t2].nsteps; ++k2) {
+              KStep& y = rp.steps[rp.tbs[t2].step_begin + k2];
+              if (y.op != K_RRC_FUSED || y.fuse_begin != x.fuse_begin) continue;
+              ok = ok && !y.pflags && first_data(rp, rp.tbs[t2], k2);
+              members.push_back(&y);
+            }
+          std::vector<KStep*> sends;
+          for (int f = 0; f < x.fuse_count && ok; ++f) {
+            const int* fz = rp.fused.data() + kFuseStride * (x.fuse_begin + f);
+            const KTB& o = rp.tbs[fz[0]];
+            KStep* s = sender(o.recv, r, o.chan, fz[1]);
+            ok = s && !s->pflags && !fz[5];
+            sends.push_back(s);
+          }
+          if (!ok) continue;
+          for (KStep* y : members) y->prog = 1;
+          for (KStep* y : sends) y->prog = 1;
+        }
+      }
+    }
+  }
+}
+
 std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends, int pull_kinds) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
@@ -597,6 +665,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
           }
         }
       }
+  mark_streamed(plans);
   return plans;
 }
 

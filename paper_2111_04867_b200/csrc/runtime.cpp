@@ -461,6 +461,10 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   // (only for plans with pulled steps: for the others the mode changes nothing, and a rank
   // running in place next to one that does not is legal)
   A.pull = (pull_on && (a->has_pull || pull_chains)) ? 1 : 0;
+  // streamed messages (plan.cpp mark_streamed): progress published every TACCL_PROG_STRIPES
+  // stripes (default 2; 0 = off, A/B knob — like every knob it must match on all ranks). Off in
+  // pull mode (nothing is pushed) and with TMA pushes (their stores complete asynchronously)
+  A.prog = (A.pull || A.tma == 2) ? 0 : (int)env_size("TACCL_PROG_STRIPES", 2);
   std::string err;
   const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -652,7 +656,7 @@ taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, c
              " deps=" + pairs(x.dep_begin, x.dep_count) + " post=" + pairs(x.post_begin, x.post_count) +
              " part=" + std::to_string(x.part) + "/" + std::to_string(x.nparts) +
              " fuse=" + std::to_string(x.op == K_RRC_FUSED ? x.fuse_count : 0) + " fwd=" + std::to_string(x.fwd_count) +
-             " pf=" + std::to_string(x.pflags) + "\n";
+             " pf=" + std::to_string(x.pflags) + (x.prog ? " prog" : "") + "\n";
       }
     }
   } catch (const SchedError& e) {

@@ -115,6 +115,9 @@ struct KStep {
                           // send's input offset (chunk units), else -1 (pull mode reads it in
                           // place); K_SEND: >= 0 iff its matched receive reads it in place
   int32_t pflags;         // bf16 partials (reading R6), bits P_*; bf16 calls only
+  int32_t prog;           // streamed message (direct kernel): K_SEND publishes its progress every
+                          // KArgs.prog stripes; K_RRC / K_RRC_FUSED reduce each stripe group as
+                          // soon as every input message published it (plan.cpp mark_streamed)
 };
 // bf16 partials: an rrc's result keeps its fp32 accumulator in the rank's shadow region (one
 // fp32 per element of o and s) when a later reduction reads it; such reads and the sends that
@@ -148,7 +151,9 @@ constexpr size_t kOffReady = kOffData + kFlagSlots * 8;          // u64[kFlagSlo
 constexpr size_t kOffDone = kOffReady + kFlagSlots * 8;          // u64[kMaxTB*kMaxSplit], local
 constexpr size_t kOffAck = kOffDone + (size_t)kMaxTB * kMaxSplit * 8;  // u64[kFlagSlots], pull mode:
                                                                   // written by readers of our input
-constexpr size_t kOffCtrl = kOffAck + kFlagSlots * 8;
+constexpr size_t kOffProg = kOffAck + kFlagSlots * 8;          // u64[kFlagSlots], written by senders
+                                                                  // of streamed messages (KStep.prog)
+constexpr size_t kOffCtrl = kOffProg + kFlagSlots * 8;
 constexpr size_t kCtrlBytes = 256;   // epoch (u64), finished (u32), error (u32), err detail
 constexpr size_t kOffScratch = (kOffCtrl + kCtrlBytes + 4095) & ~(size_t)4095;
 
@@ -225,6 +230,8 @@ struct KArgs {
   int32_t trace_ctas;         // CTAs that fit in the trace buffer
   int32_t ncta;               // grid size
   int32_t ready_per_piece;    // A/B knob (TACCL_READY_PER_PIECE): entry handshake per piece start
+  int32_t prog;               // streamed messages: stripes per published group (0 = off; every
+                              // rank of a call agrees: off in pull mode and with TMA pushes)
   int32_t pull;               // pull mode (direct kernel): a receive-reduce whose matched send
                               // reads the sender's input loads it from the peer (no push, no
                               // staging); the reader acks, the sender's CTAs wait for the acks

@@ -27,6 +27,8 @@ ap.add_argument("--chunks", type=int, default=1)
 ap.add_argument("--bytes", type=int, default=1024)
 ap.add_argument("--emulated", action="store_true")
 ap.add_argument("--calls", type=int, default=1, help="traced back-to-back calls (last one shown)")
+ap.add_argument("--pair", default="1", help="1 (default pairing), peer, or split (sends and receives in separate tbs)")
+ap.add_argument("--summary", action="store_true", help="per (rank, tb): median of every stamp instead of every CTA")
 a = ap.parse_args()
 world = int(os.environ.get("WORLD_SIZE", "1"))
 rank = int(os.environ.get("RANK", "0"))
@@ -36,7 +38,7 @@ if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
 emu = world == 1
 comm = taccl.Comm(rank=rank, nranks=n, device=torch.cuda.current_device(), emulated=emu, scratch_bytes=64 << 20)
-comm.load(generate(a.coll, a.algo, n, a.chunks, 1))
+comm.load(generate(a.coll, a.algo, n, a.chunks, 1, pair={"1": True, "peer": "peer", "split": False}[a.pair]))
 es = 2
 S = a.bytes
 count = {"allgather": S // es // n, "alltoall": S // es // n, "allreduce": S // es,
@@ -78,13 +80,26 @@ if world > 1:
     dist.all_gather_object(allT, T)
     T = torch.cat(allT)
 T = T[T[:, 0] > 0]
-t0 = int(T[:, 0].min())
+# %globaltimer is per GPU: stamps are shown relative to the earliest entry on the same rank
+ranks_of = (T[:, -2] >> 32)
+t0s = {int(r): int(T[ranks_of == r, 0].min()) for r in ranks_of.unique()}
 nsteps = (taccl.TRACE_SLOTS - 4) // 4
 if rank == 0:
     print(f"{a.coll} {a.algo} n={n} S={S} B plan={info} (us from the earliest entry)")
-    for row in T.tolist():
+    rows = T.tolist()
+    if a.summary:  # one line per (rank, tb): the median over its CTAs of every stamp
+        groups = {}
+        for row in rows:
+            groups.setdefault((row[-2] >> 32, (row[-2] >> 16) & 0xFFFF), []).append(row)
+        rows = []
+        for (r, tb), g in sorted(groups.items()):
+            med = torch.tensor(g, dtype=torch.float64).median(dim=0).values.long().tolist()
+            med[-2] = (r << 32) | (tb << 16) | 0xFFFF
+            rows.append(med)
+    for row in rows:
         ident = row[-2]
         r, tb, j = ident >> 32, (ident >> 16) & 0xFFFF, ident & 0xFFFF
+        t0 = t0s[r]
 
         def us(x):
             return f"{(x - t0) / 1e3:6.2f}" if x else "   -  "
@@ -94,7 +109,8 @@ if rank == 0:
             if not s0:
                 break
             steps.append(f"s{k}[{us(s0)} w{us(s1)}" + (f" x{us(s2)}" if s2 else "") + f" d{us(s3)}]")
-        print(f"r{r} tb{tb} j{j}: entry {us(row[0])} pro {us(row[1])} " + " ".join(steps) + f" exit {us(row[-1])}")
+        jj = "med" if j == 0xFFFF else f"j{j}"
+        print(f"r{r} tb{tb} {jj}: entry {us(row[0])} pro {us(row[1])} " + " ".join(steps) + f" exit {us(row[-1])}")
 comm.destroy()
 if world > 1:
     dist.destroy_process_group()
