@@ -1038,100 +1038,6 @@ __device__ __forceinline__ bool streamed_step(const Ctx& c, const KStep& st, int
   return !*abort;
 }
 
-// stripe s of piece j in a step of cnt chunks, in for_piece's order (co-scheduled pairs walk
-// two steps' stripes side by side; both ends of a message must count them the same way)
-__device__ __forceinline__ int64_t piece_nstripes(int64_t stripe, int j, int split, int cnt, int64_t cbytes) {
-  if (split == 1) return 1;
-  const int64_t nb = (cbytes + stripe - 1) / stripe;
-  return (j < nb ? (nb - j + split - 1) / split : 0) * cnt;
-}
-__device__ __forceinline__ int64_t piece_range(int64_t s, int64_t stripe, int j, int split, int cnt, int64_t cbytes,
-                                               int64_t* len) {
-  if (split == 1) {
-    *len = (int64_t)cnt * cbytes;
-    return 0;
-  }
-  const int64_t nb = (cbytes + stripe - 1) / stripe, per = (nb - j + split - 1) / split;
-  const int64_t b = j + (s % per) * split;
-  *len = min(stripe, cbytes - b * stripe);
-  return (s / per) * cbytes + b * stripe;
-}
-
-// Co-scheduled pair (KStep.prog == 2 on the receive-reduce): a streamed send and the streamed
-// receive-reduce after it in the same threadblock run group by group — send group g (publish
-// it), then reduce group g - 1 once every input message published it. The peers run the same
-// loop, so their group g - 1 has normally landed by then: the reduce overlaps the transfers
-// instead of following them. Returns false after a timeout (recorded; *abort set).
-__device__ __forceinline__ bool streamed_pair(const Ctx& c, const KStep& snd, const KStep& rrc, int k, const KTB* tbs,
-                                              const int* fused, const KTB& tb, int64_t stripe, int nsplit,
-                                              int64_t cbytes, char* sdst, const char* ssrc, char* const* s_fwd,
-                                              const char** s_stage, volatile int* abort) {
-  const KArgs& A = *c.a;
-  const KRank& R = *c.r;
-  const int j = c.j, tid = threadIdx.x, G = A.prog;
-  const bool fz = rrc.op == K_RRC_FUSED;
-  u64* slot = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffProg) + flag_slot(R.rank, tb.chan, j);
-  const u64 skey = prog_key(c.epoch, snd.seq);
-  const u64* my_prog = reinterpret_cast<const u64*>(R.arena + kOffProg);
-  const char* rsrc = local_base(c, rrc.srcbuf) + (int64_t)rrc.srcoff * cbytes;
-  char* rdst = local_base(c, rrc.dstbuf) + (int64_t)rrc.dstoff * cbytes;
-  if (tid == 0) {  // the receive-reduce's staging slots (push mode: streaming is off in pull mode)
-    if (fz)
-      for (int f = 0; f < rrc.fuse_count; ++f)
-        s_stage[f] = local_base(c, KB_STAGE) + (int64_t)fused[kFuseStride * (rrc.fuse_begin + f) + 2] * cbytes;
-    else
-      s_stage[0] = local_base(c, KB_STAGE) + (int64_t)rrc.soff * cbytes;
-  }
-  __syncthreads();
-  const int64_t ss = piece_nstripes(stripe, j, nsplit, snd.cnt, cbytes), sr = piece_nstripes(stripe, j, nsplit, rrc.cnt, cbytes);
-  const int64_t gs = (ss + G - 1) / G, gr = (sr + G - 1) / G;
-  const int64_t unit = (cbytes % 16 == 0) ? 16 : A.elt;
-  for (int64_t g = 0; g < gs || g <= gr; ++g) {
-    if (g < gs) {
-      for (int64_t q = g * G; q < min(ss, (g + 1) * G); ++q) {
-        int64_t len;
-        const int64_t off = piece_range(q, stripe, j, nsplit, snd.cnt, cbytes, &len);
-        cta_copy(A.variant, sdst + off, ssrc + off, len);
-      }
-      __syncthreads();
-      if (tid == 0) prog_publish(slot, skey, g + 1);
-    }
-    const int64_t h = g - 1;
-    if (h < 0 || h >= gr) continue;
-    if (tid == 0) {
-      const int nin = fz ? rrc.fuse_count : 1;
-      for (int f = 0; f < nin && !*abort; ++f) {
-        int peer = tb.recv, chan = tb.chan, seq = rrc.seq;
-        if (fz) {
-          const int* e = fused + kFuseStride * (rrc.fuse_begin + f);
-          peer = tbs[e[0]].recv;
-          chan = tbs[e[0]].chan;
-          seq = e[1];
-        }
-        if (!wait_prog(my_prog + flag_slot(peer, chan, j), prog_key(c.epoch, seq), h + 1, A.timeout_ns)) {
-          record_error(c, rrc.op, k + 1);
-          *abort = 1;
-        }
-      }
-    }
-    __syncthreads();
-    if (*abort) return false;
-    for (int64_t q = h * G; q < min(sr, (h + 1) * G); ++q) {
-      int64_t len;
-      const int64_t off = piece_range(q, stripe, j, nsplit, rrc.cnt, cbytes, &len);
-      if (!fz) {
-        reduce_dispatch(A.dtype, rdst + off, s_fwd, 0, rsrc + off, s_stage, 1, off, len / A.elt);
-        continue;
-      }
-      const int64_t nu = len / unit;
-      const int64_t a = off + nu * rrc.part / rrc.nparts * unit;
-      const int64_t b = (rrc.part + 1 == rrc.nparts) ? off + len : off + nu * (rrc.part + 1) / rrc.nparts * unit;
-      if (b > a) reduce_dispatch(A.dtype, rdst + a, s_fwd, 0, rsrc + a, s_stage, rrc.fuse_count, a, (b - a) / A.elt);
-    }
-  }
-  return true;
-}
-
 // Direct kernel, bf16 partials (reading R6): one step whose operands may be fp32 — a send of
 // a source's fp32 shadow into the receiver's (2x) staging slot (P_OUT), or a receive-reduce
 // (K_RRC, K_RRCS, a fused chain member's portion) through cta_reduce_px (out of line). Inlined
@@ -1463,13 +1369,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
               tma_finish(tp);
             }
           } else if (st.op == K_SEND && A.prog && st.prog) {  // streamed: publish every A.prog stripes
-            if (k + 1 < tb.nsteps && steps[tb.step_begin + k + 1].prog == 2) {  // with the next rrc
-              if (!streamed_pair(c, st, steps[tb.step_begin + k + 1], k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src,
-                                 s_fwd, s_stage, &s_abort))
-                return;
-            } else {
-              streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort);
-            }
+            streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort);
           } else {
             for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           }
@@ -1484,7 +1384,6 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
             px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
             break;
           }
-          if (A.prog && st.prog == 2) break;  // reduced with the send before it (streamed_pair)
           if (A.prog && st.prog) {  // streamed: reduce each stripe group once it landed
             if (!streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort)) return;
             break;
@@ -1501,7 +1400,6 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
             px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
             break;
           }
-          if (A.prog && st.prog == 2) break;  // reduced with the send before it (streamed_pair)
           if (A.prog && st.prog) {  // streamed: reduce each stripe group once every member's landed
             if (!streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort)) return;
             break;

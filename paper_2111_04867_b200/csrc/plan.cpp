@@ -292,24 +292,16 @@ std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map
 // after them. Marked per receive-reduce (a fused chain as a whole) when (1) no member carries
 // bf16 partials (the partials path moves other bytes per stripe), (2) every input message is
 // sent by a plain K_SEND (not a forward fused into K_RRCS, a chain's K_PUB or a K_RCS relay) and
-// (3) every member is its threadblock's first step doing data work, or follows exactly one
-// send with no dependencies of its own (paired send + rrc threadblocks, as the direct
-// schedules lower). Both ends get KStep.prog = 1; the kernel streams only when KArgs.prog (the
-// runtime turns it off in pull mode and for TMA pushes). A member right after a streamed send
-// gets prog = 2: the kernel runs the two together, group by group — send group g, then reduce
-// group g - 1, whose peers' groups have landed meanwhile — instead of the whole send, then
-// the whole reduce (its destination must not overlap the send's source).
+// (3) every member is the first step of its threadblock doing data work: a CTA that sends first
+// reaches the reduce when its peers' messages have landed too (paired send+rrc tbs) and the
+// progress stores would be pure cost. Both ends get KStep.prog; the kernel streams only when
+// KArgs.prog (the runtime turns it off in pull mode and for TMA pushes).
 void mark_streamed(std::vector<RankPlan>& plans) {
   const int n = (int)plans.size();
   auto first_data = [](const RankPlan& rp, const KTB& kt, int k) {
-    int sends = 0;
-    for (int q = 0; q < k; ++q) {
-      const KStep& y = rp.steps[kt.step_begin + q];
-      if (y.op == K_NOP) continue;
-      if (q + 1 != k || y.op != K_SEND || y.dep_count || y.post_count) return false;
-      ++sends;
-    }
-    return sends <= 1;
+    for (int q = 0; q < k; ++q)
+      if (rp.steps[kt.step_begin + q].op != K_NOP) return false;
+    return true;
   };
   // the K_SEND on rank q that carries message `seq` of connection (q -> r, chan), or null
   auto sender = [&](int q, int r, int chan, int seq) -> KStep* {
@@ -359,16 +351,6 @@ void mark_streamed(std::vector<RankPlan>& plans) {
       }
     }
   }
-  // co-scheduled pairs: a streamed receive-reduce right after a streamed send of its tb
-  for (RankPlan& rp : plans)
-    for (const KTB& kt : rp.tbs)
-      for (int k = 1; k < kt.nsteps; ++k) {
-        KStep& x = rp.steps[kt.step_begin + k];
-        const KStep& s = rp.steps[kt.step_begin + k - 1];
-        if (!x.prog || s.op != K_SEND || !s.prog || x.dep_count || (x.op == K_RRC_FUSED && x.fwd_count)) continue;
-        const bool overlap = x.dstbuf == s.srcbuf && x.dstoff < s.srcoff + s.cnt && s.srcoff < x.dstoff + x.cnt;
-        if (!overlap) x.prog = 2;
-      }
 }
 
 std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends, int pull_kinds) {

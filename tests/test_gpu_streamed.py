@@ -45,13 +45,10 @@ KNOBS = [{"TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "4096"},
 @pytest.mark.parametrize("coll,algo,n,p", SCHEDS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
 @pytest.mark.parametrize("knob", range(len(KNOBS)))
-@pytest.mark.parametrize("pair", [False, True])
-def test_streamed_schedules_exact(coll, algo, n, p, dtype, knob, pair):
-    # pair=False: sends and receive-reduces in separate tbs (streamed reduces); True: the default
-    # paired lowering (send + receive-reduce run together, prog 2 — except AR n=2's rrc+send)
-    text = generate(coll, algo, n, p, 1, pair=pair)
-    if algo == "direct" and not (pair and coll == "allreduce" and n == 2):
-        assert (" prog2" if pair else " prog") in taccl.plan_dump(text, 0)
+def test_streamed_split_schedules_exact(coll, algo, n, p, dtype, knob):
+    text = generate(coll, algo, n, p, 1, pair=False)
+    if algo == "direct":  # the split direct schedules stream every reduce
+        assert " prog" in taccl.plan_dump(text, 0)
     # chunks of 50-70 KiB: 13-18 stripes of 4 KiB, a ragged last stripe, several groups per piece
     c_e = 12289 if dtype == "bfloat16" else 6151
     count = p * c_e * (n if coll == "allreduce" else 1)
@@ -66,11 +63,10 @@ def test_streamed_schedules_exact(coll, algo, n, p, dtype, knob, pair):
 
 @pytest.mark.parametrize("coll,n", [("reducescatter", 4), ("allreduce", 4), ("reducescatter", 8)])
 @pytest.mark.parametrize("kind", ["uniform", "normal"])
-@pytest.mark.parametrize("pair", [False, True])
-def test_streamed_bf16_fused_rounding_bit_exact(coll, n, kind, pair):
+def test_streamed_bf16_fused_rounding_bit_exact(coll, n, kind):
     # non-integer bf16: the fused chain's fp32 sum in chain order, rounded once (reading R3), is
     # the same whether the stripes are reduced as they land or after the whole message
-    text = generate(coll, "direct", n, 1, 1, pair=pair)
+    text = generate(coll, "direct", n, 1, 1, pair=False)
     count = 40000 if coll == "allreduce" else 10000
     e_in = n * count if coll == "reducescatter" else count
     ins = [allreduce_input(e_in, "bfloat16", kind, 33, r) for r in range(n)]
@@ -78,12 +74,11 @@ def test_streamed_bf16_fused_rounding_bit_exact(coll, n, kind, pair):
     assert_bits_equal(got, oracle.run(oracle.parse(text), ins, "bfloat16"))
 
 
-@pytest.mark.parametrize("pair", [False, True])
-def test_streamed_repeated_calls_and_epochs(pair):
+def test_streamed_repeated_calls_and_epochs():
     # progress words are keyed by (epoch, message): back-to-back calls on the same slots must
     # never take an earlier call's word for this one's
     n, count = 4, 4 * 24593
-    text = generate("allreduce", "direct", n, 1, 1, pair=pair)
+    text = generate("allreduce", "direct", n, 1, 1, pair=False)
     os.environ.update({"TACCL_PULL": "0", "TACCL_STAGED_MAX": "0", "TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "4096"})
     comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=64 << 20)
     try:

@@ -10,7 +10,7 @@ from paper_2111_04867_b200 import taccl
 from paper_2111_04867_b200.generator import generate
 
 STEP = re.compile(r"\s+(\d+) (\w+) src=(\w+):(\d+) dst=(\w+):(\d+) cnt=(\d+) seq=(\d+) poff=(-?\d+) "
-                  r"deps=([\d:,]*) post=([\d:,]*) part=(\d+)/(\d+) fuse=(\d+) fwd=(\d+) pf=(\d+)(?: prog(2?))?")
+                  r"deps=([\d:,]*) post=([\d:,]*) part=(\d+)/(\d+) fuse=(\d+) fwd=(\d+) pf=(\d+)( prog)?")
 TB = re.compile(r"tb (\d+) send=(-?\d+) recv=(-?\d+) chan=(\d+) indep=(\d)")
 
 
@@ -26,7 +26,7 @@ def plan(text, rank, ll=False):
         tbs[-1]["steps"].append({"op": m[2], "src": (m[3], int(m[4])), "dst": (m[5], int(m[6])), "cnt": int(m[7]),
                                  "seq": int(m[8]), "poff": int(m[9]), "deps": [d for d in m[10].split(",") if d],
                                  "post": [d for d in m[11].split(",") if d], "part": int(m[12]), "nparts": int(m[13]),
-                                 "fuse": int(m[14]), "pf": int(m[16]), "prog": 0 if m[17] is None else 2 if m[17] else 1})
+                                 "fuse": int(m[14]), "pf": int(m[16]), "prog": bool(m[17])})
     return tbs
 
 
@@ -200,18 +200,15 @@ def test_streamed_marks_split_reduces_and_their_sends(coll, n):
     # split direct (sends and receive-reduces in separate tbs): every chain member is its tb's
     # first step and every input comes from a plain send -> the chain and exactly the sends
     # that feed it stream (seq 0 on each connection); the Allreduce's second phase (plain
-    # receives) does not. Paired send+rrc threadblocks (the default lowering) stream the same
-    # messages, and each receive-reduce runs together with the send before it (prog 2).
+    # receives) does not. Paired send+rrc threadblocks stream nothing.
     split, paired = generate(coll, "direct", n, 1, 1, pair=False), generate(coll, "direct", n, 1, 1)
-    for text, want in ((split, 1), (paired, 2)):
-        for r in range(n):
-            steps = [x for tb in plan(text, r) for x in tb["steps"]]
-            red = [x for x in steps if x["op"] in ("RRC", "RRC_FUSED")]
-            assert red and all(x["prog"] == want for x in red)
-            assert all(x["prog"] == (x["seq"] == 0) for x in steps if x["op"] == "SEND")
-            assert not any(x["prog"] for x in steps if x["op"] not in ("SEND", "RRC", "RRC_FUSED"))
-    for tb in plan(paired, 0):  # the pair: send first, its receive-reduce right after
-        assert [x["op"] for x in tb["steps"][:2]] == ["SEND", "RRC_FUSED" if n > 2 else "RRC"]
+    for r in range(n):
+        steps = [x for tb in plan(split, r) for x in tb["steps"]]
+        red = [x for x in steps if x["op"] in ("RRC", "RRC_FUSED")]
+        assert red and all(x["prog"] for x in red)
+        assert all(x["prog"] == (x["seq"] == 0) for x in steps if x["op"] == "SEND")
+        assert not any(x["prog"] for x in steps if x["op"] not in ("SEND", "RRC", "RRC_FUSED"))
+        assert not any(x["prog"] for tb in plan(paired, r) for x in tb["steps"])
 
 
 def test_streamed_skips_partials_and_forwarded_messages():
