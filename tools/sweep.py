@@ -164,6 +164,7 @@ def main():
     ap.add_argument("--colls", default="allgather,alltoall,allreduce,reducescatter")
     ap.add_argument("--size-lo", type=int, default=10, help="smallest size 2^lo bytes")
     ap.add_argument("--size-hi", type=int, default=30, help="largest size 2^hi bytes")
+    ap.add_argument("--sizes", default=None, help="comma list of sizes in MiB (overrides --size-lo/--size-hi)")
     ap.add_argument("--dtype", default="bfloat16")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-nccl", action="store_true")
@@ -182,7 +183,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    S_max = 1 << a.size_hi
+    sizes = [int(float(x) * (1 << 20)) for x in a.sizes.split(",")] if a.sizes else [1 << k for k in range(a.size_lo, a.size_hi + 1)]
+    S_max = max(sizes)
     comm = taccl.Comm(rank=rank, nranks=n, device=local, scratch_bytes=2 * S_max + (64 << 20))
     dt = torch.bfloat16 if a.dtype == "bfloat16" else torch.float32
     es = 2 if dt == torch.bfloat16 else 4
@@ -215,8 +217,7 @@ def main():
     for coll in a.colls.split(","):
         algos = (a.algos.split(",") if a.algos else ALGOS[coll]) if n > 1 else ["direct"]
         handles = {al: load(gen(coll, al, n)) for al in algos}
-        for k in range(a.size_lo, a.size_hi + 1):
-            S = 1 << k
+        for S in sizes:
             if coll == "allgather":
                 count = S // es // n
                 inp, out = big_in[:count], big_out[:n * count]
