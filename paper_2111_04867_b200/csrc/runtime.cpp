@@ -77,6 +77,7 @@ struct Algo {
   std::vector<int> wsum;        // per rank
   int fused_chains = 0;
   bool has_pull = false;  // some send of the direct plan is read in place (pull mode applies)
+  bool has_prog = false;  // some message of the direct plan is streamed (plan.cpp mark_streamed)
   bool has_mr = false;    // multicast reduce steps: needs the symmetric pool (NVLink SHARP)
   bool shadow = false;  // bf16 partials read/write the fp32 shadow (bf16 calls need its region)
   int max_o_chunks = 0, max_s_chunks = 0;
@@ -408,7 +409,10 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.trace = g.trace;
   A.trace_ctas = g.trace_ctas;
   const bool pull_on = peer_in && !G.staged && g.nranks > 1 && env_size("TACCL_PULL", 1) != 0;
-  const bool pull_chains = pull_on && !a->plans_pc.empty() &&
+  // (not for schedules with streamed reduces: those already overlap the reduce with the
+  // transfers and lose to in-place chain loads' slower peer reads — RS n=4 1 GiB 1264 vs
+  // 1369 us, profiles/r02_knob_scan_prog_n4.txt)
+  const bool pull_chains = pull_on && !a->plans_pc.empty() && !a->has_prog &&
                            G.chunk_bytes >= (int64_t)env_size("TACCL_PULL_CHAIN_MIN", 64ull << 20);
   int cta = 0, smem = 0;
   for (size_t i = 0; i < ranks.size(); ++i) {
@@ -933,6 +937,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     a->fused_chains += plans[r].fused_chains;
     for (const KStep& k : plans[r].steps) a->has_mr = a->has_mr || k.op == K_MR;
     for (const KStep& k : plans[r].steps) a->has_pull = a->has_pull || (k.op == K_SEND && k.poff >= 0);
+    for (const KStep& k : plans[r].steps) a->has_prog = a->has_prog || k.prog;
     {
       const RankPlan& rp = plans[r];
       const bool one_mr = rp.steps.size() == 1 && rp.steps[0].op == K_MR && rp.steps[0].dep_count == 0 &&

@@ -22,7 +22,8 @@ WIDE = ("int32", "float32")
 def ranges(coll: str, n: int):
     """[(algo, min_bytes, max_bytes[, dtypes])] covering [0, inf) for `coll` at n ranks, for
     every element type; algo may carry a chunk-partitioning suffix `_pK` (K chunks per rank,
-    PAPER.md:702-711); an entry with a dtypes tuple is selected only for those types."""
+    PAPER.md:702-711) and then `_split` (sends and receives lowered into separate threadblocks,
+    generate(pair=False)); an entry with a dtypes tuple is selected only for those types."""
     if n == 1:
         return [("direct", 0, INF)]
     if coll == "allgather":
@@ -52,8 +53,13 @@ def ranges(coll: str, n: int):
             return [("direct", 0, INF)]
         # bf16 rings carry fp32 partials on n-2 of n-1 hops (reading R6): 0.58-0.72x NCCL at
         # 32 MiB-1 GiB (profiles/r02_sweep_n4_graph.txt), so bf16 stays direct; int32/fp32 keep
-        # round 1's ring from 32 MiB
-        return [("direct", 0, 32 * MiB), ("direct", 32 * MiB, INF, BF16), ("ring", 32 * MiB, INF, WIDE)]
+        # round 1's ring from 32 MiB (ahead of the streamed split schedule too up to 512 MiB,
+        # profiles/r02_knob_scan_prog_n4.txt fp32 rows: 128 MiB 173.5 vs 182.6 us). bf16 from
+        # 80 MiB: sends and receive-reduces in separate threadblocks, each reduce streamed as
+        # its stripes land (plan.cpp mark_streamed) — 96 MiB 146 vs 154 us, 128 MiB 187 vs 202,
+        # 1 GiB 1264 vs 1369 (the paired schedule's pulled chains)
+        return [("direct", 0, 32 * MiB), ("direct", 32 * MiB, 80 * MiB, BF16), ("direct_split", 80 * MiB, INF, BF16),
+                ("ring", 32 * MiB, INF, WIDE)]
     raise ValueError(coll)
 
 
@@ -79,7 +85,8 @@ def default_schedules(coll: str, n: int, multicast: bool = True):
     out = []
     extra = multicast_ranges(coll, n) if multicast else []
     for algo, lo, hi, *dt in ranges(coll, n) + extra:
-        name, _, p = algo.partition("_p")
+        split = algo.endswith("_split")
+        name, _, p = algo.removesuffix("_split").partition("_p")
         out.append(generate(coll, name, n, int(p) if p else 1, 1, min_bytes=lo, max_bytes=hi,
-                            dtypes=dt[0] if dt else None))
+                            pair=not split, dtypes=dt[0] if dt else None))
     return out
