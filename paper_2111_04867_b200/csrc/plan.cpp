@@ -192,10 +192,16 @@ void fuse_chain_sends(const Program& P, RankPlan& rp, const std::vector<std::vec
     for (int fi : mem) mpos.push_back(pos(fi));
     const KStep& m0 = rp.steps[mem[0]];
     std::vector<int> sends;
-    for (size_t q = 0; q < mem.size(); ++q) {
-      const int si = mem[q] + 1;
-      const auto [t, k] = mpos[q];
-      if (k + 1 >= rp.tbs[t].nsteps) continue;
+    // candidates: the step right after each member (paired lowering) and, for split lowerings,
+    // a send anywhere whose only dependencies are chain members
+    std::vector<int> cand;
+    for (size_t q = 0; q < mem.size(); ++q)
+      if (mpos[q].second + 1 < rp.tbs[mpos[q].first].nsteps) cand.push_back(mem[q] + 1);
+    for (int si = 0; si < (int)rp.steps.size(); ++si)
+      if (rp.steps[si].op == K_SEND && !deps[si].empty() && std::find(cand.begin(), cand.end(), si) == cand.end())
+        cand.push_back(si);
+    for (int si : cand) {
+      const int t = pos(si).first;
       const KStep& s = rp.steps[si];
       if (s.op != K_SEND || s.srcbuf != m0.dstbuf || s.srcoff != m0.dstoff || s.cnt != m0.cnt || !post[si].empty())
         continue;

@@ -19,11 +19,11 @@ from paper_2111_04867_b200.inputs import allreduce_input  # noqa: E402
 from test_gpu_parity import assert_bits_equal, run_gpu  # noqa: E402
 
 
-def _run(text, coll, n, dtype, ins, env):
+def _run(text, coll, n, dtype, ins, env, mode="direct"):
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
-        return run_gpu(text, coll, n, dtype, ins, mode="direct", pull=False)
+        return run_gpu(text, coll, n, dtype, ins, mode=mode, pull=False)
     finally:
         for k, v in old.items():
             if v is None:
@@ -96,3 +96,21 @@ def test_streamed_repeated_calls_and_epochs():
         comm.destroy()
         for k in ("TACCL_PULL", "TACCL_STAGED_MAX", "TACCL_PROG_STRIPES", "TACCL_STRIPE"):
             os.environ.pop(k, None)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_split_allreduce_chain_sends(n, dtype, mode):
+    # split lowering + chain sends (plan.cpp fuse_chain_sends: the Allgather phase's sends,
+    # in other threadblocks, become K_PUB and the streamed chain members store the reduced
+    # groups to the peers as they compute them); LL plans fuse them by default
+    text = generate("allreduce", "direct", n, 1, 1, pair=False)
+    count = n * 6151 if dtype == "int32" else n * 12289
+    kind = "bits" if dtype == "int32" else "uniform"
+    ins = [allreduce_input(count, dtype, kind, 35, r) for r in range(n)]
+    env = {"TACCL_CHAIN_SENDS": "1", "TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "4096"}
+    got = _run(text, "allreduce", n, dtype, ins, env, mode=mode)
+    if dtype == "int32":
+        assert_bits_equal(got, oracle.expected_outputs("allreduce", ins, "int32"))
+    assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
