@@ -32,6 +32,7 @@ constexpr int kMaxDev = 8;
 
 struct Dests {
   int4* dst[kMaxDev];
+  const int4* src[kMaxDev];  // per destination (push: slices of the local source; pull: peers' sources)
   long long n16;  // 16-byte vectors per destination
   int c;          // destinations
 };
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(512) push_multi(Dests d, const int4* __restric
   const long long tid = (long long)(blockIdx.x / d.c) * blockDim.x + threadIdx.x;
   const long long nt = (long long)nb * blockDim.x;
   int4* dst = d.dst[which];
-  const int4* s = src + (long long)which * d.n16;
+  const int4* s = d.src[which] ? d.src[which] : src + (long long)which * d.n16;
   constexpr int U = 8;
   long long i = tid;
   for (; i + (U - 1) * nt < d.n16; i += U * nt) {
@@ -123,7 +124,7 @@ int main(int argc, char** argv) {
           // push: our source -> peer's dst slot k; pull: peer's source -> our dst slot k
           const long long per = D.n16 * 16;  // 16-byte aligned share of each connection
           D.dst[k] = pull ? (int4*)(dst[d] + (long long)k * per) : (int4*)(dst[peer] + (long long)k * per);
-          if (pull) s = (const int4*)src[peer];  // single destination in pull mode
+          D.src[k] = pull ? (const int4*)(src[peer] + (long long)k * per) : nullptr;  // pull: peer k's source
         }
         CK(cudaEventRecord(e0[d], st[d]));
         for (int r = 0; r < reps; ++r) push_multi<<<ctas, 512, 0, st[d]>>>(D, s);
@@ -188,12 +189,15 @@ int main(int argc, char** argv) {
       const char* cps = getenv("NVLINK_PROBE_CTAS_PER_SM");
       const int ctas = sms * (cps && atoi(cps) > 0 ? atoi(cps) : 1);
       const int reps = V >= (256ll << 20) ? 5 : 50;
-      const float ms = run(all, c, V, ctas, false, reps);
-      const double moved = (double)(V / c / 16 * 16) * c;
-      printf("{\"probe\": \"connections\", \"connections\": %d, \"volume_bytes\": %.0f, \"us\": %.3f, "
-             "\"egress_GBps\": %.1f, \"per_connection_GBps\": %.1f, \"n_devices\": %d, \"ctas\": %d}\n",
-             c, moved, ms * 1e3, moved / (ms / 1e3) / 1e9, moved / c / (ms / 1e3) / 1e9, ndev, ctas);
-      fflush(stdout);
+      for (int pull = 0; pull < 2; ++pull) {  // pull: every GPU loads its c peers' data (ingress)
+        const float ms = run(all, c, V, ctas, pull, reps);
+        const double moved = (double)(V / c / 16 * 16) * c;
+        printf("{\"probe\": \"%s\", \"connections\": %d, \"volume_bytes\": %.0f, \"us\": %.3f, "
+               "\"egress_GBps\": %.1f, \"per_connection_GBps\": %.1f, \"n_devices\": %d, \"ctas\": %d}\n",
+               pull ? "connections_pull" : "connections", c, moved, ms * 1e3, moved / (ms / 1e3) / 1e9,
+               moved / c / (ms / 1e3) / 1e9, ndev, ctas);
+        fflush(stdout);
+      }
     }
   }
   return 0;
