@@ -187,7 +187,8 @@ int main(int argc, char** argv) {
     for (int c = 1; c < ndev; ++c) {
       // one CTA per SM, split among the c connections (NVLINK_PROBE_CTAS_PER_SM overrides)
       const char* cps = getenv("NVLINK_PROBE_CTAS_PER_SM");
-      const int ctas = sms * (cps && atoi(cps) > 0 ? atoi(cps) : 1);
+      const char* cabs = getenv("NVLINK_PROBE_CTAS");  // absolute CTA count (fewer than one per SM)
+      const int ctas = cabs && atoi(cabs) > 0 ? atoi(cabs) : sms * (cps && atoi(cps) > 0 ? atoi(cps) : 1);
       const int reps = V >= (256ll << 20) ? 5 : 50;
       for (int pull = 0; pull < 2; ++pull) {  // pull: every GPU loads its c peers' data (ingress)
         const float ms = run(all, c, V, ctas, pull, reps);
