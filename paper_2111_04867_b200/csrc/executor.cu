@@ -1131,6 +1131,8 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   const KStep* steps = reinterpret_cast<const KStep*>(planp + R.steps_off);
   const int32_t* deps = reinterpret_cast<const int32_t*>(planp + R.deps_off);
   const int32_t* fused = reinterpret_cast<const int32_t*>(planp + R.fused_off);
+  const bool merged = !LL && cta_merged(me);
+  const int32_t* order = reinterpret_cast<const int32_t*>(planp + R.order_off);
   // CTA (t, c0) runs pieces j = c0, c0 + C, ... of threadblock t, each piece's whole program
   // before the next (every CTA visits pieces in increasing order, so a wait on piece j only
   // ever depends on piece-j work of CTAs that have finished all their pieces < j).
@@ -1139,7 +1141,8 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   Ctx c{&A, &R, t, 0, 0};
   c.epoch = s_epoch;
   const u64 E = c.epoch << 24;
-  const KTB& tb = tbs[c.t];  // plan lives in shared memory (or global): read fields on use
+  // this CTA's threadblocks: its own, or every one of the rank's (merged execution)
+  const int t_lo = merged ? 0 : c.t, t_hi = merged ? R.ntb : c.t + 1;
   u64* my_data = reinterpret_cast<u64*>(R.arena + kOffData);
   u64* my_ready = reinterpret_cast<u64*>(R.arena + kOffReady);
   u64* my_done = reinterpret_cast<u64*>(R.arena + kOffDone);
@@ -1166,27 +1169,38 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   // front — this rank's previous call has fully completed (stream order), so nothing of it
   // can still read the buffers the sender is about to store into; announcing per piece as
   // it starts would throttle the sender to this CTA's per-piece progress.
-  if (!LL && tb.recv >= 0 && tid == 0 && !A.ready_per_piece) {
-    u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
-    for (int j = c0; j < nsplit; j += ct) st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), ready_word);
-  }
+  if (!LL && tid == 0 && !A.ready_per_piece)
+    for (int t2 = t_lo; t2 < t_hi; ++t2) {
+      const KTB& x = tbs[t2];
+      if (x.recv < 0) continue;
+      u64* ready = reinterpret_cast<u64*>(R.peer_arena[x.recv] + kOffReady);
+      for (int j = c0; j < nsplit; j += ct) st_relaxed_sys(ready + flag_slot(R.rank, x.chan, j), ready_word);
+    }
   unsigned fin_early = 0;
+  const int nunits = merged ? R.norder : tbs[c.t].nsteps;  // steps this CTA runs per piece
   for (int j = c0; j < nsplit; j += ct) {
     c.j = j;
-    if (!LL && tb.recv >= 0 && tid == 0 && A.ready_per_piece) {  // A/B knob: announce as each piece starts
-      u64* ready = reinterpret_cast<u64*>(R.peer_arena[tb.recv] + kOffReady);
-      st_relaxed_sys(ready + flag_slot(R.rank, tb.chan, j), ready_word);
-    }
-    bool sender_ready = false;
+    if (!LL && tid == 0 && A.ready_per_piece)  // A/B knob: announce as each piece starts
+      for (int t2 = t_lo; t2 < t_hi; ++t2) {
+        const KTB& x = tbs[t2];
+        if (x.recv < 0) continue;
+        u64* ready = reinterpret_cast<u64*>(R.peer_arena[x.recv] + kOffReady);
+        st_relaxed_sys(ready + flag_slot(R.rank, x.chan, j), ready_word);
+      }
+    u64 sender_ready = 0;  // bit t: threadblock t's send connection passed the entry handshake
 
-    for (int k = 0; k < tb.nsteps; ++k) {
+    for (int u = 0; u < nunits; ++u) {
+      // unit u: step k of threadblock c.t (merged: the plan's level order over all of them)
+      const int k = merged ? (order[u] & 0xFFFF) : u;
+      if (merged) c.t = order[u] >> 16;
+      const KTB& tb = tbs[c.t];  // plan lives in shared memory (or global): read fields on use
       const KStep& st = steps[tb.step_begin + k];
       // the rank's CTA 0: load the arrival counter as its last step starts, so the exit check
       // below normally finds every CTA arrived without another L2 round trip on its path
-      if (tid == 0 && c0 == 0 && t == 0 && k + 1 == tb.nsteps && j + ct >= nsplit)
+      if (tid == 0 && c0 == 0 && t == 0 && u + 1 == nunits && j + ct >= nsplit)
         fin_early = *reinterpret_cast<volatile unsigned*>(&ctrl->finished);
-      const bool tr = trace && j == c0 && k < kTraceSteps;
-      if (tr) trace[2 + 4 * k] = globaltimer();
+      const bool tr = trace && j == c0 && u < kTraceSteps;
+      if (tr) trace[2 + 4 * u] = globaltimer();
       // LL data steps (one copy of their code, so the kernel's executed footprint stays small):
       // thread 0 waits for the step's dependencies, if any (LL lines carry their own flags, so
       // there is nothing else to wait for); then every thread derives its slot pointers itself
@@ -1208,7 +1222,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           __syncthreads();
           if (s_abort) return;
         }
-        if (tr) trace[3 + 4 * k] = globaltimer();
+        if (tr) trace[3 + 4 * u] = globaltimer();
         const bool fz = st.op == K_RRC_FUSED;
         const char* ins[kMaxRanks];
         char* fws[kMaxRanks];
@@ -1268,7 +1282,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
                                                ll_flag, A.timeout_ns)
                                  : ll_lines<kMaxRanks>(A.dtype, true, src, dst, ins, nin, fws, nfw, cbytes, ll_cb, st.cnt,
                                                        l0, l1, ll_flag, A.timeout_ns);
-        if (tr) trace[4 + 4 * k] = globaltimer();
+        if (tr) trace[4 + 4 * u] = globaltimer();
 #endif
         if (__syncthreads_or(!ok)) {
           if (tid == 0) record_error(c, st.op, k);
@@ -1283,11 +1297,11 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           const int dt = deps[2 * (st.dep_begin + d)], dk = deps[2 * (st.dep_begin + d) + 1];
           ok = wait_ge<false>(my_done + (size_t)dt * kMaxSplit + j, E | (u64)(dk + 1), A.timeout_ns);
         }
-        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) && !sender_ready) {
+        if (ok && !LL && (st.op == K_SEND || st.op == K_RRCS || st.op == K_RCS) && !((sender_ready >> c.t) & 1)) {
           const int w = wait_ready(my_ready + flag_slot(tb.send, tb.chan, j), c.epoch, A.pull, A.timeout_ns);
           ok = w == 0;
           what = w == 2 ? kErrPullMismatch : st.op;
-          sender_ready = true;
+          sender_ready |= 1ull << c.t;
         }
         // staged (LL) mode: no data flags, every line carries its own (ll_lines)
         // (a streamed rrc waits per stripe group instead, in its data loop)
@@ -1331,7 +1345,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
           record_error(c, what, k);
           s_abort = 1;
         }
-        if (tr) trace[3 + 4 * k] = globaltimer();
+        if (tr) trace[3 + 4 * u] = globaltimer();
       }
       __syncthreads();
       if (s_abort) return;
@@ -1479,7 +1493,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
                          E | (u64)((st.op == K_RRCS || st.op == K_RCS ? st.fwd_seq : st.seq) + 1));
         }
         if (st.need_done && ok) st_release_gpu(my_done + (size_t)c.t * kMaxSplit + j, E | (u64)(k + 1));
-        if (tr) trace[5 + 4 * k] = globaltimer();
+        if (tr) trace[5 + 4 * u] = globaltimer();
       }
       if (st.post_count) {
         __syncthreads();
@@ -1490,17 +1504,22 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
   // pull mode: this CTA's pulled sends are complete once their readers acked (the caller may
   // reuse the input after the call). Waited here, after every piece, so no reader can be
   // waiting on this CTA (its data flags were published at the sends' places).
-  if (!LL && A.pull && tid == 0 && tb.send >= 0) {
+  if (!LL && A.pull && tid == 0) {
     const u64* ack = reinterpret_cast<const u64*>(R.arena + kOffAck);
-    for (int j = c0; j < nsplit; j += ct)
-      for (int k = 0; k < tb.nsteps; ++k) {
-        const KStep& st = steps[tb.step_begin + k];
-        if (pulled(A, st) && !wait_ge<true>(ack + flag_slot(tb.send, tb.chan, j), E | (u64)(st.seq + 1), A.timeout_ns)) {
-          record_error(c, st.op, k);
-          j = nsplit;
-          break;
+    bool ok = true;
+    for (int t2 = t_lo; t2 < t_hi && ok; ++t2) {
+      const KTB& x = tbs[t2];
+      if (x.send < 0) continue;
+      for (int j = c0; j < nsplit && ok; j += ct)
+        for (int k = 0; k < x.nsteps && ok; ++k) {
+          const KStep& st = steps[x.step_begin + k];
+          if (pulled(A, st) && !wait_ge<true>(ack + flag_slot(x.send, x.chan, j), E | (u64)(st.seq + 1), A.timeout_ns)) {
+            c.t = t2;
+            record_error(c, st.op, k);
+            ok = false;
+          }
         }
-      }
+    }
   }
   // completion: the rank's CTA 0 advances the rank's epoch for the next call once all other
   // CTAs of the rank have arrived (read this call's epoch) — by now they normally have, so

@@ -359,6 +359,90 @@ void mark_streamed(std::vector<RankPlan>& plans) {
   }
 }
 
+// Merged execution (DESIGN.md §6 "merged threadblocks"): every CTA of a rank runs, for each of
+// its pieces, the steps of ALL the rank's threadblocks, instead of one threadblock's. The order
+// must never make a CTA wait for something that waits for it. Levels over the global step
+// graph give one: edges are program order, dependencies (pre and post), and message edges (the
+// step that publishes a message's data flag -> every step that waits for it); a step's level
+// is its longest path from a source. Every wait then points at a strictly lower level, so CTAs
+// that run their steps by increasing level (any order within a level) make progress level by
+// level (and piece by piece, as before). Multicast reduces (a barrier across ranks) and graphs
+// with a message nobody publishes or a cycle leave `order` empty (not mergeable).
+void merged_order(std::vector<RankPlan>& plans) {
+  const int n = (int)plans.size();
+  std::vector<int> base(n + 1, 0);
+  for (int r = 0; r < n; ++r) base[r + 1] = base[r] + (int)plans[r].steps.size();
+  const int N = base[n];
+  std::vector<std::vector<int>> succ(N);
+  std::vector<int> indeg(N, 0);
+  auto edge = [&](int a, int b) {
+    succ[a].push_back(b);
+    ++indeg[b];
+  };
+  std::map<std::tuple<int, int, int, int>, int> writer;  // (receiver, sender, chan, seq) -> node
+  for (int q = 0; q < n; ++q) {
+    const RankPlan& rp = plans[q];
+    for (const KTB& kt : rp.tbs)
+      for (int k = 0; k < kt.nsteps; ++k) {
+        const KStep& s = rp.steps[kt.step_begin + k];
+        const int node = base[q] + kt.step_begin + k;
+        if (s.op == K_MR) return;
+        if (s.op == K_SEND || s.op == K_PUB) writer[{kt.send, q, kt.chan, s.seq}] = node;
+        if (s.op == K_RRCS || s.op == K_RCS) writer[{kt.send, q, kt.chan, s.fwd_seq}] = node;
+      }
+  }
+  for (int r = 0; r < n; ++r) {
+    const RankPlan& rp = plans[r];
+    for (const KTB& kt : rp.tbs)
+      for (int k = 0; k < kt.nsteps; ++k) {
+        const int i = kt.step_begin + k, node = base[r] + i;
+        const KStep& s = rp.steps[i];
+        if (k > 0) edge(node - 1, node);
+        for (int d = 0; d < s.dep_count + s.post_count; ++d) {
+          const int e = d < s.dep_count ? s.dep_begin + d : s.post_begin + (d - s.dep_count);
+          edge(base[r] + rp.tbs[rp.deps[2 * e]].step_begin + rp.deps[2 * e + 1], node);
+        }
+        auto msg = [&](int sender, int chan, int seq) {
+          auto it = writer.find({r, sender, chan, seq});
+          if (it == writer.end()) return false;
+          edge(it->second, node);
+          return true;
+        };
+        bool ok = true;
+        if (s.op == K_RECV || s.op == K_RRC || s.op == K_RRCS || s.op == K_RCS) ok = msg(kt.recv, kt.chan, s.seq);
+        if (s.op == K_RRC_FUSED)
+          for (int f = 0; f < s.fuse_count && ok; ++f) {
+            const int* fz = rp.fused.data() + kFuseStride * (s.fuse_begin + f);
+            ok = msg(rp.tbs[fz[0]].recv, rp.tbs[fz[0]].chan, fz[1]);
+          }
+        if (!ok) return;
+      }
+  }
+  std::vector<int> level(N, 0), ready;
+  for (int v = 0; v < N; ++v)
+    if (!indeg[v]) ready.push_back(v);
+  int seen = 0;
+  while (!ready.empty()) {
+    const int v = ready.back();
+    ready.pop_back();
+    ++seen;
+    for (int w : succ[v]) {
+      level[w] = std::max(level[w], level[v] + 1);
+      if (--indeg[w] == 0) ready.push_back(w);
+    }
+  }
+  if (seen != N) return;  // a cycle: the checker's happens-before should exclude it
+  for (int r = 0; r < n; ++r) {
+    RankPlan& rp = plans[r];
+    std::vector<std::tuple<int, int, int>> key;  // (level, tb, step)
+    for (int t = 0; t < (int)rp.tbs.size(); ++t)
+      for (int k = 0; k < rp.tbs[t].nsteps; ++k) key.push_back({level[base[r] + rp.tbs[t].step_begin + k], t, k});
+    std::sort(key.begin(), key.end());
+    rp.order.clear();
+    for (auto [l, t, k] : key) rp.order.push_back((t << 16) | k);
+  }
+}
+
 std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, bool chain_sends, int pull_kinds) {
   const int n = P.nranks;
   std::vector<RankPlan> plans(n);
@@ -672,6 +756,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
         }
       }
   mark_streamed(plans);
+  merged_order(plans);
   return plans;
 }
 

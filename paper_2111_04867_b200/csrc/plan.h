@@ -18,6 +18,8 @@ struct RankPlan {
   bool partials = false;       // some step carries bf16 partial flags
   bool shadow = false;         // some step reads or writes the fp32 shadow of o / s (bf16 calls
                                // then need the shadow region: 2 x (o + s) bytes)
+  std::vector<int32_t> order;  // merged execution: every step of the rank as tb << 16 | step, in
+                               // global level order (plan.cpp merged_order); empty = not mergeable
 };
 
 // `fuse`: fuse rrc chains into multi-input reductions (env TACCL_NO_FUSE=1 disables);

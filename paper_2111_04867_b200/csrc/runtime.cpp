@@ -49,6 +49,7 @@ struct DevPlan {  // one rank's plan blob in device memory
   void* mem = nullptr;
   int bytes = 0, steps_off = 0, deps_off = 0, fused_off = 0;
   int ntb = 0;
+  int order_off = 0, norder = 0;  // merged execution order (norder 0: not mergeable)
 };
 
 struct Algo {
@@ -78,6 +79,7 @@ struct Algo {
   int fused_chains = 0;
   bool has_pull = false;  // some send of the direct plan is read in place (pull mode applies)
   bool has_prog = false;  // some message of the direct plan is streamed (plan.cpp mark_streamed)
+  bool mergeable = false; // every rank's direct plans have a merged execution order (plan.cpp merged_order)
   bool has_mr = false;    // multicast reduce steps: needs the symmetric pool (NVLink SHARP)
   bool shadow = false;  // bf16 partials read/write the fp32 shadow (bf16 calls need its region)
   int max_o_chunks = 0, max_s_chunks = 0;
@@ -209,6 +211,7 @@ Algo* select_algo(taccl_coll_t coll, uint64_t S, taccl_dtype_t dtype, bool mr_ok
 struct Geometry {
   int64_t ce = 0, chunk_bytes = 0, stripe = 0;
   int split = 1, grid = 0, budget = 0, dep_ctas = 1, staged = 0, indep_cap = 1;
+  int merged = 0;  // merged execution: dep_ctas CTAs per rank, each running every threadblock
   int64_t scratch_off = 0, staging_off = 0, need = 0, shadow_off = 0, shadow_s = 0;
   std::vector<std::vector<int>> ct;  // [rank][tb] CTAs of the threadblock (0 for non-local ranks)
 };
@@ -250,6 +253,9 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
     if (a->plans[r].mem) ++nlocal;
   G->indep_cap = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxSplit, (int64_t)a->max_steps_cnt * G->chunk_bytes / min_piece));
   G->budget = std::max(1, target / std::max(1, nlocal));
+  // merged execution (TACCL_MERGED=1, A/B knob; plan.cpp merged_order): every CTA of a rank
+  // runs all of its threadblocks, so each step gets the rank's whole CTA budget
+  G->merged = !G->staged && a->mergeable && env_size("TACCL_MERGED", 0) != 0 ? 1 : 0;
   // CTAs left for the dependent tbs once independent tbs took their weight share, shared
   // equally among the dependent tbs (TACCL_DEP_WEIGHTED=1: by data-volume weight — measured
   // slower for split send/reduce tbs, the reduce side needs its CTAs for HBM bandwidth);
@@ -278,6 +284,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
         per_dep = std::max(per_dep, sh);
       }
   }
+  if (G->merged) per_dep = G->budget;
   if (forced) {
     lanes = (int)forced;
     G->split = a->instances * lanes;
@@ -309,7 +316,8 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   G->dep_ctas = std::min(G->split, per_dep);
   G->grid = 0;
   G->ct.assign(a->nranks, {});
-  for (int r = 0; r < a->nranks; ++r)
+  if (G->merged) G->grid = nlocal * G->dep_ctas;
+  for (int r = 0; r < a->nranks && !G->merged; ++r)
     if (a->plans[r].mem) {
       G->ct[r].assign(a->ntb[r], 0);
       for (int t = 0; t < a->ntb[r]; ++t) {
@@ -424,6 +432,8 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     R.steps_off = dp.steps_off;
     R.deps_off = dp.deps_off;
     R.fused_off = dp.fused_off;
+    R.order_off = dp.order_off;
+    R.norder = dp.norder;
     smem = std::max(smem, dp.bytes);
     R.in = (const char*)sends[i];
     R.out = (char*)recvs[i];
@@ -444,7 +454,13 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     R.budget = G.budget;
     R.wsum = a->wsum[r];
     const int first = cta;
-    for (int t = 0; t < dp.ntb; ++t) {
+    if (G.merged) {  // every CTA of the rank runs all its threadblocks (plan order)
+      for (int c = 0; c < G.dep_ctas; ++c) {
+        if (cta >= kMaxGrid) return fail(TACCL_ERR_UNSUPPORTED, "launch exceeds " + std::to_string(kMaxGrid) + " CTAs");
+        A.cta_map[cta++] = cta_pack((int)i, 0, c, G.dep_ctas, 0) | kCtaMerged;
+      }
+    }
+    for (int t = 0; t < dp.ntb && !G.merged; ++t) {
       const int ind = a->indep[r][t];
       const int ct = G.ct[r][t];
       for (int c = 0; c < ct; ++c) {
@@ -572,13 +588,14 @@ taccl_result_t run_one(taccl_coll_t coll, const void* sendbuf, void* recvbuf, si
 taccl_result_t upload(const RankPlan& rp, DevPlan* dp) {
   auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
   const size_t b1 = al(rp.tbs.size() * sizeof(KTB)), b2 = al(rp.steps.size() * sizeof(KStep));
-  const size_t b3 = al(rp.deps.size() * 4), b4 = al(rp.fused.size() * 4);
-  const size_t total = b1 + b2 + b3 + b4 + 16;
+  const size_t b3 = al(rp.deps.size() * 4), b4 = al(rp.fused.size() * 4), b5 = al(rp.order.size() * 4);
+  const size_t total = b1 + b2 + b3 + b4 + b5 + 16;
   std::vector<char> host(total, 0);
   if (!rp.tbs.empty()) memcpy(host.data(), rp.tbs.data(), rp.tbs.size() * sizeof(KTB));
   if (!rp.steps.empty()) memcpy(host.data() + b1, rp.steps.data(), rp.steps.size() * sizeof(KStep));
   if (!rp.deps.empty()) memcpy(host.data() + b1 + b2, rp.deps.data(), rp.deps.size() * 4);
   if (!rp.fused.empty()) memcpy(host.data() + b1 + b2 + b3, rp.fused.data(), rp.fused.size() * 4);
+  if (!rp.order.empty()) memcpy(host.data() + b1 + b2 + b3 + b4, rp.order.data(), rp.order.size() * 4);
   char* m = nullptr;
   CUDA_TRY(cudaMalloc(&m, total));
   CUDA_TRY(cudaMemcpy(m, host.data(), total, cudaMemcpyHostToDevice));
@@ -587,6 +604,8 @@ taccl_result_t upload(const RankPlan& rp, DevPlan* dp) {
   dp->steps_off = (int)b1;
   dp->deps_off = (int)(b1 + b2);
   dp->fused_off = (int)(b1 + b2 + b3);
+  dp->order_off = (int)(b1 + b2 + b3 + b4);
+  dp->norder = (int)rp.order.size();
   dp->ntb = (int)rp.tbs.size();
   return TACCL_SUCCESS;
 }
@@ -662,6 +681,11 @@ taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, c
              " fuse=" + std::to_string(x.op == K_RRC_FUSED ? x.fuse_count : 0) + " fwd=" + std::to_string(x.fwd_count) +
              " pf=" + std::to_string(x.pflags) + (x.prog ? " prog" : "") + "\n";
       }
+    }
+    if (!rp.order.empty()) {  // merged execution order (plan.cpp merged_order): tb:step ...
+      d += "order";
+      for (int32_t o : rp.order) d += " " + std::to_string(o >> 16) + ":" + std::to_string(o & 0xFFFF);
+      d += "\n";
     }
   } catch (const SchedError& e) {
     return fail(TACCL_ERR_INVALID_SCHEDULE, e.kind + ": " + e.msg);
@@ -938,6 +962,7 @@ taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) 
     for (const KStep& k : plans[r].steps) a->has_mr = a->has_mr || k.op == K_MR;
     for (const KStep& k : plans[r].steps) a->has_pull = a->has_pull || (k.op == K_SEND && k.poff >= 0);
     for (const KStep& k : plans[r].steps) a->has_prog = a->has_prog || k.prog;
+    a->mergeable = (r == 0 || a->mergeable) && !plans[r].order.empty() && (!pc || !plans_pc[r].order.empty());
     {
       const RankPlan& rp = plans[r];
       const bool one_mr = rp.steps.size() == 1 && rp.steps[0].op == K_MR && rp.steps[0].dep_count == 0 &&

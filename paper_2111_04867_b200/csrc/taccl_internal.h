@@ -198,6 +198,7 @@ struct KRank {
   int32_t rank, ntb, ncta;  // ncta: CTAs of this rank in the launch
   int32_t budget;          // CTAs of this rank: tb t gets tb_ctas(weight_t, wsum, ...)
   int32_t wsum, pad;
+  int32_t order_off, norder;  // merged execution: the plan blob's step order (tb << 16 | step)
 };
 
 struct KArgs {
@@ -249,6 +250,10 @@ TACCL_HD inline int cta_c0(uint32_t m) { return (int)((m >> 6) & 511); }
 TACCL_HD inline int cta_ct(uint32_t m) { return (int)((m >> 15) & 1023); }
 TACCL_HD inline int cta_lr(uint32_t m) { return (int)((m >> 25) & 7); }
 TACCL_HD inline int cta_indep(uint32_t m) { return (int)((m >> 28) & 1); }
+// merged execution (plan.cpp merged_order): the CTA runs every threadblock's steps of its
+// pieces in the plan's level order (tb field 0, CTAs of the tb = the rank's CTAs)
+constexpr uint32_t kCtaMerged = 1u << 29;
+TACCL_HD inline int cta_merged(uint32_t m) { return (int)((m >> 29) & 1); }
 
 // Trace record of one CTA (TACCL_TRACE_SLOTS u64 per CTA; first piece only):
 // [0] entry, [1] prologue done (plan + epoch), then per step k < kTraceSteps:

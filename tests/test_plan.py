@@ -17,6 +17,8 @@ TB = re.compile(r"tb (\d+) send=(-?\d+) recv=(-?\d+) chan=(\d+) indep=(\d)")
 def plan(text, rank, ll=False):
     tbs = []
     for line in taccl.plan_dump(text, rank, ll).splitlines():
+        if line.startswith("order"):
+            continue
         m = TB.match(line)
         if m:
             tbs.append({"send": int(m[2]), "recv": int(m[3]), "chan": int(m[4]), "steps": []})
@@ -218,3 +220,35 @@ def test_streamed_skips_partials_and_forwarded_messages():
         text = generate("allreduce", "ring", 4, 1, 1, pair=pair)
         for r in range(4):
             assert not any(x["prog"] for tb in plan(text, r) for x in tb["steps"])
+
+
+ORDER_SCHEDS = [("alltoall", "direct", 4, {}), ("allgather", "ring", 4, {}), ("allreduce", "direct", 8, {}),
+                ("allreduce", "ring", 3, {}), ("reducescatter", "direct", 4, {"pair": False}),
+                ("allreduce", "dring", 4, {}), ("allgather", "greedy", 8, {}), ("alltoall", "hier", 4, {})]
+
+
+@pytest.mark.parametrize("coll,algo,n,kw", ORDER_SCHEDS)
+def test_merged_order_is_a_level_order(coll, algo, n, kw):
+    # merged execution (plan.cpp merged_order): every step exactly once and each threadblock's
+    # steps in program order (cross-rank consistency is what the GPU tests exercise: a wrong
+    # order deadlocks and surfaces as a watchdog timeout)
+    text = generate(coll, algo, n, 1, 1, **kw)
+    for r in range(n):
+        dump = taccl.plan_dump(text, r)
+        order = [tuple(map(int, x.split(":"))) for x in next(l for l in dump.splitlines() if l.startswith("order")).split()[1:]]
+        tbs = plan(text, r)
+        assert sorted(order) == sorted((t, k) for t, tb in enumerate(tbs) for k in range(len(tb["steps"])))
+        for t in range(len(tbs)):
+            ks = [k for (tt, k) in order if tt == t]
+            assert ks == sorted(ks)
+
+
+def test_merged_order_puts_a2a_sends_before_receives():
+    # all-pairs Alltoall: the three sends (one per peer, level 0) come first, then the receives
+    text = generate("alltoall", "direct", 4, 1, 1)
+    tbs = plan(text, 0)
+    dump = taccl.plan_dump(text, 0)
+    order = [tuple(map(int, x.split(":"))) for x in next(l for l in dump.splitlines() if l.startswith("order")).split()[1:]]
+    ops = [tbs[t]["steps"][k]["op"] for t, k in order]
+    first_recv = ops.index("RECV")
+    assert all(o != "RECV" for o in ops[:first_recv]) and all(o in ("RECV", "NOP") for o in ops[first_recv:])
