@@ -78,6 +78,30 @@ __global__ void __launch_bounds__(512) push_multi(Dests d, const int4* __restric
   for (; i < d.n16; i += nt) dst[i] = __ldcg(s + i);
 }
 
+// same, but CTA-contiguous: the destination's range is cut into blocks of `blk` vectors and
+// each CTA walks whole blocks (blocks b, b + nb, ...; the executor's stripes are such blocks)
+__global__ void __launch_bounds__(512) push_blocks(Dests d, const int4* __restrict__ src, long long blk) {
+  const int which = blockIdx.x % d.c;
+  const int nb = gridDim.x / d.c + (blockIdx.x % d.c < gridDim.x % d.c ? 1 : 0);
+  const int me = blockIdx.x / d.c;
+  int4* dst = d.dst[which];
+  const int4* s = d.src[which] ? d.src[which] : src + (long long)which * d.n16;
+  constexpr int U = 8;
+  const int nt = blockDim.x;
+  for (long long b0 = (long long)me * blk; b0 < d.n16; b0 += (long long)nb * blk) {
+    const long long e = b0 + blk < d.n16 ? b0 + blk : d.n16;
+    long long i = b0 + threadIdx.x;
+    for (; i + (U - 1) * nt < e; i += U * nt) {
+      int4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcg(s + i + u * nt);
+#pragma unroll
+      for (int u = 0; u < U; ++u) dst[i + u * nt] = v[u];
+    }
+    for (; i < e; i += nt) dst[i] = __ldcg(s + i);
+  }
+}
+
 int main(int argc, char** argv) {
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -127,7 +151,12 @@ int main(int argc, char** argv) {
           D.src[k] = pull ? (const int4*)(src[peer] + (long long)k * per) : nullptr;  // pull: peer k's source
         }
         CK(cudaEventRecord(e0[d], st[d]));
-        for (int r = 0; r < reps; ++r) push_multi<<<ctas, 512, 0, st[d]>>>(D, s);
+        const char* bk = getenv("NVLINK_PROBE_BLOCK");  // bytes per CTA-contiguous block (0: grid-stride)
+        const long long blk = bk ? atoll(bk) / 16 : 0;
+        for (int r = 0; r < reps; ++r) {
+          if (blk > 0) push_blocks<<<ctas, 512, 0, st[d]>>>(D, s, blk);
+          else push_multi<<<ctas, 512, 0, st[d]>>>(D, s);
+        }
         CK(cudaEventRecord(e1[d], st[d]));
       }
       worst = 0;
