@@ -1,0 +1,13 @@
+#!/bin/bash
+# env-knob scan at n=2 (gpurun --gpus 2): COLLS, ALGOS, SIZES (MiB list) or LO..HI, ENVS list (A=1,B=2 sets two)
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1 --nproc-per-node 2"
+mkdir -p gpurun_out
+out=gpurun_out/knob_scan2_${1:-s}.txt; : > $out
+for env in ${ENVS:-base}; do
+  e=${env//,/ }; [ "$e" = base ] && e="X=1"
+  env $e timeout 600 $TR --master-port 29672 tools/sweep.py --graph $POOL ${DTYPE:+--dtype $DTYPE} --colls ${COLLS:-reducescatter} --size-lo ${LO:-24} --size-hi ${HI:-28} ${SIZES:+--sizes $SIZES} \
+    $( [ $env = base ] || echo --no-nccl ) --algos ${ALGOS:-direct} --out gpurun_out/knob2_tmp.jsonl > /dev/null 2>&1
+  echo "== $env" >> $out
+  python tools/show_sweep.py gpurun_out/knob2_tmp.jsonl >> $out; rm -f gpurun_out/knob2_tmp.jsonl
+done
+cat $out
