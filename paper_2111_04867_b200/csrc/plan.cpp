@@ -331,6 +331,9 @@ void mark_streamed(std::vector<RankPlan>& plans) {
           KStep* s = sender(kt.recv, r, kt.chan, x.seq);
           if (x.pflags || !s || s->pflags || !first_data(rp, kt, k)) continue;
           x.prog = s->prog = 1;
+          // streamed pushes beat in-place loads for such a reduce (RS n=2 1 GiB 800 vs 833 us,
+          // profiles/r02_knob_scan_split_n2.txt): it no longer pulls (both ends agree)
+          x.poff = s->poff = -1;
         } else if (x.op == K_RRC_FUSED && x.part == 0) {
           // the chain's members: the steps sharing its fused entries, one per member tb
           std::vector<KStep*> members;

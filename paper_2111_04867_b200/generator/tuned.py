@@ -49,7 +49,11 @@ def ranges(coll: str, n: int):
         return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("dring", 128 * MiB, INF, BF16),
                 ("ring", 128 * MiB, INF, WIDE)]
     if coll == "reducescatter":
-        if n == 2 or n >= 8:
+        if n == 2:
+            # from 256 MiB the split lowering's streamed push reduce beats the paired schedule's
+            # in-place pull (1 GiB 800 vs 833 us, 256 MiB 221 vs 223; profiles/r02_knob_scan_split_n2.txt)
+            return [("direct", 0, 256 * MiB), ("direct_split", 256 * MiB, INF)]
+        if n >= 8:
             return [("direct", 0, INF)]
         # bf16 rings carry fp32 partials on n-2 of n-1 hops (reading R6): 0.58-0.72x NCCL at
         # 32 MiB-1 GiB (profiles/r02_sweep_n4_graph.txt), so bf16 stays direct; int32/fp32 keep
