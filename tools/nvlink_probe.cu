@@ -102,6 +102,27 @@ __global__ void __launch_bounds__(512) push_blocks(Dests d, const int4* __restri
   }
 }
 
+// rounds: every CTA streams its grid-stride share to destination 0, then 1, ... (no barrier
+// between rounds: CTAs drift apart as they would in a merged-threadblock executor)
+__global__ void __launch_bounds__(512) push_rounds(Dests d, const int4* __restrict__ src) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  constexpr int U = 8;
+  for (int w = 0; w < d.c; ++w) {
+    int4* dst = d.dst[w];
+    const int4* s = d.src[w] ? d.src[w] : src + (long long)w * d.n16;
+    long long i = tid;
+    for (; i + (U - 1) * nt < d.n16; i += U * nt) {
+      int4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcg(s + i + u * nt);
+#pragma unroll
+      for (int u = 0; u < U; ++u) dst[i + u * nt] = v[u];
+    }
+    for (; i < d.n16; i += nt) dst[i] = __ldcg(s + i);
+  }
+}
+
 int main(int argc, char** argv) {
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -154,7 +175,8 @@ int main(int argc, char** argv) {
         const char* bk = getenv("NVLINK_PROBE_BLOCK");  // bytes per CTA-contiguous block (0: grid-stride)
         const long long blk = bk ? atoll(bk) / 16 : 0;
         for (int r = 0; r < reps; ++r) {
-          if (blk > 0) push_blocks<<<ctas, 512, 0, st[d]>>>(D, s, blk);
+          if (getenv("NVLINK_PROBE_ROUNDS")) push_rounds<<<ctas, 512, 0, st[d]>>>(D, s);
+          else if (blk > 0) push_blocks<<<ctas, 512, 0, st[d]>>>(D, s, blk);
           else push_multi<<<ctas, 512, 0, st[d]>>>(D, s);
         }
         CK(cudaEventRecord(e1[d], st[d]));
