@@ -14,6 +14,9 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
     step (no contiguity coalescing, lowering.coalesce)."""
     if algo == "nvls":  # multicast reduce through the switch: written directly (templates.nvls_text)
         return templates.nvls_text(coll, nranks, chunks, instances, min_bytes, max_bytes, dtypes)
+    if algo == "rounds":  # all-pairs in rounds (A/B experiment, DESIGN.md §6 merged threadblocks)
+        return _rounds(generate(coll, "direct", nranks, chunks, instances, min_bytes, max_bytes, pair=False,
+                                merge=merge, dtypes=dtypes), nranks)
     if algo == "hier":
         if nranks % 2:
             raise ValueError("hier needs 2 x k ranks")
@@ -36,3 +39,28 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
         name += "_nomerge"
     return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name, pair=pair,
                  merge=merge, dtypes=dtypes)
+
+
+def _rounds(text, n):
+    """The split all-pairs schedule with round order: the send to rank r + d waits for the
+    receive from rank r - (d - 1) (round d - 1 landed), so with merged threadblocks every round
+    is one permutation of peers, flow-controlled by the previous round's arrival."""
+    import re
+    out, pos = [], 0
+    for m in re.finditer(r'<gpu id="(\d+)".*?</gpu>', text, re.S):
+        r = int(m.group(1))
+        body = m.group(0)
+        recv_tb = {int(b): int(a) for a, b in re.findall(r'<tb id="(\d+)" send="-1" recv="(\d+)"', body)}
+
+        def dep(mt):
+            t, peer = int(mt.group(1)), int(mt.group(2))
+            d = (peer - r) % n
+            if d < 2:
+                return mt.group(0)
+            prev = recv_tb[(r - (d - 1)) % n]
+            return mt.group(0).replace('deps=""', f'deps="{prev}:0"', 1)
+        body = re.sub(r'<tb id="(\d+)" send="(\d+)" recv="-1"[^>]*>\s*<step s="0" type="s"[^/]*/>', dep, body)
+        out.append(text[pos:m.start()] + body)
+        pos = m.end()
+    out.append(text[pos:])
+    return "".join(out).replace('_split"', '_rounds"', 1)

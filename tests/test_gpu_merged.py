@@ -21,7 +21,8 @@ SCHEDS = [("allgather", "direct", 4, 1, {}), ("allgather", "ring", 4, 2, {}), ("
           ("allreduce", "direct", 4, 1, {}), ("allreduce", "direct", 8, 1, {}), ("allreduce", "ring", 4, 1, {}),
           ("allreduce", "dring", 4, 1, {}), ("allreduce", "oneshot", 4, 1, {}), ("allreduce", "direct", 4, 1, {"pair": False}),
           ("reducescatter", "direct", 4, 1, {}), ("reducescatter", "direct", 4, 1, {"pair": False}),
-          ("reducescatter", "ring", 4, 2, {}), ("reducescatter", "direct", 2, 1, {})]
+          ("reducescatter", "ring", 4, 2, {}), ("reducescatter", "direct", 2, 1, {}),
+          ("alltoall", "rounds", 4, 1, {}), ("allgather", "rounds", 8, 1, {}), ("alltoall", "rounds", 3, 2, {})]
 
 
 def _inputs(coll, n, p, dtype, seed):
