@@ -84,23 +84,21 @@ __device__ bool wait_ge(const u64* p, u64 target, u64 timeout_ns) {
   }
 }
 
-// streamed messages (KStep.prog): the sender publishes, after every group of KArgs.prog stripes
-// of its piece, word = key << 20 | groups done, key = (epoch mod 2^20) << 24 | (seq + 1). A
-// later key on the slot (the sender's next message, or a later call) means "all of it" —
-// compared modulo 2^44, so the epoch may wrap. Groups stay far below 2^20 (a piece's stripes
-// are >= 4 KiB apart except for small chunks).
-__device__ __forceinline__ u64 prog_key(u64 epoch, int seq) { return ((epoch & 0xFFFFF) << 24) | (u64)(seq + 1); }
-__device__ __forceinline__ bool prog_reached(u64 v, u64 key, int64_t groups) {
-  const int64_t d = (int64_t)(((v >> 20) - key) << 20) >> 20;
-  return d > 0 || (d == 0 && (int64_t)(v & 0xFFFFF) >= groups);
-}
-__device__ bool wait_prog(const u64* p, u64 key, int64_t groups, u64 timeout_ns) {
-  if (prog_reached(ld_acquire_sys(p), key, groups)) return true;
+// streamed messages (KStep.prog): the sender publishes, after every group of stripes of its
+// piece, word = epoch << 24 | (seq + 1) << 12 | groups done. The word grows with the group,
+// the message and the call (40-bit epochs, as the data flags), so a plain >= comparison holds
+// across calls and a later message on the slot means "all of it". The plan streams only
+// messages with seq < kProgSeqMax; a piece with more than kProgGroups groups widens its groups
+// (streamed_step, the same on both ends).
+constexpr int64_t kProgGroups = 4095;
+__device__ __forceinline__ u64 prog_key(u64 epoch, int seq) { return (epoch << 24) | ((u64)(seq + 1) << 12); }
+__device__ bool wait_prog(const u64* p, u64 want, u64 timeout_ns) {
+  if (ld_acquire_sys(p) >= want) return true;
   const u64 t0 = globaltimer();
   for (;;) {
 #pragma unroll 1
     for (int i = 0; i < 256; ++i)
-      if (prog_reached(ld_acquire_sys(p), key, groups)) return true;
+      if (ld_acquire_sys(p) >= want) return true;
     if (globaltimer() - t0 > timeout_ns) return false;
   }
 }
@@ -108,7 +106,7 @@ __device__ bool wait_prog(const u64* p, u64 key, int64_t groups, u64 timeout_ns)
 // the system-scope fence makes them visible before the word, as for data flags)
 __device__ __forceinline__ void prog_publish(u64* slot, u64 key, int64_t groups) {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
-  st_relaxed_sys(slot, (key << 20) | (u64)groups);
+  st_relaxed_sys(slot, key | (u64)groups);
 }
 
 // ---------------------------------------------------------------- CTA-wide data movement
@@ -972,17 +970,20 @@ __device__ __forceinline__ bool pulled(const KArgs& A, const KStep& st) {
 
 // Direct kernel, streamed messages (KStep.prog, plan.cpp mark_streamed): a K_SEND publishes
 // its progress every A.prog stripes; a K_RRC / K_RRC_FUSED member waits, before each group of
-// A.prog stripes, until every input message published that group, then reduces it. Out of line
-// (called once per step and piece) so the stripe loops do not add to the kernel's registers.
-// Returns false after a timeout (recorded; *abort set for the CTA).
+// A.prog stripes (more for pieces of over kProgGroups groups), until every input message
+// published that group, then reduces it. Returns false after a timeout (recorded; *abort set
+// for the CTA).
 __device__ __forceinline__ bool streamed_step(const Ctx& c, const KStep& st, int k, const KTB* tbs, const int* fused,
                                            const KTB& tb, int64_t stripe, int nsplit, int64_t cbytes, char* dst,
                                            const char* src, char* const* s_fwd, const char* const* s_stage,
                                            volatile int* abort) {
   const KArgs& A = *c.a;
   const KRank& R = *c.r;
-  const int j = c.j, tid = threadIdx.x, G = A.prog;
+  const int j = c.j, tid = threadIdx.x;
   int64_t ns = 0;
+  for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t, int64_t) { ++ns; });  // stripes of the piece
+  const int64_t G = max((int64_t)A.prog, (ns + kProgGroups - 1) / kProgGroups);
+  ns = 0;
   if (st.op == K_SEND) {
     u64* slot = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffProg) + flag_slot(R.rank, tb.chan, j);
     const u64 key = prog_key(c.epoch, st.seq);
@@ -1015,7 +1016,7 @@ __device__ __forceinline__ bool streamed_step(const Ctx& c, const KStep& st, int
             chan = tbs[e[0]].chan;
             seq = e[1];
           }
-          if (!wait_prog(my_prog + flag_slot(peer, chan, j), prog_key(c.epoch, seq), ns / G + 1, A.timeout_ns)) {
+          if (!wait_prog(my_prog + flag_slot(peer, chan, j), prog_key(c.epoch, seq) | (u64)(ns / G + 1), A.timeout_ns)) {
             record_error(c, st.op, k);
             *abort = 1;
           }

@@ -329,7 +329,7 @@ void mark_streamed(std::vector<RankPlan>& plans) {
         KStep& x = rp.steps[kt.step_begin + k];
         if (x.op == K_RRC) {
           KStep* s = sender(kt.recv, r, kt.chan, x.seq);
-          if (x.pflags || !s || s->pflags || !first_data(rp, kt, k)) continue;
+          if (x.pflags || !s || s->pflags || !first_data(rp, kt, k) || x.seq >= kProgSeqMax) continue;
           x.prog = s->prog = 1;
           // streamed pushes beat in-place loads for such a reduce (RS n=2 1 GiB 800 vs 833 us,
           // profiles/r02_knob_scan_split_n2.txt): it no longer pulls (both ends agree)
@@ -350,7 +350,7 @@ void mark_streamed(std::vector<RankPlan>& plans) {
             const int* fz = rp.fused.data() + kFuseStride * (x.fuse_begin + f);
             const KTB& o = rp.tbs[fz[0]];
             KStep* s = sender(o.recv, r, o.chan, fz[1]);
-            ok = s && !s->pflags && !fz[5];
+            ok = s && !s->pflags && !fz[5] && fz[1] < kProgSeqMax;
             sends.push_back(s);
           }
           if (!ok) continue;

@@ -129,6 +129,8 @@ constexpr int P_OUT = 8;   // send (or the forward of K_RRCS): transmit fp32 (fr
 constexpr int P_MIX = 16;  // K_RRC_FUSED: some member message or forward is fp32 (fused array bits)
 // K_RRC_FUSED member entries in the fused array: tb, seq, soff, soff2, poff, P_IN of its message
 constexpr int kFuseStride = 6;
+// streamed messages: the progress word carries the message index in 12 bits (executor.cu)
+constexpr int kProgSeqMax = 4094;
 // forward entries (fuse_chain_sends): peer, chan, rbuf, roff, roff2, seq, P_OUT
 constexpr int kFwdStride = 7;
 

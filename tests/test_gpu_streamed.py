@@ -114,3 +114,14 @@ def test_split_allreduce_chain_sends(n, dtype, mode):
     if dtype == "int32":
         assert_bits_equal(got, oracle.expected_outputs("allreduce", ins, "int32"))
     assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))
+
+
+def test_streamed_piece_with_more_groups_than_the_word_holds():
+    # 16 MiB chunks, 1 KiB stripes, 2 pieces: 8192 stripes per piece at one stripe per group —
+    # more than the progress word's 4095 groups, so both ends widen the groups to 3 stripes
+    n, count = 2, 4 << 20
+    text = generate("reducescatter", "direct", n, 1, 1, pair=False)
+    ins = [allreduce_input(n * count, "int32", "bits", 39, r) for r in range(n)]
+    env = {"TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "1024", "TACCL_LANES": "2"}
+    got = _run(text, "reducescatter", n, "int32", ins, env)
+    assert_bits_equal(got, oracle.expected_outputs("reducescatter", ins, "int32"))
