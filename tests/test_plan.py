@@ -252,3 +252,17 @@ def test_merged_order_puts_a2a_sends_before_receives():
     ops = [tbs[t]["steps"][k]["op"] for t, k in order]
     first_recv = ops.index("RECV")
     assert all(o != "RECV" for o in ops[:first_recv]) and all(o in ("RECV", "NOP") for o in ops[first_recv:])
+
+
+def test_streamed_plain_rrc_is_not_pulled():
+    # RS n=2: the paired schedule's plain rrc reads the peer's input in place (pull); the split
+    # lowering streams it instead, and then neither end pulls (plan.cpp mark_streamed)
+    paired, split = generate("reducescatter", "direct", 2, 1, 1), generate("reducescatter", "direct", 2, 1, 1, pair=False)
+    for r in range(2):
+        steps = [x for tb in plan(paired, r) for x in tb["steps"]]
+        assert any(x["op"] == "RRC" and x["poff"] >= 0 and not x["prog"] for x in steps)
+        steps = [x for tb in plan(split, r) for x in tb["steps"]]
+        rrc = [x for x in steps if x["op"] == "RRC"]
+        send = [x for x in steps if x["op"] == "SEND"]
+        assert rrc and all(x["prog"] and x["poff"] == -1 for x in rrc)
+        assert send and all(x["prog"] and x["poff"] == -1 for x in send)
