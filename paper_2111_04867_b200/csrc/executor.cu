@@ -115,10 +115,17 @@ __device__ __forceinline__ void st_v4_cs(int4* p, int4 v) {
                : "memory");
 }
 
+// The CTA-wide data loops run on the whole CTA, or (s_half, warp-specialised pairs: half the
+// warps send while the other half reduces, streamed_pair) on one half of it: thread index and
+// count within the running half.
+__shared__ int s_half;
+__device__ __forceinline__ int grp_tid() { return s_half ? (int)(threadIdx.x % (blockDim.x / 2)) : (int)threadIdx.x; }
+__device__ __forceinline__ int grp_nt() { return s_half ? (int)blockDim.x / 2 : (int)blockDim.x; }
+
 // U 16-byte vectors in flight per thread; CS: streaming (evict-first) stores
 template <int U, bool CS>
 __device__ __noinline__ void cta_copy_t(char* __restrict__ dst, const char* __restrict__ src, int64_t n) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = grp_tid(), nt = grp_nt();
   if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
     const int64_t nv = n >> 4;
     const int4* s = reinterpret_cast<const int4*>(src);
@@ -222,7 +229,7 @@ __device__ __noinline__ void cta_reduce(char* dst, char* const* fwd, int nfwd, c
   // = src0 + stages[0] + ... ; RU vectors per thread in flight per input
   using E = Elt<DT>;
   constexpr int V = E::V, RU = 4;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = grp_tid(), nt = grp_nt();
   uintptr_t align = (uintptr_t)dst | (uintptr_t)src0;
   for (int s = 0; s < ns; ++s) align |= (uintptr_t)(stages[s] + soff);
   for (int f = 0; f < nfwd; ++f) align |= (uintptr_t)(fwd[f] + soff);
@@ -290,7 +297,7 @@ __device__ __noinline__ void cta_reduce_n(char* dst, char* const* fwd, int nfwd,
                                           const char* const* stages, int64_t soff, int64_t nelem) {
   using E = Elt<DT>;
   constexpr int V = E::V, RU = NS == 1 ? 4 : 2;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = grp_tid(), nt = grp_nt();
   const char* in[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) in[s] = stages[s] + soff;
@@ -1039,6 +1046,96 @@ __device__ __forceinline__ bool streamed_step(const Ctx& c, const KStep& st, int
   return !*abort;
 }
 
+// Warp-specialised pair (KStep.prog == 2 on the receive-reduce, TACCL_WARPSPEC=1): a streamed
+// send and the streamed receive-reduce right after it in the same threadblock run at once —
+// threads [0, T/2) send the piece group by group, publishing each group, while threads
+// [T/2, T) wait for each group of every input message and reduce it (named barriers 1 and 2
+// order each half; the CTA-wide loops run on their half, s_half). Nothing in the send half
+// waits on the reduce half, so the peers' sends — and with them every reduce — progress.
+// Returns false after a timeout (recorded; *abort set).
+__device__ __forceinline__ bool streamed_pair(const Ctx& c, const KStep& snd, const KStep& rrc, int k, const KTB* tbs,
+                                              const int* fused, const KTB& tb, int64_t stripe, int nsplit,
+                                              int64_t cbytes, char* sdst, const char* ssrc, char* const* s_fwd,
+                                              const char** s_stage, volatile int* abort) {
+  const KArgs& A = *c.a;
+  const KRank& R = *c.r;
+  const int j = c.j, tid = threadIdx.x, half = blockDim.x / 2;
+  const bool fz = rrc.op == K_RRC_FUSED;
+  if (tid == 0) {  // the receive-reduce's staging slots (push mode: streaming is off in pull mode)
+    if (fz)
+      for (int f = 0; f < rrc.fuse_count; ++f)
+        s_stage[f] = local_base(c, KB_STAGE) + (int64_t)fused[kFuseStride * (rrc.fuse_begin + f) + 2] * cbytes;
+    else
+      s_stage[0] = local_base(c, KB_STAGE) + (int64_t)rrc.soff * cbytes;
+    s_half = 1;
+  }
+  __syncthreads();
+  if (tid < half) {  // send half
+    int64_t ns = 0;
+    for_piece(stripe, j, nsplit, snd.cnt, cbytes, [&](int64_t, int64_t) { ++ns; });
+    const int64_t G = max((int64_t)A.prog, (ns + kProgGroups - 1) / kProgGroups);
+    u64* slot = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffProg) + flag_slot(R.rank, tb.chan, j);
+    const u64 key = prog_key(c.epoch, snd.seq);
+    ns = 0;
+    for_piece(stripe, j, nsplit, snd.cnt, cbytes, [&](int64_t off, int64_t len) {
+      cta_copy(A.variant, sdst + off, ssrc + off, len);
+      if (++ns % G == 0) {
+        asm volatile("bar.sync 1, %0;" ::"r"(half) : "memory");
+        if (tid == 0) prog_publish(slot, key, ns / G);
+      }
+    });
+    if (ns % G) {
+      asm volatile("bar.sync 1, %0;" ::"r"(half) : "memory");
+      if (tid == 0) prog_publish(slot, key, ns / G + 1);
+    }
+  } else {  // reduce half
+    const char* rsrc = local_base(c, rrc.srcbuf) + (int64_t)rrc.srcoff * cbytes;
+    char* rdst = local_base(c, rrc.dstbuf) + (int64_t)rrc.dstoff * cbytes;
+    const u64* my_prog = reinterpret_cast<const u64*>(R.arena + kOffProg);
+    const int64_t unit = (cbytes % 16 == 0) ? 16 : A.elt;
+    int64_t ns = 0;
+    for_piece(stripe, j, nsplit, rrc.cnt, cbytes, [&](int64_t, int64_t) { ++ns; });
+    const int64_t G = max((int64_t)A.prog, (ns + kProgGroups - 1) / kProgGroups);
+    ns = 0;
+    for_piece(stripe, j, nsplit, rrc.cnt, cbytes, [&](int64_t off, int64_t len) {
+      if (*abort) return;
+      if (ns % G == 0) {
+        if (tid == half) {
+          const int nin = fz ? rrc.fuse_count : 1;
+          for (int f = 0; f < nin && !*abort; ++f) {
+            int peer = tb.recv, chan = tb.chan, seq = rrc.seq;
+            if (fz) {
+              const int* e = fused + kFuseStride * (rrc.fuse_begin + f);
+              peer = tbs[e[0]].recv;
+              chan = tbs[e[0]].chan;
+              seq = e[1];
+            }
+            if (!wait_prog(my_prog + flag_slot(peer, chan, j), prog_key(c.epoch, seq) | (u64)(ns / G + 1), A.timeout_ns)) {
+              record_error(c, rrc.op, k + 1);
+              *abort = 1;
+            }
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"r"(half) : "memory");
+        if (*abort) return;
+      }
+      ++ns;
+      if (!fz) {
+        reduce_dispatch(A.dtype, rdst + off, s_fwd, 0, rsrc + off, s_stage, 1, off, len / A.elt);
+        return;
+      }
+      const int64_t nu = len / unit;
+      const int64_t a = off + nu * rrc.part / rrc.nparts * unit;
+      const int64_t b = (rrc.part + 1 == rrc.nparts) ? off + len : off + nu * (rrc.part + 1) / rrc.nparts * unit;
+      if (b > a) reduce_dispatch(A.dtype, rdst + a, s_fwd, 0, rsrc + a, s_stage, rrc.fuse_count, a, (b - a) / A.elt);
+    });
+  }
+  __syncthreads();
+  if (tid == 0) s_half = 0;
+  __syncthreads();
+  return !*abort;
+}
+
 // Direct kernel, bf16 partials (reading R6): one step whose operands may be fp32 — a send of
 // a source's fp32 shadow into the receiver's (2x) staging slot (P_OUT), or a receive-reduce
 // (K_RRC, K_RRCS, a fused chain member's portion) through cta_reduce_px (out of line). Inlined
@@ -1105,6 +1202,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
     const u64 ep = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
     s_epoch = ep;
     s_abort = 0;
+    s_half = 0;
     // arrival: the rank's CTA 0 advances the epoch at its end once every other CTA of the
     // rank has read it. The added value depends on the loaded epoch (always 1), so the
     // reduction cannot overtake the load.
@@ -1384,7 +1482,13 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
               tma_finish(tp);
             }
           } else if (st.op == K_SEND && A.prog && st.prog) {  // streamed: publish every A.prog stripes
-            streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort);
+            if (k + 1 < tb.nsteps && steps[tb.step_begin + k + 1].prog == 2) {  // with the rrc after it
+              if (!streamed_pair(c, st, steps[tb.step_begin + k + 1], k, tbs, fused, tb, stripe, nsplit, cbytes, dst,
+                                 src, s_fwd, s_stage, &s_abort))
+                return;
+            } else {
+              streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort);
+            }
           } else {
             for_piece(stripe, j, nsplit, st.cnt, cbytes, [&](int64_t off, int64_t len) { cta_copy(A.variant, dst + off, src + off, len); });
           }
@@ -1399,6 +1503,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
             px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
             break;
           }
+          if (A.prog && st.prog == 2) break;  // reduced beside the send before it (streamed_pair)
           if (A.prog && st.prog) {  // streamed: reduce each stripe group once it landed
             if (!streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort)) return;
             break;
@@ -1415,6 +1520,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
             px_step(c, st, fused, tb.send, stripe, nsplit, cbytes, s_fwd, s_stage);
             break;
           }
+          if (A.prog && st.prog == 2) break;  // reduced beside the send before it (streamed_pair)
           if (A.prog && st.prog) {  // streamed: reduce each stripe group once every member's landed
             if (!streamed_step(c, st, k, tbs, fused, tb, stripe, nsplit, cbytes, dst, src, s_fwd, s_stage, &s_abort)) return;
             break;

@@ -302,11 +302,19 @@ std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map
 // reaches the reduce when its peers' messages have landed too (paired send+rrc tbs) and the
 // progress stores would be pure cost. Both ends get KStep.prog; the kernel streams only when
 // KArgs.prog (the runtime turns it off in pull mode and for TMA pushes).
+// With TACCL_WARPSPEC=1 a member may also follow exactly one send without dependencies of its
+// own (paired send + rrc threadblocks, as the direct schedules lower): such a member gets
+// prog = 2 and the kernel runs it beside that send — one half of the CTA's warps sends
+// (publishing groups) while the other half reduces the groups as they land (streamed_pair).
 void mark_streamed(std::vector<RankPlan>& plans) {
   const int n = (int)plans.size();
-  auto first_data = [](const RankPlan& rp, const KTB& kt, int k) {
-    for (int q = 0; q < k; ++q)
-      if (rp.steps[kt.step_begin + q].op != K_NOP) return false;
+  const bool pairs = getenv("TACCL_WARPSPEC") && atoi(getenv("TACCL_WARPSPEC"));
+  auto first_data = [&](const RankPlan& rp, const KTB& kt, int k) {
+    for (int q = 0; q < k; ++q) {
+      const KStep& y = rp.steps[kt.step_begin + q];
+      if (y.op == K_NOP) continue;
+      if (!pairs || q + 1 != k || y.op != K_SEND || y.dep_count || y.post_count) return false;
+    }
     return true;
   };
   // the K_SEND on rank q that carries message `seq` of connection (q -> r, chan), or null
@@ -360,6 +368,17 @@ void mark_streamed(std::vector<RankPlan>& plans) {
       }
     }
   }
+  // warp-specialised pairs: a streamed receive-reduce right after a streamed send of its tb,
+  // without dependencies or forwards, whose destination does not overlap the send's source
+  for (RankPlan& rp : plans)
+    for (const KTB& kt : rp.tbs)
+      for (int k = 1; k < kt.nsteps && pairs; ++k) {
+        KStep& x = rp.steps[kt.step_begin + k];
+        const KStep& s = rp.steps[kt.step_begin + k - 1];
+        if (!x.prog || s.op != K_SEND || !s.prog || x.dep_count || (x.op == K_RRC_FUSED && x.fwd_count)) continue;
+        const bool overlap = x.dstbuf == s.srcbuf && x.dstoff < s.srcoff + s.cnt && s.srcoff < x.dstoff + x.cnt;
+        if (!overlap) x.prog = 2;
+      }
 }
 
 // Merged execution (DESIGN.md §6 "merged threadblocks"): every CTA of a rank runs, for each of

@@ -679,7 +679,7 @@ taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, c
              " deps=" + pairs(x.dep_begin, x.dep_count) + " post=" + pairs(x.post_begin, x.post_count) +
              " part=" + std::to_string(x.part) + "/" + std::to_string(x.nparts) +
              " fuse=" + std::to_string(x.op == K_RRC_FUSED ? x.fuse_count : 0) + " fwd=" + std::to_string(x.fwd_count) +
-             " pf=" + std::to_string(x.pflags) + (x.prog ? " prog" : "") + "\n";
+             " pf=" + std::to_string(x.pflags) + (x.prog == 2 ? " prog2" : x.prog ? " prog" : "") + "\n";
       }
     }
     if (!rp.order.empty()) {  // merged execution order (plan.cpp merged_order): tb:step ...

@@ -125,3 +125,34 @@ def test_streamed_piece_with_more_groups_than_the_word_holds():
     env = {"TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "1024", "TACCL_LANES": "2"}
     got = _run(text, "reducescatter", n, "int32", ins, env)
     assert_bits_equal(got, oracle.expected_outputs("reducescatter", ins, "int32"))
+
+
+@pytest.mark.parametrize("coll,n,p", [("reducescatter", 2, 1), ("reducescatter", 4, 1), ("reducescatter", 4, 2),
+                                      ("reducescatter", 8, 1), ("allreduce", 4, 1), ("allreduce", 8, 1)])
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
+@pytest.mark.parametrize("knob", [{}, {"TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "4096"},
+                                  {"TACCL_LANES": "3", "TACCL_STRIPE": "8192"}])
+def test_warp_specialised_pairs(coll, n, p, dtype, knob):
+    # TACCL_WARPSPEC=1: the paired lowering's send + receive-reduce threadblocks run both steps
+    # at once on the two halves of each CTA (streamed_pair, prog 2)
+    env = {"TACCL_WARPSPEC": "1", **knob}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        text = generate(coll, "direct", n, p, 1)
+        assert " prog2" in taccl.plan_dump(text, 0) or (coll == "allreduce" and n == 2)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    c_e = 12289 if dtype == "bfloat16" else 6151
+    count = p * c_e * (n if coll == "allreduce" else 1)
+    kind = "bits" if dtype == "int32" else "intval"
+    e_in = n * count if coll == "reducescatter" else count
+    ins = [allreduce_input(e_in, dtype, kind, 41, r) for r in range(n)]
+    got = _run(text, coll, n, dtype, ins, env)
+    if dtype == "int32":
+        assert_bits_equal(got, oracle.expected_outputs(coll, ins, "int32"))
+    assert_bits_equal(got, oracle.run(oracle.parse(text), ins, dtype))

@@ -10,7 +10,7 @@ from paper_2111_04867_b200 import taccl
 from paper_2111_04867_b200.generator import generate
 
 STEP = re.compile(r"\s+(\d+) (\w+) src=(\w+):(\d+) dst=(\w+):(\d+) cnt=(\d+) seq=(\d+) poff=(-?\d+) "
-                  r"deps=([\d:,]*) post=([\d:,]*) part=(\d+)/(\d+) fuse=(\d+) fwd=(\d+) pf=(\d+)( prog)?")
+                  r"deps=([\d:,]*) post=([\d:,]*) part=(\d+)/(\d+) fuse=(\d+) fwd=(\d+) pf=(\d+)( prog2?)?")
 TB = re.compile(r"tb (\d+) send=(-?\d+) recv=(-?\d+) chan=(\d+) indep=(\d)")
 
 
@@ -28,7 +28,7 @@ def plan(text, rank, ll=False):
         tbs[-1]["steps"].append({"op": m[2], "src": (m[3], int(m[4])), "dst": (m[5], int(m[6])), "cnt": int(m[7]),
                                  "seq": int(m[8]), "poff": int(m[9]), "deps": [d for d in m[10].split(",") if d],
                                  "post": [d for d in m[11].split(",") if d], "part": int(m[12]), "nparts": int(m[13]),
-                                 "fuse": int(m[14]), "pf": int(m[16]), "prog": bool(m[17])})
+                                 "fuse": int(m[14]), "pf": int(m[16]), "prog": 0 if not m[17] else 2 if m[17].endswith("2") else 1})
     return tbs
 
 
