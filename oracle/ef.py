@@ -160,6 +160,10 @@ def parse(text: str) -> Program:
     for d in filter(None, (root.get("dtypes") or "").split(",")):
         if d not in ("int32", "float32", "bfloat16"):
             raise ScheduleError("syntax", f"dtypes: unknown element type {d!r}")
+    # optional overlap="0|1": an execution hint for a runtime (warp-specialised send + reduce
+    # pairs); like dtypes it changes nothing the program computes
+    if (root.get("overlap") or "0") not in ("0", "1"):
+        raise ScheduleError("syntax", "overlap must be 0 or 1")
     gpus = [g for g in root if g.tag == "gpu"]
     if any(g.tag != "gpu" for g in root):
         raise ScheduleError("syntax", "<algo> may only contain <gpu>")

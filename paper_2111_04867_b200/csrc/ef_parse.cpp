@@ -214,6 +214,10 @@ Program parse_ef(const char* text, size_t len) {
       i = j + 1;
     }
   }
+  // optional overlap="1": an execution hint (a paired send and the receive-reduce after it
+  // run at once on the two halves of each CTA, plan.cpp mark_streamed); computes the same
+  prog.overlap = t.attrs.count("overlap") ? (int)to_int(t, "overlap", 0) : 0;
+  if (prog.overlap != 0 && prog.overlap != 1) fail("overlap must be 0 or 1");
   if (prog.nranks > 4096 || prog.p > 4096) fail("nranks or chunks_per_rank too large");
 
   // <gpu> elements

@@ -302,13 +302,14 @@ std::map<SKey, int> partial_flags(const Program& P, const HB& hb, const std::map
 // reaches the reduce when its peers' messages have landed too (paired send+rrc tbs) and the
 // progress stores would be pure cost. Both ends get KStep.prog; the kernel streams only when
 // KArgs.prog (the runtime turns it off in pull mode and for TMA pushes).
-// With TACCL_WARPSPEC=1 a member may also follow exactly one send without dependencies of its
-// own (paired send + rrc threadblocks, as the direct schedules lower): such a member gets
+// With the program's overlap="1" hint (or TACCL_WARPSPEC=1) a member may also follow exactly
+// one send without dependencies of its own (paired send + rrc threadblocks, as the direct schedules lower): such a member gets
 // prog = 2 and the kernel runs it beside that send — one half of the CTA's warps sends
 // (publishing groups) while the other half reduces the groups as they land (streamed_pair).
-void mark_streamed(std::vector<RankPlan>& plans) {
+void mark_streamed(std::vector<RankPlan>& plans, bool overlap) {
   const int n = (int)plans.size();
-  const bool pairs = getenv("TACCL_WARPSPEC") && atoi(getenv("TACCL_WARPSPEC"));
+  const char* ws = getenv("TACCL_WARPSPEC");  // A/B knob: 1 forces the pairs on, 0 off
+  const bool pairs = ws ? atoi(ws) != 0 : overlap;
   auto first_data = [&](const RankPlan& rp, const KTB& kt, int k) {
     for (int q = 0; q < k; ++q) {
       const KStep& y = rp.steps[kt.step_begin + q];
@@ -787,7 +788,7 @@ std::vector<RankPlan> build_plans(const Program& P, bool fuse, bool fuse_rrcs, b
           }
         }
       }
-  mark_streamed(plans);
+  mark_streamed(plans, P.overlap != 0);
   merged_order(plans);
   return plans;
 }

@@ -46,6 +46,7 @@ struct Program {
   int nranks = 0, p = 1, instances = 1;
   uint64_t min_bytes = 0, max_bytes = 0;  // max_bytes == UINT64_MAX means inf
   uint32_t dtypes = 7;                    // bit taccl_dtype_t: element types it is selected for
+  int overlap = 0;                        // execution hint: warp-specialised send + reduce pairs
   std::vector<Gpu> gpus;
 };
 

@@ -7,11 +7,12 @@ from .tuned import default_schedules  # noqa: F401
 
 
 def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=float("inf"), pair=True, merge=True,
-             dtypes=None, **kw):
+             dtypes=None, overlap=False, **kw):
     """EF v1 text for (collective, algorithm) — the one-call entry the CLI and tests use.
     pair=False lowers sends and receives into separate threadblocks; pair="peer" pairs only by
     peer (no relay-first threadblocks, lowering.py); merge=False keeps every transfer its own
-    step (no contiguity coalescing, lowering.coalesce)."""
+    step (no contiguity coalescing, lowering.coalesce); overlap=True adds the overlap="1"
+    execution hint (warp-specialised send + receive-reduce pairs, docs/SCHEDULE.md)."""
     if algo == "nvls":  # multicast reduce through the switch: written directly (templates.nvls_text)
         return templates.nvls_text(coll, nranks, chunks, instances, min_bytes, max_bytes, dtypes)
     if algo == "rounds":  # all-pairs in rounds (A/B experiment, DESIGN.md §6 merged threadblocks)
@@ -37,8 +38,10 @@ def generate(coll, algo, nranks, chunks=1, instances=1, min_bytes=0, max_bytes=f
         name += "_peer"
     if not merge:
         name += "_nomerge"
+    if overlap:
+        name += "_ovl"
     return lower(alg, instances=instances, min_bytes=min_bytes, max_bytes=max_bytes, name=name, pair=pair,
-                 merge=merge, dtypes=dtypes)
+                 merge=merge, dtypes=dtypes, overlap=overlap)
 
 
 def _rounds(text, n):

@@ -272,7 +272,7 @@ def _ranges(ins):
 
 
 def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, name=None, pair=True,
-          merge=True, dtypes=None) -> str:
+          merge=True, dtypes=None, overlap=False) -> str:
     """Lower `alg` to EF v1 text (docs/SCHEDULE.md). pair: share one threadblock between the
     send to and the receive from the same peer (see _allocate_tbs); merge: coalesce final
     deliveries on a link into multi-chunk transfers (see coalesce)."""
@@ -287,7 +287,7 @@ def lower(alg: Algorithm, instances: int = 1, min_bytes=0, max_bytes=math.inf, n
     mx = "inf" if max_bytes == math.inf else str(int(max_bytes))
     out = [f'<algo name="{name or alg.name}" coll="{alg.coll}" nranks="{n}" chunks_per_rank="{p}" '
            f'instances="{instances}" minBytes="{int(min_bytes)}" maxBytes="{mx}" inplace="0"'
-           + (f' dtypes="{",".join(dtypes)}"' if dtypes else "") + '>']
+           + (f' dtypes="{",".join(dtypes)}"' if dtypes else "") + (' overlap="1"' if overlap else "") + '>']
     for r in range(n):
         lst = instrs[r]
         tbs, assign = _allocate_tbs(lst, pair)

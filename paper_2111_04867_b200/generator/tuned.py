@@ -22,8 +22,9 @@ WIDE = ("int32", "float32")
 def ranges(coll: str, n: int):
     """[(algo, min_bytes, max_bytes[, dtypes])] covering [0, inf) for `coll` at n ranks, for
     every element type; algo may carry a chunk-partitioning suffix `_pK` (K chunks per rank,
-    PAPER.md:702-711) and then `_split` (sends and receives lowered into separate threadblocks,
-    generate(pair=False)); an entry with a dtypes tuple is selected only for those types."""
+    PAPER.md:702-711), then `_split` (sends and receives lowered into separate threadblocks,
+    generate(pair=False)) and then `_ovl` (the overlap="1" execution hint: warp-specialised send +
+    receive-reduce pairs); an entry with a dtypes tuple is selected only for those types."""
     if n == 1:
         return [("direct", 0, INF)]
     if coll == "allgather":
@@ -89,8 +90,10 @@ def default_schedules(coll: str, n: int, multicast: bool = True):
     out = []
     extra = multicast_ranges(coll, n) if multicast else []
     for algo, lo, hi, *dt in ranges(coll, n) + extra:
+        ovl = algo.endswith("_ovl")
+        algo = algo.removesuffix("_ovl")
         split = algo.endswith("_split")
         name, _, p = algo.removesuffix("_split").partition("_p")
         out.append(generate(coll, name, n, int(p) if p else 1, 1, min_bytes=lo, max_bytes=hi,
-                            pair=not split, dtypes=dt[0] if dt else None))
+                            pair=not split, dtypes=dt[0] if dt else None, overlap=ovl))
     return out

@@ -63,10 +63,12 @@ def test_streamed_split_schedules_exact(coll, algo, n, p, dtype, knob):
 
 @pytest.mark.parametrize("coll,n", [("reducescatter", 4), ("allreduce", 4), ("reducescatter", 8)])
 @pytest.mark.parametrize("kind", ["uniform", "normal"])
-def test_streamed_bf16_fused_rounding_bit_exact(coll, n, kind):
+@pytest.mark.parametrize("form", ["split", "overlap"])
+def test_streamed_bf16_fused_rounding_bit_exact(coll, n, kind, form):
     # non-integer bf16: the fused chain's fp32 sum in chain order, rounded once (reading R3), is
-    # the same whether the stripes are reduced as they land or after the whole message
-    text = generate(coll, "direct", n, 1, 1, pair=False)
+    # the same whether the stripes are reduced as they land (split lowering, or beside the send
+    # on half the warps: overlap="1") or after the whole message
+    text = generate(coll, "direct", n, 1, 1, pair=form != "split", overlap=form == "overlap")
     count = 40000 if coll == "allreduce" else 10000
     e_in = n * count if coll == "reducescatter" else count
     ins = [allreduce_input(e_in, "bfloat16", kind, 33, r) for r in range(n)]
@@ -133,20 +135,11 @@ def test_streamed_piece_with_more_groups_than_the_word_holds():
 @pytest.mark.parametrize("knob", [{}, {"TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "4096"},
                                   {"TACCL_LANES": "3", "TACCL_STRIPE": "8192"}])
 def test_warp_specialised_pairs(coll, n, p, dtype, knob):
-    # TACCL_WARPSPEC=1: the paired lowering's send + receive-reduce threadblocks run both steps
-    # at once on the two halves of each CTA (streamed_pair, prog 2)
-    env = {"TACCL_WARPSPEC": "1", **knob}
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        text = generate(coll, "direct", n, p, 1)
-        assert " prog2" in taccl.plan_dump(text, 0) or (coll == "allreduce" and n == 2)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+    # overlap="1": the paired lowering's send + receive-reduce threadblocks run both steps at
+    # once on the two halves of each CTA (streamed_pair, prog 2)
+    text = generate(coll, "direct", n, p, 1, overlap=True)
+    assert " prog2" in taccl.plan_dump(text, 0)
+    env = dict(knob)
     c_e = 12289 if dtype == "bfloat16" else 6151
     count = p * c_e * (n if coll == "allreduce" else 1)
     kind = "bits" if dtype == "int32" else "intval"

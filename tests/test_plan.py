@@ -266,3 +266,29 @@ def test_streamed_plain_rrc_is_not_pulled():
         send = [x for x in steps if x["op"] == "SEND"]
         assert rrc and all(x["prog"] and x["poff"] == -1 for x in rrc)
         assert send and all(x["prog"] and x["poff"] == -1 for x in send)
+
+
+def test_overlap_hint_pairs_sends_with_their_receive_reduces(monkeypatch):
+    # overlap="1" (docs/SCHEDULE.md): the paired direct schedules' receive-reduces run beside
+    # the send before them (prog 2) and their input sends stream; without the hint nothing
+    # streams; TACCL_WARPSPEC=0 turns the hint off, =1 forces it on
+    monkeypatch.delenv("TACCL_WARPSPEC", raising=False)
+    for coll, n in (("reducescatter", 4), ("allreduce", 4), ("reducescatter", 8)):
+        hinted, plain = generate(coll, "direct", n, 1, 1, overlap=True), generate(coll, "direct", n, 1, 1)
+        assert 'overlap="1"' in hinted and "overlap" not in plain
+        red = [x for tb in plan(hinted, 0) for x in tb["steps"] if x["op"] == "RRC_FUSED"]
+        assert red and all(x["prog"] == 2 for x in red)
+        assert not any(x["prog"] for tb in plan(plain, 0) for x in tb["steps"])
+        monkeypatch.setenv("TACCL_WARPSPEC", "0")
+        assert not any(x["prog"] == 2 for tb in plan(hinted, 0) for x in tb["steps"])
+        monkeypatch.setenv("TACCL_WARPSPEC", "1")
+        assert any(x["prog"] == 2 for tb in plan(plain, 0) for x in tb["steps"])
+        monkeypatch.delenv("TACCL_WARPSPEC")
+
+
+def test_overlap_attribute_is_validated_by_both_checkers():
+    import oracle
+    text = generate("reducescatter", "direct", 4, 1, 1, overlap=True)
+    assert oracle.validate(text).ok and taccl.validate(text, True)[0]
+    bad = text.replace('overlap="1"', 'overlap="2"')
+    assert oracle.validate(bad).kind == "syntax" and taccl.validate(bad, True)[:2] == (False, "syntax")

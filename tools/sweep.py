@@ -33,14 +33,15 @@ def gen(coll, al, n):
     if al == "auto":  # the size-specialised default set (generator/tuned.py)
         from paper_2111_04867_b200.generator.tuned import default_schedules
         return default_schedules(coll, n)
-    """algorithm name -> EF text. name[_pP][_mM][_split|_peer]: chunks per rank P, instances M
+    """algorithm name -> EF text. name[_pP][_mM][_split|_peer][_ovl]: chunks per rank P, instances M
     (PAPER.md:702-711, 785-789); _split = sends and receives in separate threadblocks;
-    _peer = same-peer threadblock pairing only (no relay-first pairing)"""
+    _peer = same-peer threadblock pairing only (no relay-first pairing); _ovl = the overlap="1"
+    execution hint (warp-specialised send + receive-reduce pairs)"""
     parts = al.split("_")
     p = next((int(x[1:]) for x in parts[1:] if x[:1] == "p" and x[1:].isdigit()), 1)
     m = next((int(x[1:]) for x in parts[1:] if x[:1] == "m" and x[1:].isdigit()), 1)
     pair = False if "split" in parts[1:] else "peer" if "peer" in parts[1:] else True
-    return generate(coll, parts[0], n, p, m, pair=pair)
+    return generate(coll, parts[0], n, p, m, pair=pair, overlap="ovl" in parts[1:])
 
 
 def cpu_model():
