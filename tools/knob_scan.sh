@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 out=gpurun_out/knob_scan_${1:-s}.txt; : > $out
 for env in ${ENVS:-base}; do
   e=${env//,/ }; [ "$e" = base ] && e="X=1"
-  env $e timeout 600 $TR --master-port 29671 tools/sweep.py --graph $POOL --colls ${COLLS:-reducescatter} --size-lo ${LO:-24} --size-hi ${HI:-28} ${SIZES:+--sizes $SIZES} \
+  env $e timeout 600 $TR --master-port 29671 tools/sweep.py --graph $POOL ${DTYPE:+--dtype $DTYPE} --colls ${COLLS:-reducescatter} --size-lo ${LO:-24} --size-hi ${HI:-28} ${SIZES:+--sizes $SIZES} \
     $( [ $env = base ] || echo --no-nccl ) --algos ${ALGOS:-direct} --out gpurun_out/knob_tmp.jsonl > /dev/null 2>&1
   echo "== $env" >> $out
   python tools/show_sweep.py gpurun_out/knob_tmp.jsonl >> $out; rm -f gpurun_out/knob_tmp.jsonl
