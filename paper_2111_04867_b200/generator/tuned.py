@@ -35,36 +35,39 @@ def ranges(coll: str, n: int):
         if n == 2:
             return [("oneshot", 0, 16 * MiB), ("direct", 16 * MiB, INF)]
         small = MiB // 2 if n <= 4 else MiB // 4
-        if n >= 8:
-            return [("oneshot", 0, small), ("direct", small, INF)]
-        # below 128 MiB the direct schedule (multi-input reduce with every load in flight) is
+        if n >= 8:  # extrapolated from n = 4 (no 8-GPU box): overlap pairs from 64 MiB
+            return [("oneshot", 0, small), ("direct", small, 64 * MiB), ("direct_ovl", 64 * MiB, INF)]
+        # below 64 MiB the direct schedule (multi-input reduce with every load in flight) is
         # ahead of the ring (r01_sweep_n4_graph.jsonl: 64 MiB 185 vs 203 us). bf16: a ring
-        # carries fp32 partials on its n-2 middle hops (reading R6; 2x those bytes), so direct
-        # stays ahead at every size (profiles/r02_sweep_ar_ring_ab_n4.txt: 128 MiB 366 vs 463
-        # us, 512 MiB 1356 vs 1723). int32/fp32 partials are the values themselves: there the
-        # relay-first ring (one recv-reduce-copy-send pass per hop) is ahead from 128 MiB
-        # (profiles/r02_sweep_n4_fp32_ar.txt: 128 MiB 329 vs 350 us, 1 GiB 2436 vs 2676; ring_p2
-        # 2493)
-        # bf16 from 128 MiB: all-pairs RS + ring AG ("dring": one AG connection per GPU) edges
-        # out direct (profiles/r02_ar_dring_n4.txt: 512 MiB 1277 vs 1296 us, 1 GiB 2499 vs 2560)
-        return [("oneshot", 0, small), ("direct", small, 128 * MiB), ("dring", 128 * MiB, INF, BF16),
-                ("ring", 128 * MiB, INF, WIDE)]
+        # carries fp32 partials on its n-2 middle hops (reading R6; 2x those bytes), so rings
+        # are out (profiles/r02_sweep_ar_ring_ab_n4.txt: 128 MiB 366 vs 463 us, 512 MiB 1356 vs
+        # 1723). From 64 MiB the overlap hint (each paired send and the receive-reduce after it
+        # run at once on the two halves of every CTA, the reduce consuming stripes as they land)
+        # removes the reduce tail between the two phases (profiles/r02_knob_scan_overlap_n4.txt:
+        # bf16 64 MiB 181 vs 187 us, 128 MiB 327 vs 357, 1 GiB 2381 vs 2557); from 256 MiB the
+        # all-pairs RS + ring AG ("dring": one AG connection per GPU) with the hint is ahead
+        # (512 MiB 1180 vs 1208, 1 GiB 2358 vs 2381); fp32/int32 the same shape from 128 MiB
+        # (fp32 512 MiB 1189 vs ring 1209 and direct+hint 1211)
+        return [("oneshot", 0, small), ("direct", small, 64 * MiB), ("direct_ovl", 64 * MiB, 256 * MiB, BF16),
+                ("dring_ovl", 256 * MiB, INF, BF16), ("direct_ovl", 64 * MiB, 128 * MiB, WIDE),
+                ("dring_ovl", 128 * MiB, INF, WIDE)]
     if coll == "reducescatter":
         if n == 2:
             # from 256 MiB the split lowering's streamed push reduce beats the paired schedule's
-            # in-place pull (1 GiB 800 vs 833 us, 256 MiB 221 vs 223; profiles/r02_knob_scan_split_n2.txt)
+            # in-place pull (1 GiB 800 vs 833 us, 256 MiB 221 vs 223; profiles/r02_knob_scan_split_n2.txt);
+            # the overlap hint loses at n=2 (1 GiB 877 us, r02_knob_scan_overlap_n4.txt)
             return [("direct", 0, 256 * MiB), ("direct_split", 256 * MiB, INF)]
-        if n >= 8:
-            return [("direct", 0, INF)]
+        if n >= 8:  # extrapolated from n = 4 (no 8-GPU box)
+            return [("direct", 0, 80 * MiB), ("direct_ovl", 80 * MiB, INF)]
         # bf16 rings carry fp32 partials on n-2 of n-1 hops (reading R6): 0.58-0.72x NCCL at
-        # 32 MiB-1 GiB (profiles/r02_sweep_n4_graph.txt), so bf16 stays direct; int32/fp32 keep
-        # round 1's ring from 32 MiB (ahead of the streamed split schedule too up to 512 MiB,
-        # profiles/r02_knob_scan_prog_n4.txt fp32 rows: 128 MiB 173.5 vs 182.6 us). bf16 from
-        # 80 MiB: sends and receive-reduces in separate threadblocks, each reduce streamed as
-        # its stripes land (plan.cpp mark_streamed) — 96 MiB 146 vs 154 us, 128 MiB 187 vs 202,
-        # 1 GiB 1264 vs 1369 (the paired schedule's pulled chains)
-        return [("direct", 0, 32 * MiB), ("direct", 32 * MiB, 80 * MiB, BF16), ("direct_split", 80 * MiB, INF, BF16),
-                ("ring", 32 * MiB, INF, WIDE)]
+        # 32 MiB-1 GiB (profiles/r02_sweep_n4_graph.txt), so bf16 stays all-pairs; from 80 MiB
+        # with the overlap hint (warp-specialised send + streamed reduce pairs; profiles/
+        # r02_knob_scan_overlap_n4.txt: 96 MiB 147 vs 155 us, 128 MiB 186 vs 203, 1 GiB 1231 vs
+        # 1372; the split lowering's streamed reduces 147 / 187 / 1279). int32/fp32 keep round
+        # 1's relay-first ring from 32 MiB up to 512 MiB, the hinted all-pairs schedule above
+        # (fp32 768 MiB 935 vs 953 us, 1 GiB 1232 vs 1266)
+        return [("direct", 0, 32 * MiB), ("direct", 32 * MiB, 80 * MiB, BF16), ("direct_ovl", 80 * MiB, INF, BF16),
+                ("ring", 32 * MiB, 512 * MiB, WIDE), ("direct_ovl", 512 * MiB, INF, WIDE)]
     raise ValueError(coll)
 
 
