@@ -115,12 +115,18 @@ __device__ __forceinline__ void st_v4_cs(int4* p, int4 v) {
                : "memory");
 }
 
-// The CTA-wide data loops run on the whole CTA, or (s_half, warp-specialised pairs: half the
-// warps send while the other half reduces, streamed_pair) on one half of it: thread index and
-// count within the running half.
+// The CTA-wide data loops run on the whole CTA, or (s_half = b > 0, warp-specialised pairs:
+// threads [0, b) send while [b, T) reduce, streamed_pair) on one part of it: thread index and
+// count within the running part.
 __shared__ int s_half;
-__device__ __forceinline__ int grp_tid() { return s_half ? (int)(threadIdx.x % (blockDim.x / 2)) : (int)threadIdx.x; }
-__device__ __forceinline__ int grp_nt() { return s_half ? (int)blockDim.x / 2 : (int)blockDim.x; }
+__device__ __forceinline__ int grp_tid() {
+  const int b = s_half, t = threadIdx.x;
+  return b == 0 ? t : t < b ? t : t - b;
+}
+__device__ __forceinline__ int grp_nt() {
+  const int b = s_half;
+  return b == 0 ? (int)blockDim.x : (int)threadIdx.x < b ? b : (int)blockDim.x - b;
+}
 
 // U 16-byte vectors in flight per thread; CS: streaming (evict-first) stores
 template <int U, bool CS>
@@ -1059,7 +1065,8 @@ __device__ __forceinline__ bool streamed_pair(const Ctx& c, const KStep& snd, co
                                               const char** s_stage, volatile int* abort) {
   const KArgs& A = *c.a;
   const KRank& R = *c.r;
-  const int j = c.j, tid = threadIdx.x, half = blockDim.x / 2;
+  // send part: A.pair_send threads (a multiple of 32; default half the CTA)
+  const int j = c.j, tid = threadIdx.x, half = A.pair_send, rest = blockDim.x - half;
   const bool fz = rrc.op == K_RRC_FUSED;
   if (tid == 0) {  // the receive-reduce's staging slots (push mode: streaming is off in pull mode)
     if (fz)
@@ -1067,7 +1074,7 @@ __device__ __forceinline__ bool streamed_pair(const Ctx& c, const KStep& snd, co
         s_stage[f] = local_base(c, KB_STAGE) + (int64_t)fused[kFuseStride * (rrc.fuse_begin + f) + 2] * cbytes;
     else
       s_stage[0] = local_base(c, KB_STAGE) + (int64_t)rrc.soff * cbytes;
-    s_half = 1;
+    s_half = half;
   }
   __syncthreads();
   if (tid < half) {  // send half
@@ -1116,7 +1123,7 @@ __device__ __forceinline__ bool streamed_pair(const Ctx& c, const KStep& snd, co
             }
           }
         }
-        asm volatile("bar.sync 2, %0;" ::"r"(half) : "memory");
+        asm volatile("bar.sync 2, %0;" ::"r"(rest) : "memory");
         if (*abort) return;
       }
       ++ns;

@@ -234,6 +234,7 @@ struct KArgs {
   int32_t trace_ctas;         // CTAs that fit in the trace buffer
   int32_t ncta;               // grid size
   int32_t ready_per_piece;    // A/B knob (TACCL_READY_PER_PIECE): entry handshake per piece start
+  int32_t pair_send;          // warp-specialised pairs: threads of the send part (TACCL_PAIR_SEND_WARPS)
   int32_t prog;               // streamed messages: stripes per published group (0 = off; every
                               // rank of a call agrees: off in pull mode and with TMA pushes)
   int32_t pull;               // pull mode (direct kernel): a receive-reduce whose matched send

@@ -133,7 +133,8 @@ def test_streamed_piece_with_more_groups_than_the_word_holds():
                                       ("reducescatter", 8, 1), ("allreduce", 4, 1), ("allreduce", 8, 1)])
 @pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
 @pytest.mark.parametrize("knob", [{}, {"TACCL_PROG_STRIPES": "1", "TACCL_STRIPE": "4096"},
-                                  {"TACCL_LANES": "3", "TACCL_STRIPE": "8192"}])
+                                  {"TACCL_LANES": "3", "TACCL_STRIPE": "8192"},
+                                  {"TACCL_PAIR_SEND_WARPS": "12"}, {"TACCL_PAIR_SEND_WARPS": "3"}])
 def test_warp_specialised_pairs(coll, n, p, dtype, knob):
     # overlap="1": the paired lowering's send + receive-reduce threadblocks run both steps at
     # once on the two halves of each CTA (streamed_pair, prog 2)
