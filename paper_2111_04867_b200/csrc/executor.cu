@@ -118,15 +118,14 @@ __device__ __forceinline__ void st_v4_cs(int4* p, int4 v) {
 // The CTA-wide data loops run on the whole CTA, or (s_half = b > 0, warp-specialised pairs:
 // threads [0, b) send while [b, T) reduce, streamed_pair) on one part of it: thread index and
 // count within the running part.
-// (s_pub: the send part's first warp publishes progress and copies nothing)
-__shared__ int s_half, s_pub;
+__shared__ int s_half;
 __device__ __forceinline__ int grp_tid() {
   const int b = s_half, t = threadIdx.x;
-  return b == 0 ? t : t < b ? t - s_pub : t - b;
+  return b == 0 ? t : t < b ? t : t - b;
 }
 __device__ __forceinline__ int grp_nt() {
   const int b = s_half;
-  return b == 0 ? (int)blockDim.x : (int)threadIdx.x < b ? b - s_pub : (int)blockDim.x - b;
+  return b == 0 ? (int)blockDim.x : (int)threadIdx.x < b ? b : (int)blockDim.x - b;
 }
 
 // U 16-byte vectors in flight per thread; CS: streaming (evict-first) stores
@@ -1076,34 +1075,25 @@ __device__ __forceinline__ bool streamed_pair(const Ctx& c, const KStep& snd, co
     else
       s_stage[0] = local_base(c, KB_STAGE) + (int64_t)rrc.soff * cbytes;
     s_half = half;
-    s_pub = 32;
   }
   __syncthreads();
-  if (tid < half) {  // send part: warp 0 publishes, the other warps copy
+  if (tid < half) {  // send half
     int64_t ns = 0;
     for_piece(stripe, j, nsplit, snd.cnt, cbytes, [&](int64_t, int64_t) { ++ns; });
     const int64_t G = max((int64_t)A.prog, (ns + kProgGroups - 1) / kProgGroups);
-    const int64_t ngroups = (ns + G - 1) / G;
-    // named barriers: full[g & 1] (ids 1, 3: the copy warps finished group g), empty[g & 1]
-    // (ids 4, 5: the publisher took group g, so full[g & 1] may be reused for group g + 2).
-    // The copy warps only arrive on full, so they run ahead of the fence and the word
-    // while the publisher warp waits for them.
-    if (tid < 32) {
-      u64* slot = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffProg) + flag_slot(R.rank, tb.chan, j);
-      const u64 key = prog_key(c.epoch, snd.seq);
-      for (int64_t g = 0; g < ngroups; ++g) {
-        asm volatile("bar.sync %0, %1;" ::"r"(g & 1 ? 3 : 1), "r"(half) : "memory");
-        if (g + 2 < ngroups) asm volatile("bar.arrive %0, %1;" ::"r"(g & 1 ? 5 : 4), "r"(half) : "memory");
-        if (tid == 0) prog_publish(slot, key, g + 1);
+    u64* slot = reinterpret_cast<u64*>(R.peer_arena[tb.send] + kOffProg) + flag_slot(R.rank, tb.chan, j);
+    const u64 key = prog_key(c.epoch, snd.seq);
+    ns = 0;
+    for_piece(stripe, j, nsplit, snd.cnt, cbytes, [&](int64_t off, int64_t len) {
+      cta_copy(A.variant, sdst + off, ssrc + off, len);
+      if (++ns % G == 0) {
+        asm volatile("bar.sync 1, %0;" ::"r"(half) : "memory");
+        if (tid == 0) prog_publish(slot, key, ns / G);
       }
-    } else {
-      int64_t q = 0;
-      for_piece(stripe, j, nsplit, snd.cnt, cbytes, [&](int64_t off, int64_t len) {
-        const int64_t g = q / G;
-        if (q % G == 0 && g >= 2) asm volatile("bar.sync %0, %1;" ::"r"(g & 1 ? 5 : 4), "r"(half) : "memory");
-        cta_copy(A.variant, sdst + off, ssrc + off, len);
-        if (++q % G == 0 || q == ns) asm volatile("bar.arrive %0, %1;" ::"r"(g & 1 ? 3 : 1), "r"(half) : "memory");
-      });
+    });
+    if (ns % G) {
+      asm volatile("bar.sync 1, %0;" ::"r"(half) : "memory");
+      if (tid == 0) prog_publish(slot, key, ns / G + 1);
     }
   } else {  // reduce half
     const char* rsrc = local_base(c, rrc.srcbuf) + (int64_t)rrc.srcoff * cbytes;
@@ -1148,7 +1138,7 @@ __device__ __forceinline__ bool streamed_pair(const Ctx& c, const KStep& snd, co
     });
   }
   __syncthreads();
-  if (tid == 0) s_half = s_pub = 0;
+  if (tid == 0) s_half = 0;
   __syncthreads();
   return !*abort;
 }
@@ -1219,7 +1209,7 @@ __global__ void __launch_bounds__(LL ? kThreadsLL : kThreads, LL ? 1 : kDirectPe
     const u64 ep = *reinterpret_cast<volatile u64*>(&ctrl->epoch);
     s_epoch = ep;
     s_abort = 0;
-    s_half = s_pub = 0;
+    s_half = 0;
     // arrival: the rank's CTA 0 advances the epoch at its end once every other CTA of the
     // rank has read it. The added value depends on the loaded epoch (always 1), so the
     // reduction cannot overtake the load.

@@ -486,7 +486,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   // pull mode (nothing is pushed) and with TMA pushes (their stores complete asynchronously)
   A.prog = (A.pull || A.tma == 2) ? 0 : (int)env_size("TACCL_PROG_STRIPES", 2);
   // warp-specialised pairs: warps of the send part (of 16; A/B knob, default half)
-  A.pair_send = 32 * (int)std::min<size_t>(15, std::max<size_t>(2, env_size("TACCL_PAIR_SEND_WARPS", 8)));
+  A.pair_send = 32 * (int)std::min<size_t>(15, std::max<size_t>(1, env_size("TACCL_PAIR_SEND_WARPS", 8)));
   std::string err;
   const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
