@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Time one schedule with all ranks emulated on cuda:0 (one launch per call).
-  python tools/emu_time.py --coll allreduce --algo ring --n 4 --bytes 268435456 [--iters 20]"""
+  python tools/emu_time.py --coll allreduce --algo ring --n 4 --bytes 268435456 [--iters 20] [--overlap] [--split]"""
 import argparse
 import os
 import sys
@@ -20,10 +20,12 @@ ap.add_argument("--chunks", type=int, default=1)
 ap.add_argument("--instances", type=int, default=1)
 ap.add_argument("--bytes", type=int, default=1 << 28)
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--overlap", action="store_true", help='the overlap="1" hint (warp-specialised pairs)')
+ap.add_argument("--split", action="store_true", help="sends and receives in separate threadblocks")
 a = ap.parse_args()
 n = a.n
 comm = taccl.Comm(nranks=n, device=0, emulated=True, scratch_bytes=2 * a.bytes + (64 << 20))
-comm.load(generate(a.coll, a.algo, n, a.chunks, a.instances))
+comm.load(generate(a.coll, a.algo, n, a.chunks, a.instances, pair=not a.split, overlap=a.overlap))
 es = 2
 count = a.bytes // es // (1 if a.coll == "allreduce" else n)
 e_in = n * count if a.coll in ("alltoall", "reducescatter") else count
