@@ -29,6 +29,7 @@ ap.add_argument("--emulated", action="store_true")
 ap.add_argument("--calls", type=int, default=1, help="traced back-to-back calls (last one shown)")
 ap.add_argument("--pair", default="1", help="1 (default pairing), peer, or split (sends and receives in separate tbs)")
 ap.add_argument("--summary", action="store_true", help="per (rank, tb): median of every stamp instead of every CTA")
+ap.add_argument("--overlap", action="store_true", help='the overlap="1" hint (warp-specialised pairs)')
 a = ap.parse_args()
 world = int(os.environ.get("WORLD_SIZE", "1"))
 rank = int(os.environ.get("RANK", "0"))
@@ -38,7 +39,8 @@ if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
 emu = world == 1
 comm = taccl.Comm(rank=rank, nranks=n, device=torch.cuda.current_device(), emulated=emu, scratch_bytes=64 << 20)
-comm.load(generate(a.coll, a.algo, n, a.chunks, 1, pair={"1": True, "peer": "peer", "split": False}[a.pair]))
+comm.load(generate(a.coll, a.algo, n, a.chunks, 1, pair={"1": True, "peer": "peer", "split": False}[a.pair],
+                   overlap=a.overlap))
 es = 2
 S = a.bytes
 count = {"allgather": S // es // n, "alltoall": S // es // n, "allreduce": S // es,
