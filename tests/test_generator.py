@@ -212,9 +212,11 @@ def test_default_sets_cover_all_sizes_once(coll, n):
         assert rs[0][1] == 0 and rs[-1][2] == math.inf
         for (_, _, hi), (_, lo, _) in zip(rs, rs[1:]):
             assert hi == lo
+    from paper_2111_04867_b200 import taccl
     for text in default_schedules(coll, n):
         v = oracle.validate(text)
         assert v.ok, f"{v.kind}: {v.msg}"
+        assert taccl.validate(text, True)[0]  # the C++ loader's checks too (overlap hints included)
 
 
 # ---------------------------------------------------------------- contiguity (lowering.coalesce)
