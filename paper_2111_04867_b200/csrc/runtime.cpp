@@ -460,14 +460,19 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
         A.cta_map[cta++] = cta_pack((int)i, 0, c, G.dep_ctas, 0) | kCtaMerged;
       }
     }
-    for (int t = 0; t < dp.ntb && !G.merged; ++t) {
-      const int ind = a->indep[r][t];
-      const int ct = G.ct[r][t];
-      for (int c = 0; c < ct; ++c) {
+    // CTA order within the rank: threadblock by threadblock, or (TACCL_CTA_ORDER=1, A/B knob)
+    // round-robin over the threadblocks so every block index range mixes all connections
+    const bool rr = env_size("TACCL_CTA_ORDER", 0) == 1;
+    int maxct = 0;
+    for (int t = 0; t < dp.ntb && !G.merged; ++t) maxct = std::max(maxct, G.ct[r][t]);
+    for (int o = 0; o < (rr ? maxct : dp.ntb) && !G.merged; ++o)
+      for (int q = 0; q < (rr ? dp.ntb : G.ct[r][o]); ++q) {
+        const int t = rr ? q : o, c = rr ? o : q;
+        const int ct = G.ct[r][t];
+        if (c >= ct) continue;
         if (cta >= kMaxGrid) return fail(TACCL_ERR_UNSUPPORTED, "launch exceeds " + std::to_string(kMaxGrid) + " CTAs");
-        A.cta_map[cta++] = cta_pack((int)i, t, c, ct, ind);
+        A.cta_map[cta++] = cta_pack((int)i, t, c, ct, a->indep[r][t]);
       }
-    }
     R.ncta = cta - first;
   }
   A.ncta = cta;
