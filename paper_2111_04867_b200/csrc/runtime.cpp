@@ -460,9 +460,11 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
         A.cta_map[cta++] = cta_pack((int)i, 0, c, G.dep_ctas, 0) | kCtaMerged;
       }
     }
-    // CTA order within the rank: threadblock by threadblock, or (TACCL_CTA_ORDER=1, A/B knob)
-    // round-robin over the threadblocks so every block index range mixes all connections
-    const bool rr = env_size("TACCL_CTA_ORDER", 0) == 1;
+    // CTA order within the rank: round-robin over the threadblocks (CTA k of every tb, then
+    // k + 1, ...), so every range of block indices — and with it every group of SMs the block
+    // scheduler fills — mixes all connections (A2A n=4 1 GiB 1162 vs 1203 us, AR 64 MiB 176 vs
+    // 180; profiles/r02_knob_scan_cta_order_n4.txt). TACCL_CTA_ORDER=0: tb by tb (A/B knob)
+    const bool rr = env_size("TACCL_CTA_ORDER", 1) == 1;
     int maxct = 0;
     for (int t = 0; t < dp.ntb && !G.merged; ++t) maxct = std::max(maxct, G.ct[r][t]);
     for (int o = 0; o < (rr ? maxct : dp.ntb) && !G.merged; ++o)
