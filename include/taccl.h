@@ -88,7 +88,9 @@ taccl_result_t taccl_validate(const char* text, size_t len, int direct_store);
  * step: "  <k> <OP> src=<buf>:<off> dst=<buf>:<off> cnt=<n> seq=<s> poff=<o> deps=<t:k,...>
  * post=<t:k,...> part=<i>/<n> fuse=<count> fwd=<count>". For tests and inspection of the
  * plan transformations (chain fusion, rrc+send fusion, pull-mode marking).
- * Env knobs that shape plans at load (TACCL_NO_FUSE, TACCL_PULL_KINDS, ...) apply.
+ * Env knobs that shape plans at load (TACCL_NO_FUSE, TACCL_PULL_KINDS, ...) apply; the
+ * per-call knobs (TACCL_STAGED_MAX, TACCL_MIN_PIECE, TACCL_PROG_STRIPES, ...) are also re-read
+ * here (and at communicator creation), not on every taccl_run.
  * Errors: INVALID_ARG (null pointers, rank out of range), INVALID_SCHEDULE. */
 taccl_result_t taccl_plan_dump(const char* text, size_t len, int rank, int ll, char* out, size_t cap,
                                size_t* needed);

@@ -1739,15 +1739,19 @@ __global__ void __launch_bounds__(512, 2) taccl_mr_kernel(const __grid_constant_
 }  // namespace
 
 int mr_grid(int device) {
-  static int sms = 0;
-  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
+  // computed once per process (the occupancy query and the env read cost host time per call)
+  static int grid = 0;
+  if (grid) return grid;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
   int per = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, taccl_mr_kernel, 512, 0) != cudaSuccess || per < 1) per = 1;
   // one CTA per SM measured best (profiles/r02_nvls_lean_scan_n4.txt: 64 MiB 170.6 us at 1,
   // 182 at 2-4; 1 MiB 24.3 vs 31.7); TACCL_MR_CTAS_PER_SM overrides
   const char* e = getenv("TACCL_MR_CTAS_PER_SM");
   const int want = e && atoi(e) > 0 ? atoi(e) : 1;
-  return sms * std::min(per, want);
+  grid = sms * std::min(per, want);
+  return grid;
 }
 
 int launch_mr(const KArgs& a, int64_t src_off, int64_t dst_off, int64_t bytes, int grid, void* stream, std::string* err) {

@@ -122,6 +122,30 @@ size_t env_size(const char* name, size_t dflt) {
   return (size_t)strtoull(v, nullptr, 10);
 }
 
+// Per-call knobs, read from the environment when a communicator is created and whenever an
+// algorithm is loaded (taccl.h), not on every call: ~20 getenv scans of a 130-entry
+// environment cost ~3.4 us of host time per eager call.
+enum Knob {
+  KN_LANES, KN_STAGED_MAX, KN_LL_MIN_PIECE, KN_MIN_PIECE, KN_TARGET_CTAS, KN_MERGED, KN_DEP_WEIGHTED,
+  KN_PIECES_PER_CTA, KN_STRIPE, KN_LEAN_MAX, KN_MR_UNROLL, KN_COPY_VARIANT, KN_PULL, KN_PULL_CHAIN_MIN,
+  KN_CTA_ORDER, KN_TMA, KN_READY_PER_PIECE, KN_PROG_STRIPES, KN_PAIR_SEND_WARPS, KN_COUNT
+};
+const char* const kKnobNames[KN_COUNT] = {
+    "TACCL_LANES", "TACCL_STAGED_MAX", "TACCL_LL_MIN_PIECE", "TACCL_MIN_PIECE", "TACCL_TARGET_CTAS", "TACCL_MERGED",
+    "TACCL_DEP_WEIGHTED", "TACCL_PIECES_PER_CTA", "TACCL_STRIPE", "TACCL_LEAN_MAX", "TACCL_MR_UNROLL",
+    "TACCL_COPY_VARIANT", "TACCL_PULL", "TACCL_PULL_CHAIN_MIN", "TACCL_CTA_ORDER", "TACCL_TMA",
+    "TACCL_READY_PER_PIECE", "TACCL_PROG_STRIPES", "TACCL_PAIR_SEND_WARPS"};
+size_t g_knob_val[KN_COUNT];
+bool g_knob_set[KN_COUNT];
+void refresh_knobs() {
+  for (int k = 0; k < KN_COUNT; ++k) {
+    const char* v = getenv(kKnobNames[k]);
+    g_knob_set[k] = v && *v;
+    g_knob_val[k] = g_knob_set[k] ? (size_t)strtoull(v, nullptr, 10) : 0;
+  }
+}
+inline size_t knob(Knob k, size_t dflt) { return g_knob_set[k] ? g_knob_val[k] : dflt; }
+
 // one parity region of the staged (small-message) mode; both sit at the front of the arena's
 // scratch area at a fixed place for the communicator's lifetime
 int64_t staged_region_bytes() { return g.staged_bytes; }
@@ -139,6 +163,7 @@ taccl_result_t alloc_arena(char** out, size_t scratch) {
 
 taccl_result_t comm_common_init(int nranks, int device, size_t scratch) {
   if (g.up) return fail(TACCL_ERR_INVALID_ARG, "communicator already initialized");
+  refresh_knobs();
   if (nranks < 1 || nranks > kMaxRanks)
     return fail(TACCL_ERR_UNSUPPORTED, "nranks must be in [1, " + std::to_string(kMaxRanks) + "]");
   CUDA_TRY(cudaSetDevice(device));
@@ -231,7 +256,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   for (int r = 0; r < a->nranks; ++r)
     if (a->plans[r].mem) total_tb += a->ntb[r];
   int lanes = 1;
-  const size_t forced = env_size("TACCL_LANES", 0);
+  const size_t forced = knob(KN_LANES, 0);
   // staged (LL) mode for small messages: no entry handshake, no fences; sends write 16-byte
   // LL lines (8 payload bytes + flags) into the receiver's parity slot
   const int64_t sb = staged_region_bytes();
@@ -239,15 +264,15 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   const int64_t ll_cb = 16 * ((G->chunk_bytes + 7) / 8);
   // LL up to 2 MiB of output for AG/A2A/AR and 4 MiB for RS (measured crossovers vs the
   // direct kernel at n=2 and n=4, profiles/r01_ll_threshold.txt); TACCL_STAGED_MAX overrides
-  const int64_t ll_max = (int64_t)env_size("TACCL_STAGED_MAX", coll == TACCL_REDUCESCATTER ? (4 << 20) : (2 << 20));
+  const int64_t ll_max = (int64_t)knob(KN_STAGED_MAX, coll == TACCL_REDUCESCATTER ? (4 << 20) : (2 << 20));
   G->staged = (int64_t)a->max_stage2_chunks * ll_cb <= sb && total_bytes <= ll_max && !a->has_mr ? 1 : 0;
   // bytes per CTA: LL lines are latency-bound, so LL pieces are small (4 KiB of payload per
   // CTA measured best at n=2 up to 1 MiB, profiles/r01_small_sweep_n2.txt)
-  const int64_t min_piece = G->staged ? (int64_t)env_size("TACCL_LL_MIN_PIECE", 4 << 10)
-                                      : (int64_t)env_size("TACCL_MIN_PIECE", 64 << 10);
+  const int64_t min_piece = G->staged ? (int64_t)knob(KN_LL_MIN_PIECE, 4 << 10)
+                                      : (int64_t)knob(KN_MIN_PIECE, 64 << 10);
   // 128 CTAs x 512 threads measured best for the HBM copy and 2-GPU pushes, 148 (one per SM)
   // for 4 ranks (AR ring +5%, AG/A2A equal; profiles/r01_scan.txt, r01_envscan_n4.txt)
-  const int target = std::min(g.max_ctas, (int)env_size("TACCL_TARGET_CTAS", g.nranks >= 4 ? 148 : 128));
+  const int target = std::min(g.max_ctas, (int)knob(KN_TARGET_CTAS, g.nranks >= 4 ? 148 : 128));
   int nlocal = 0;
   for (int r = 0; r < a->nranks; ++r)
     if (a->plans[r].mem) ++nlocal;
@@ -255,13 +280,13 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   G->budget = std::max(1, target / std::max(1, nlocal));
   // merged execution (TACCL_MERGED=1, A/B knob; plan.cpp merged_order): every CTA of a rank
   // runs all of its threadblocks, so each step gets the rank's whole CTA budget
-  G->merged = !G->staged && a->mergeable && env_size("TACCL_MERGED", 0) != 0 ? 1 : 0;
+  G->merged = !G->staged && a->mergeable && knob(KN_MERGED, 0) != 0 ? 1 : 0;
   // CTAs left for the dependent tbs once independent tbs took their weight share, shared
   // equally among the dependent tbs (TACCL_DEP_WEIGHTED=1: by data-volume weight — measured
   // slower for split send/reduce tbs, the reduce side needs its CTAs for HBM bandwidth);
   // per_dep = the largest share, which sets the piece count
   int per_dep = 1;
-  const bool weighted = env_size("TACCL_DEP_WEIGHTED", 0) != 0;
+  const bool weighted = knob(KN_DEP_WEIGHTED, 0) != 0;
   std::vector<std::vector<int>> share(a->nranks);
   for (int r = 0; r < a->nranks; ++r) {
     if (!a->plans[r].mem) continue;
@@ -295,7 +320,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
     // when CTAs and bytes allow more pieces than m, m adds nothing (a multiple-of-m split
     // only cost CTAs: A2A n=4 1 GiB m=8 1284 vs 1197 us, profiles/r02_c3_grid_n4.txt)
     const int64_t step_bytes = (int64_t)a->max_steps_cnt * G->chunk_bytes;
-    const int64_t ppc = std::max<int64_t>(1, (int64_t)env_size("TACCL_PIECES_PER_CTA", 1));  // A/B knob
+    const int64_t ppc = std::max<int64_t>(1, (int64_t)knob(KN_PIECES_PER_CTA, 1));  // A/B knob
     const int64_t natural = std::max<int64_t>(1, std::min<int64_t>({step_bytes / min_piece, (int64_t)per_dep * ppc, (int64_t)kMaxSplit}));
     G->split = (int)std::min<int64_t>(kMaxSplit, std::max<int64_t>(a->instances, natural));
     lanes = (G->split + a->instances - 1) / a->instances;
@@ -306,7 +331,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
   while (gb < 4096 && G->chunk_bytes % (gb * 2) == 0) gb *= 2;
   // multicast reduces stream best in 16 KiB stripes (profiles/r02_nvls_scan_n4.txt: 64 MiB
   // 172 vs 183 us at 64 KiB)
-  const int64_t smax = (int64_t)env_size("TACCL_STRIPE", a->has_mr ? (16 << 10) : (64 << 10));
+  const int64_t smax = (int64_t)knob(KN_STRIPE, a->has_mr ? (16 << 10) : (64 << 10));
   int64_t st = gb;
   while (st * 2 <= smax && st * 2 * G->split <= G->chunk_bytes) st *= 2;
   G->stripe = st;
@@ -350,7 +375,7 @@ taccl_result_t geometry(const Algo* a, taccl_coll_t coll, size_t count, int elt,
 // faster (1 GiB: 6300 vs 6090 GB/s r+w), the lean kernel wins below (1 KB: 1.3 vs 3.2 us;
 // 64 MiB: 22.3 vs 23.5 us; profiles/r01_lean_copy_n1.txt)
 bool lean(const Algo* a, const Geometry& G) {
-  return a->lean_copy && (int64_t)a->lean_cnt * G.chunk_bytes < (int64_t)env_size("TACCL_LEAN_MAX", 256ull << 20);
+  return a->lean_copy && (int64_t)a->lean_cnt * G.chunk_bytes < (int64_t)knob(KN_LEAN_MAX, 256ull << 20);
 }
 
 taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int elt,
@@ -398,7 +423,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.nranks = g.nranks;
   // one multimem.ld_reduce in flight per thread measured best (profiles/r02_nvls_scan_n4.txt:
   // 64 MiB 173 us at 1, 177 at 2, 183 at 4, 194 at 8)
-  A.mr_unroll = (int)env_size("TACCL_MR_UNROLL", 1);
+  A.mr_unroll = (int)knob(KN_MR_UNROLL, 1);
   A.split = G.split;
   A.dep_ctas = G.dep_ctas;
   A.indep_cap = G.indep_cap;
@@ -408,7 +433,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.dtype = dtype;
   A.chunk_elems = G.ce;
   A.stripe = G.stripe;
-  A.variant = (int)env_size("TACCL_COPY_VARIANT", 0);
+  A.variant = (int)knob(KN_COPY_VARIANT, 0);
   A.scratch_off = G.scratch_off;
   A.staging_off = G.staging_off;
   A.shadow_off = G.shadow_off;
@@ -416,12 +441,12 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   A.timeout_ns = g.timeout_ns;
   A.trace = g.trace;
   A.trace_ctas = g.trace_ctas;
-  const bool pull_on = peer_in && !G.staged && g.nranks > 1 && env_size("TACCL_PULL", 1) != 0;
+  const bool pull_on = peer_in && !G.staged && g.nranks > 1 && knob(KN_PULL, 1) != 0;
   // (not for schedules with streamed reduces: those already overlap the reduce with the
   // transfers and lose to in-place chain loads' slower peer reads — RS n=4 1 GiB 1264 vs
   // 1369 us, profiles/r02_knob_scan_prog_n4.txt)
   const bool pull_chains = pull_on && !a->plans_pc.empty() && !a->has_prog &&
-                           G.chunk_bytes >= (int64_t)env_size("TACCL_PULL_CHAIN_MIN", 64ull << 20);
+                           G.chunk_bytes >= (int64_t)knob(KN_PULL_CHAIN_MIN, 64ull << 20);
   int cta = 0, smem = 0;
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
@@ -464,7 +489,7 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
     // k + 1, ...), so every range of block indices — and with it every group of SMs the block
     // scheduler fills — mixes all connections (A2A n=4 1 GiB 1162 vs 1203 us, AR 64 MiB 176 vs
     // 180; profiles/r02_knob_scan_cta_order_n4.txt). TACCL_CTA_ORDER=0: tb by tb (A/B knob)
-    const bool rr = env_size("TACCL_CTA_ORDER", 1) == 1;
+    const bool rr = knob(KN_CTA_ORDER, 1) == 1;
     int maxct = 0;
     for (int t = 0; t < dp.ntb && !G.merged; ++t) maxct = std::max(maxct, G.ct[r][t]);
     for (int o = 0; o < (rr ? maxct : dp.ntb) && !G.merged; ++o)
@@ -479,8 +504,8 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   }
   A.ncta = cta;
   A.plan_smem = smem <= kPlanSmemMax ? 1 : 0;
-  A.tma = (int)env_size("TACCL_TMA", 1);
-  A.ready_per_piece = (int)env_size("TACCL_READY_PER_PIECE", 0);
+  A.tma = (int)knob(KN_TMA, 1);
+  A.ready_per_piece = (int)knob(KN_READY_PER_PIECE, 0);
   // pull mode needs every peer's input mapped (registered, or in the symmetric arena) and
   // the direct kernel; TACCL_PULL=0 disables it
   // which receive-reduces pull is decided per step by the plan (TACCL_PULL_KINDS at load,
@@ -491,9 +516,9 @@ taccl_result_t launch(const Algo* a, const Geometry& G, taccl_dtype_t dtype, int
   // streamed messages (plan.cpp mark_streamed): progress published every TACCL_PROG_STRIPES
   // stripes (default 2; 0 = off, A/B knob — like every knob it must match on all ranks). Off in
   // pull mode (nothing is pushed) and with TMA pushes (their stores complete asynchronously)
-  A.prog = (A.pull || A.tma == 2) ? 0 : (int)env_size("TACCL_PROG_STRIPES", 2);
+  A.prog = (A.pull || A.tma == 2) ? 0 : (int)knob(KN_PROG_STRIPES, 2);
   // warp-specialised pairs: warps of the send part (of 16; A/B knob, default half)
-  A.pair_send = 32 * (int)std::min<size_t>(15, std::max<size_t>(1, env_size("TACCL_PAIR_SEND_WARPS", 8)));
+  A.pair_send = 32 * (int)std::min<size_t>(15, std::max<size_t>(1, knob(KN_PAIR_SEND_WARPS, 8)));
   std::string err;
   const int dyn = (A.plan_smem ? smem : 0) + (A.staged || !A.tma ? 0 : kTmaBytes);
   if (launch_executor(A, cta, dyn, stream, &err)) return fail(TACCL_ERR_CUDA, err);
@@ -904,6 +929,7 @@ taccl_result_t taccl_pool_alloc(size_t bytes, void** ptr) {
 
 taccl_result_t taccl_load_algo(const char* text, size_t len, taccl_algo_t* out) {
   if (!g.up) return fail(TACCL_ERR_NOT_INITIALIZED, "no communicator");
+  refresh_knobs();
   if (!text) return fail(TACCL_ERR_INVALID_ARG, "null text");
   std::unique_ptr<Algo> a(new Algo);
   std::vector<RankPlan> plans, plans_ll, plans_pc;
