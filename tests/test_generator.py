@@ -257,3 +257,43 @@ def test_merged_schedules_compute_the_same_result():
         b = oracle.run(oracle.parse(generate(coll, algo, n, p, 1, merge=False)), ins, "int32")
         assert all(np.array_equal(x, y) for x, y in zip(a, b))
         assert all(np.array_equal(x, y) for x, y in zip(a, oracle.expected_outputs(coll, ins, "int32")))
+
+
+def test_rounds_variant_orders_sends_by_round():
+    # generate(..., "rounds"): the split all-pairs schedule where the send of round d waits for
+    # the receive of round d - 1 (both validators accept it; deps only on this rank's receives)
+    import re
+    from paper_2111_04867_b200 import taccl
+    for coll, n in (("alltoall", 4), ("allgather", 8)):
+        text = generate(coll, "rounds", n, 1, 1)
+        assert oracle.validate(text).ok and taccl.validate(text, True)[0]
+        for r in range(n):
+            body = text[text.index(f'<gpu id="{r}"'):]
+            body = body[:body.index("</gpu>")]
+            recv_tb = {int(b): int(a) for a, b in re.findall(r'<tb id="(\d+)" send="-1" recv="(\d+)"', body)}
+            for t, peer, deps in re.findall(r'<tb id="(\d+)" send="(\d+)" recv="-1"[^>]*>\s*<step s="0" type="s"[^>]*deps="([^"]*)"', body):
+                d = (int(peer) - r) % n
+                want = "" if d < 2 else f"{recv_tb[(r - (d - 1)) % n]}:0"
+                assert deps == want, (coll, r, t, deps, want)
+
+
+def test_default_sets_use_the_measured_variants():
+    # generator/tuned.py choices pinned to the measurements they cite (profiles/r02_*):
+    # overlap pairs for RS n=4 bf16 from 80 MiB and AR n=4 from 64 MiB, the streamed split RS at
+    # n=2 from 256 MiB, the fp32 ring RS up to 512 MiB
+    from paper_2111_04867_b200.generator.tuned import ranges
+    MiB = 1 << 20
+
+    def pick(coll, n, S, dt):
+        return next(r[0] for r in ranges(coll, n) if r[1] <= S < r[2] and (len(r) == 3 or dt in r[3]))
+    assert pick("reducescatter", 4, 64 * MiB, "bfloat16") == "direct"
+    assert pick("reducescatter", 4, 80 * MiB, "bfloat16") == "direct_ovl"
+    assert pick("reducescatter", 4, 256 * MiB, "float32") == "ring"
+    assert pick("reducescatter", 4, 512 * MiB, "float32") == "direct_ovl"
+    assert pick("reducescatter", 2, 128 * MiB, "bfloat16") == "direct"
+    assert pick("reducescatter", 2, 256 * MiB, "bfloat16") == "direct_split"
+    assert pick("allreduce", 4, 32 * MiB, "bfloat16") == "direct"
+    assert pick("allreduce", 4, 64 * MiB, "bfloat16") == "direct_ovl"
+    assert pick("allreduce", 4, 256 * MiB, "bfloat16") == "dring_ovl"
+    assert pick("allreduce", 4, 128 * MiB, "int32") == "dring_ovl"
+    assert 'overlap="1"' in generate("reducescatter", "direct", 4, 1, 1, overlap=True)
